@@ -1,0 +1,1121 @@
+// es_workflow.cu -- device-resident EsWorkflow behind the C ABI
+// (include/evorl_b200.h).  Host orchestration of one generation
+// (proj/src/workflow_es.cpp:87-172):
+//
+//   step_key k = fold_in(fold_in(rng, 0), iteration)
+//   ask  (implicit: perturbations regenerated in-kernel from fold_in(k, 0))
+//   rollout of agents [a0, a1) keyed fold_in(k, 1)          -> K2 rollout
+//   fitness reduction                                       -> k_fitness
+//   [caller all-gathers fitness across ranks]               (C1)
+//   RunningStats merge + rs_update (ARS)                    -> k_rs_update
+//   ranks / elites                                          -> k_rank
+//   tell on coordinates [p0, p1) (+ Adam for OpenES)        -> K4 tell
+//   [caller all-gathers mean slices across ranks]           (C2)
+//
+// Nothing on this path runs on the CPU except key derivation (two Threefry
+// blocks per generation) and launch orchestration; there is no CPU fallback:
+// a missing device or a failed launch is an EVORL_E_CUDA error.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/evorl_b200.h"
+#include "kernels.cuh"
+
+using namespace evorl_b200;
+
+namespace evorl_b200 {
+long long kernel_launch_count();
+}
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return set_err(EVORL_E_CUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(_e), \
+                     __FILE__, __LINE__, #call);                                        \
+  } while (0)
+
+extern "C" const char* evorl_last_error(void) { return g_err.c_str(); }
+extern "C" int evorl_abi_version(void) { return EVORL_B200_ABI_VERSION; }
+extern "C" int64_t evorl_kernel_launches(void) { return kernel_launch_count(); }
+
+static DKey mk(uint64_t hi, uint64_t lo) { return DKey{hi, lo}; }
+
+// -------------------------------------------------------- spec builders
+static EnvDesc make_env(int env_id, int fixed_horizon, int max_steps) {
+  EnvDesc e{};
+  e.id = env_id;
+  if (env_id == ENV_CARTPOLE) {  // EnvSpec::cartpole, proj/src/env.cpp:55-66
+    e.obs_dim = 4;
+    e.discrete = 1;
+    e.num_actions = 2;
+    e.act_dim = 1;
+    e.act_low = 0.0;
+    e.act_high = 0.0;
+    e.max_episode_steps = max_steps > 0 ? max_steps : 500;
+  } else {  // EnvSpec::pendulum, proj/src/env.cpp:68-81
+    e.obs_dim = 3;
+    e.discrete = 0;
+    e.num_actions = 0;
+    e.act_dim = 1;
+    e.act_low = -2.0;
+    e.act_high = 2.0;
+    e.max_episode_steps = max_steps > 0 ? max_steps : 200;
+  }
+  e.fixed_horizon = fixed_horizon;
+  return e;
+}
+
+// param_layout (proj/src/net.cpp:26-48) without layer norm / logstd.
+static int make_net(const evorl_mlp_desc& m, NetDesc* out) {
+  if (m.layer_norm)
+    return set_err(EVORL_E_UNSUPPORTED, "net.layer_norm is not supported on the B200 device path");
+  if (m.n_hidden <= 0 && !m.allow_linear) return set_err(EVORL_E_INVALID_ARGUMENT, "MlpSpec.hidden must be nonempty");
+  if (m.n_hidden > EVORL_MAX_HIDDEN) return set_err(EVORL_E_INVALID_ARGUMENT, "too many hidden layers");
+  if (m.head == EVORL_HEAD_GAUSSIAN)
+    return set_err(EVORL_E_UNSUPPORTED, "Gaussian head is not on the ES path");
+  NetDesc n{};
+  n.nlayers = m.n_hidden + 1;
+  n.dims[0] = m.input_dim;
+  for (int i = 0; i < m.n_hidden; ++i) n.dims[i + 1] = m.hidden[i];
+  n.dims[n.nlayers] = m.output_dim;
+  long long off = 0;
+  for (int l = 0; l < n.nlayers; ++l) {
+    n.w_off[l] = off;
+    off += (long long)n.dims[l] * n.dims[l + 1];
+    n.b_off[l] = off;
+    off += n.dims[l + 1];
+  }
+  n.d = off;
+  n.head = m.head;
+  n.tanh_scale = m.tanh_scale;
+  *out = n;
+  return EVORL_OK;
+}
+
+// policy_net_spec (proj/src/workflow.cpp:87-101)
+static evorl_mlp_desc policy_net(const EnvDesc& env, const int* hidden, int nh, int allow_linear) {
+  evorl_mlp_desc m{};
+  m.input_dim = env.obs_dim;
+  m.n_hidden = nh;
+  for (int i = 0; i < nh && i < EVORL_MAX_HIDDEN; ++i) m.hidden[i] = hidden[i];
+  m.allow_linear = allow_linear;
+  if (env.discrete) {
+    m.output_dim = env.num_actions;
+    m.head = EVORL_HEAD_CATEGORICAL;
+    m.tanh_scale = 1.0;
+  } else {
+    m.output_dim = env.act_dim;
+    m.head = EVORL_HEAD_TANH;
+    m.tanh_scale = env.act_high;
+  }
+  return m;
+}
+
+static int fault_to_error(unsigned long long code) {
+  const unsigned kind = (unsigned)((code >> 4) & 15u);
+  const unsigned layer = (unsigned)(code & 15u);
+  // EnvFault from batched_step inside rollout_lane always carries "[lane 0]"
+  // (proj/src/env.cpp:170-172 with a one-state batch, proj/src/rollout.cpp:131)
+  switch (kind) {
+    case FAULT_ENV_STATE:
+      return set_err(EVORL_E_ENV_FAULT, "env_step: non-finite state value (numeric divergence) [lane 0]");
+    case FAULT_ENV_ACTION:
+      return set_err(EVORL_E_ENV_FAULT, "env_step: non-finite action value (numeric divergence) [lane 0]");
+    case FAULT_ENV_SUCCESSOR:
+      return set_err(EVORL_E_ENV_FAULT,
+                     "env_step: non-finite successor state (numeric divergence) [lane 0]");
+    default:
+      return set_err(EVORL_E_NET_FAULT, "forward: non-finite activations at layer %u", layer);
+  }
+}
+
+// ------------------------------------------------------------ the handle
+struct Pinned {
+  double metrics[3];
+  unsigned long long steps;
+  unsigned long long fault;
+  ArsSel sel;
+  double eval[2];
+};
+
+struct evorl_es {
+  evorl_es_config cfg{};
+  EnvDesc env{};
+  NetDesc net{};
+  int norm_mode = 0;
+  long long d = 0;
+  int e = 1, count = 1;
+  SmemPlan plan{};
+  int groups = 1;
+  cudaStream_t stream = nullptr;
+  // WorkflowState (proj/include/evorl/workflow.hpp:31-36)
+  DKey rng{};
+  long long iteration = 0, env_steps = 0, episodes = 0;
+  bool initialised = false;
+  // EsState on the device
+  double *d_mean = nullptr, *d_m = nullptr, *d_v = nullptr, *d_var = nullptr;
+  long long* d_t = nullptr;
+  long long adam_t_host = 0;
+  long long cem_iter = 0;
+  DevNorm* d_norm = nullptr;
+  NormParams* d_normp = nullptr;
+  // generation buffers
+  double *d_fitness = nullptr, *d_ep_returns = nullptr, *d_lane_stats = nullptr, *d_agent_stats = nullptr;
+  long long* d_lane_steps = nullptr;
+  int *d_rank = nullptr, *d_order = nullptr, *d_elite_idx = nullptr;
+  double *d_shaped = nullptr, *d_scores = nullptr, *d_elite_diff = nullptr, *d_metrics = nullptr;
+  ArsSel* d_sel = nullptr;
+  unsigned long long *d_steps = nullptr, *d_fault = nullptr;
+  double* d_adam_bc = nullptr;
+  long long adam_bc_len = 0;
+  double* d_ves_w = nullptr;
+  Pinned* h = nullptr;
+  // sharding
+  int rank = 0, world = 1, a0 = 0, a1 = 0;
+  long long p0 = 0, p1 = 0;
+  // timing
+  cudaEvent_t ev_r0 = nullptr, ev_r1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+  float last_rollout_ms = 0.f, last_step_ms = 0.f;
+  // per-step keys
+  DKey step_key{}, ask_key{}, rollout_key{};
+};
+
+extern "C" void evorl_es_default_config(evorl_es_config* c) {
+  // registry defaults, proj/src/config.cpp:23-70
+  std::memset(c, 0, sizeof *c);
+  c->algo = EVORL_ALGO_OPENES;
+  c->env_id = EVORL_ENV_CARTPOLE;
+  c->fixed_horizon = 0;
+  c->max_episode_steps = 0;
+  c->n_hidden = 2;
+  c->hidden[0] = 64;
+  c->hidden[1] = 64;
+  c->pop = 128;
+  c->fitness_episodes = 1;
+  c->obs_norm_mode = EVORL_NORM_AUTO;
+  c->vbn_samples = 10000;
+  c->openes_sigma = 0.02;
+  c->openes_lr = 0.01;
+  c->openes_weight_decay = 0.005;
+  c->openes_mirrored = 1;
+  c->openes_noise_table = 0;
+  c->openes_noise_table_size = 4194304;
+  c->ars_sigma = 0.03;
+  c->ars_lr = 0.02;
+  c->ars_elites = 16;
+  c->ves_sigma = 0.02;
+  c->ves_elites = 16;
+  c->ves_mirrored = 1;
+  c->cmaes_sigma0 = 0.1;
+  c->cmaes_elites = 64;
+  c->cmaes_max_dim = 4096;
+  c->cem_elites = 5;
+  c->cem_var_init = 1e-3;
+  c->cem_noise_start = 1e-3;
+  c->cem_noise_end = 1e-5;
+  c->cem_decay_iters = 2000;
+  c->precision = EVORL_PREC_F64;
+  c->device = 0;
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+  return cudaMalloc((void**)p, sizeof(T) * (n ? n : 1));
+}
+
+static void free_all(evorl_es* s) {
+  void* ptrs[] = {s->d_mean, s->d_m, s->d_v, s->d_var, s->d_t, s->d_norm, s->d_normp, s->d_fitness,
+                  s->d_ep_returns, s->d_lane_stats, s->d_agent_stats, s->d_lane_steps, s->d_rank,
+                  s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
+                  s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (s->h) cudaFreeHost(s->h);
+  for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1})
+    if (ev) cudaEventDestroy(ev);
+  if (s->stream) cudaStreamDestroy(s->stream);
+}
+
+static int resolve_norm(const evorl_es_config& c) {  // proj/src/workflow.cpp:131-144
+  if (c.obs_norm_mode >= 0) return c.obs_norm_mode;
+  if (c.algo == EVORL_ALGO_ARS) return EVORL_NORM_RS;
+  if (c.algo == EVORL_ALGO_CEM) return EVORL_NORM_NONE;
+  return EVORL_NORM_VBN;
+}
+
+extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
+  *out = nullptr;
+  if (cfg->algo < 0 || cfg->algo > EVORL_ALGO_CEM) return set_err(EVORL_E_CONFIG, "ec.algo: unknown algorithm");
+  if (cfg->env_id != EVORL_ENV_CARTPOLE && cfg->env_id != EVORL_ENV_PENDULUM)
+    return set_err(EVORL_E_INVALID_ARGUMENT, "unknown env id");
+  if (cfg->algo == EVORL_ALGO_CMAES)
+    return set_err(EVORL_E_UNSUPPORTED, "cmaes: device path not built in this revision");
+  if (cfg->algo == EVORL_ALGO_OPENES && cfg->openes_noise_table)
+    return set_err(EVORL_E_UNSUPPORTED, "openes noise_table mode: device path not built in this revision");
+  if (cfg->precision != EVORL_PREC_F64 && cfg->precision != EVORL_PREC_F32)
+    return set_err(EVORL_E_INVALID_ARGUMENT, "precision must be EVORL_PREC_F64 or EVORL_PREC_F32");
+  if (cfg->pop < 1 || cfg->fitness_episodes < 1)
+    return set_err(EVORL_E_INVALID_ARGUMENT, "ec.pop and ec.fitness_episodes must be positive");
+  auto* s = new evorl_es();
+  s->cfg = *cfg;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    delete s;
+    return set_err(EVORL_E_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  if (cudaSetDevice(cfg->device) != cudaSuccess) {
+    delete s;
+    return set_err(EVORL_E_CUDA, "cudaSetDevice(%d) failed", cfg->device);
+  }
+  s->env = make_env(cfg->env_id, cfg->fixed_horizon, cfg->max_episode_steps);
+  const evorl_mlp_desc md = policy_net(s->env, cfg->hidden, cfg->n_hidden, cfg->allow_linear);
+  int rc = make_net(md, &s->net);
+  if (rc) {
+    delete s;
+    return rc;
+  }
+  s->d = s->net.d;
+  s->norm_mode = resolve_norm(*cfg);
+  s->e = cfg->fitness_episodes;
+  s->count = cfg->fitness_episodes;  // RolloutMode::episodes(fitness_episodes)
+  if (!plan_rollout(s->net, s->env.obs_dim, s->e, cfg->precision, &s->plan)) {
+    delete s;
+    return set_err(EVORL_E_UNSUPPORTED, "policy too large for a shared-memory resident team");
+  }
+  s->groups = (s->e + s->plan.ET - 1) / s->plan.ET;
+  s->a0 = 0;
+  s->a1 = cfg->pop;
+  s->p0 = 0;
+  s->p1 = s->d;
+  const int n = cfg->pop;
+  const long long d = s->d;
+#define A(call)                \
+  do {                         \
+    cudaError_t _e = (call);   \
+    if (_e != cudaSuccess) {   \
+      free_all(s);             \
+      delete s;                \
+      return set_err(EVORL_E_CUDA, "allocation failed: %s", cudaGetErrorString(_e)); \
+    }                          \
+  } while (0)
+  A(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  A(dalloc(&s->d_mean, d));
+  A(dalloc(&s->d_m, d));
+  A(dalloc(&s->d_v, d));
+  A(dalloc(&s->d_var, d));
+  A(dalloc(&s->d_t, 1));
+  A(dalloc(&s->d_norm, 1));
+  A(dalloc(&s->d_normp, 1));
+  A(dalloc(&s->d_fitness, n));
+  A(dalloc(&s->d_ep_returns, (size_t)n * s->count));
+  A(dalloc(&s->d_lane_stats, (size_t)n * s->e * 9));
+  A(dalloc(&s->d_agent_stats, (size_t)n * 9));
+  A(dalloc(&s->d_lane_steps, (size_t)n * s->e));
+  A(dalloc(&s->d_rank, n));
+  A(dalloc(&s->d_order, n));
+  A(dalloc(&s->d_elite_idx, n));
+  A(dalloc(&s->d_shaped, n));
+  A(dalloc(&s->d_scores, n));
+  A(dalloc(&s->d_elite_diff, n));
+  A(dalloc(&s->d_metrics, 4));
+  A(dalloc(&s->d_sel, 1));
+  A(dalloc(&s->d_steps, 1));
+  A(dalloc(&s->d_fault, 1));
+  A(cudaMallocHost((void**)&s->h, sizeof(Pinned)));
+  A(cudaEventCreate(&s->ev_r0));
+  A(cudaEventCreate(&s->ev_r1));
+  A(cudaEventCreate(&s->ev_s0));
+  A(cudaEventCreate(&s->ev_s1));
+  // Adam bias corrections 1 - beta^t with the host libm pow (the reference's
+  // std::pow, proj/src/optim.cpp:12-13), t = 1..65536.
+  s->adam_bc_len = 65536;
+  std::vector<double> bc(2 * s->adam_bc_len);
+  for (long long t = 1; t <= s->adam_bc_len; ++t) {
+    bc[2 * (t - 1)] = 1.0 - std::pow(0.9, (double)t);
+    bc[2 * (t - 1) + 1] = 1.0 - std::pow(0.999, (double)t);
+  }
+  A(dalloc(&s->d_adam_bc, bc.size()));
+  A(cudaMemcpy(s->d_adam_bc, bc.data(), sizeof(double) * bc.size(), cudaMemcpyHostToDevice));
+  if (cfg->algo == EVORL_ALGO_VES) {  // canonical_es_weights (proj/src/ec.cpp:158-162)
+    const int mu = std::min(cfg->ves_elites, n);
+    std::vector<double> w(mu);
+    double sum = 0.0;
+    for (int i = 0; i < mu; ++i) {
+      w[i] = std::log(mu + 0.5) - std::log(i + 1.0);
+      sum += w[i];
+    }
+    for (auto& x : w) x /= sum;
+    A(dalloc(&s->d_ves_w, mu));
+    A(cudaMemcpy(s->d_ves_w, w.data(), sizeof(double) * mu, cudaMemcpyHostToDevice));
+  }
+#undef A
+  *out = s;
+  return EVORL_OK;
+}
+
+extern "C" void evorl_es_destroy(evorl_es* s) {
+  if (!s) return;
+  cudaSetDevice(s->cfg.device);
+  cudaStreamSynchronize(s->stream);
+  free_all(s);
+  delete s;
+}
+
+extern "C" int64_t evorl_es_dim(const evorl_es* s) { return s->d; }
+
+static DKey init_key(DKey run, uint64_t i) { return fold_in(fold_in(run, 2), i); }
+
+// EsWorkflow::init (proj/src/workflow_es.cpp:68-85)
+extern "C" int evorl_es_init(evorl_es* s, uint64_t key_hi, uint64_t key_lo) {
+  CK(cudaSetDevice(s->cfg.device));
+  const DKey key = mk(key_hi, key_lo);
+  s->rng = key;
+  s->iteration = s->env_steps = s->episodes = 0;
+  s->adam_t_host = 0;
+  s->cem_iter = 0;
+  CK(run_init_params(s->net, init_key(key, 1), s->d_mean, s->stream));
+  CK(cudaMemsetAsync(s->d_m, 0, sizeof(double) * s->d, s->stream));
+  CK(cudaMemsetAsync(s->d_v, 0, sizeof(double) * s->d, s->stream));
+  CK(cudaMemsetAsync(s->d_t, 0, sizeof(long long), s->stream));
+  if (s->cfg.algo == EVORL_ALGO_CEM) {
+    std::vector<double> v(s->d, s->cfg.cem_var_init);
+    CK(cudaMemcpyAsync(s->d_var, v.data(), sizeof(double) * s->d, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  }
+  DevNorm nm{};
+  nm.mode = s->norm_mode;
+  nm.dim = s->env.obs_dim;
+  if (s->norm_mode == EVORL_NORM_VBN) {
+    CK(run_vbn_fit(s->env, init_key(key, 0), s->cfg.vbn_samples, s->d_norm, s->d_normp, s->stream));
+  } else {
+    if (s->norm_mode == EVORL_NORM_RS)  // ObsNormState::running_stats
+      for (int i = 0; i < nm.dim; ++i) {
+        nm.mean[i] = 0.0;
+        nm.var[i] = 1.0;
+      }
+    CK(cudaMemcpyAsync(s->d_norm, &nm, sizeof nm, cudaMemcpyHostToDevice, s->stream));
+    CK(run_norm_params(s->d_norm, s->d_normp, s->stream));
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  s->initialised = true;
+  return EVORL_OK;
+}
+
+static ParamDesc param_desc(const evorl_es* s) {
+  ParamDesc p{};
+  p.mean = s->d_mean;
+  p.ask_key = s->ask_key;
+  switch (s->cfg.algo) {
+    case EVORL_ALGO_OPENES:
+      p.src = SRC_OPENES;
+      p.sigma = s->cfg.openes_sigma;
+      p.mirrored = s->cfg.openes_mirrored;
+      p.base = p.mirrored ? s->cfg.pop / 2 : s->cfg.pop;
+      break;
+    case EVORL_ALGO_VES:
+      p.src = SRC_OPENES;
+      p.sigma = s->cfg.ves_sigma;
+      p.mirrored = s->cfg.ves_mirrored;
+      p.base = p.mirrored ? s->cfg.pop / 2 : s->cfg.pop;
+      break;
+    case EVORL_ALGO_ARS:
+      p.src = SRC_ARS;
+      p.sigma = s->cfg.ars_sigma;
+      break;
+    case EVORL_ALGO_CEM:
+      p.src = SRC_CEM;
+      p.var = s->d_var;
+      break;
+  }
+  return p;
+}
+
+static int check_ask(const evorl_es* s) {  // the ask-side argument checks
+  const int n = s->cfg.pop;
+  switch (s->cfg.algo) {
+    case EVORL_ALGO_OPENES:
+      if (n < 2) return set_err(EVORL_E_INVALID_ARGUMENT, "openes_ask: population must be at least 2");
+      if (s->cfg.openes_mirrored && n % 2)
+        return set_err(EVORL_E_INVALID_ARGUMENT, "openes_ask: mirrored sampling needs an even population");
+      break;
+    case EVORL_ALGO_ARS:
+      if (n < 2 || n % 2) return set_err(EVORL_E_INVALID_ARGUMENT, "ars_ask: population must be even");
+      break;
+    case EVORL_ALGO_VES:
+      if (n < 2) return set_err(EVORL_E_INVALID_ARGUMENT, "ves_ask: population must be at least 2");
+      if (s->cfg.ves_mirrored && n % 2)
+        return set_err(EVORL_E_INVALID_ARGUMENT, "ves_ask: mirrored sampling needs an even population");
+      break;
+  }
+  return EVORL_OK;
+}
+
+static RolloutArgs rollout_args(const evorl_es* s) {
+  RolloutArgs a{};
+  a.env = s->env;
+  a.net = s->net;
+  a.par = param_desc(s);
+  a.plan = s->plan;
+  a.norm = s->d_normp;
+  a.n_agents = s->a1 - s->a0;
+  a.agent_offset = s->a0;
+  a.e = s->e;
+  a.count = s->count;
+  a.groups = s->groups;
+  a.rollout_key = s->rollout_key;
+  a.track_stats = s->norm_mode == EVORL_NORM_RS;
+  const int per_lane = (s->count + s->e - 1) / s->e;
+  a.max_iters = per_lane * s->env.max_episode_steps + 1;
+  a.ep_returns = s->d_ep_returns + (long long)s->a0 * s->count;
+  a.ep_lengths = nullptr;
+  a.lane_steps = s->d_lane_steps + (long long)s->a0 * s->e;
+  a.lane_stats = s->d_lane_stats + (long long)s->a0 * s->e * 9;
+  a.fault = s->d_fault;
+  return a;
+}
+
+// ask + rollout + fitness of agents [a0, a1)
+extern "C" int evorl_es_phase_rollout(evorl_es* s) {
+  if (!s->initialised) return set_err(EVORL_E_INVALID_ARGUMENT, "evorl_es_step before evorl_es_init");
+  CK(cudaSetDevice(s->cfg.device));
+  int rc = check_ask(s);
+  if (rc) return rc;
+  // WorkflowState::step_key (proj/include/evorl/workflow.hpp:41)
+  s->step_key = fold_in(fold_in(s->rng, 0), (uint64_t)s->iteration);
+  s->ask_key = fold_in(s->step_key, 0);      // proj/src/workflow_es.cpp:94
+  s->rollout_key = fold_in(s->step_key, 1);  // proj/src/workflow_es.cpp:125
+  CK(cudaEventRecord(s->ev_s0, s->stream));
+  CK(cudaMemsetAsync(s->d_steps, 0, sizeof(unsigned long long), s->stream));
+  CK(cudaMemsetAsync(s->d_fault, 0xFF, sizeof(unsigned long long), s->stream));
+  const RolloutArgs a = rollout_args(s);
+  CK(cudaEventRecord(s->ev_r0, s->stream));
+  CK(launch_rollout(a, s->cfg.precision, s->stream));
+  count_launch();
+  CK(cudaEventRecord(s->ev_r1, s->stream));
+  CK(run_fitness(a.ep_returns, s->count, a.n_agents, s->a0, s->d_fitness, a.lane_steps, s->e, s->d_steps,
+                 s->stream));
+  CK(cudaMemcpyAsync(&s->h->steps, s->d_steps, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(&s->h->fault, s->d_fault, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (s->h->fault != ~0ull) return fault_to_error(s->h->fault);
+  return EVORL_OK;
+}
+
+static double cem_floor(const evorl_es* s) {  // CemState::noise_floor, proj/src/ec.cpp:292-298
+  const double frac = s->cfg.cem_decay_iters > 0
+                          ? std::min(1.0, (double)s->cem_iter / (double)s->cfg.cem_decay_iters)
+                          : 1.0;
+  return s->cfg.cem_noise_start * std::pow(s->cfg.cem_noise_end / s->cfg.cem_noise_start, frac);
+}
+
+// ranks + tell on [p0, p1) + metrics; expects the full fitness vector.
+extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
+  CK(cudaSetDevice(s->cfg.device));
+  const int n = s->cfg.pop;
+  const cudaStream_t st = s->stream;
+  if (s->norm_mode == EVORL_NORM_RS)  // proj/src/workflow_es.cpp:136-138
+    CK(run_rs_merge(s->d_lane_stats, n, s->e, s->d_norm, s->d_normp, s->d_agent_stats, st));
+  double sigma = 0.0;
+  bool ars = false;
+  switch (s->cfg.algo) {
+    case EVORL_ALGO_OPENES: {
+      CK(run_rank(s->d_fitness, n, 0, s->d_rank, st));
+      CK(run_shaped_from_rank(s->d_rank, n, s->d_shaped, st));
+      OpenEsTellArgs t{};
+      t.mean = s->d_mean;
+      t.m = s->d_m;
+      t.v = s->d_v;
+      t.t_dev = s->d_t;
+      t.d = s->d;
+      t.p0 = s->p0;
+      t.p1 = s->p1;
+      t.sigma = s->cfg.openes_sigma;
+      t.lr = s->cfg.openes_lr;
+      t.weight_decay = s->cfg.openes_weight_decay;
+      t.lrwd = s->cfg.openes_lr * s->cfg.openes_weight_decay;
+      t.beta1 = 0.9;
+      t.beta2 = 0.999;
+      t.omb1 = 1.0 - 0.9;
+      t.omb2 = 1.0 - 0.999;
+      t.eps = 1e-8;
+      t.n = n;
+      t.mirrored = s->cfg.openes_mirrored;
+      t.base = t.mirrored ? n / 2 : n;
+      t.ask_key = s->ask_key;
+      t.shaped = s->d_shaped;
+      t.adam_bc = s->d_adam_bc;
+      t.adam_bc_len = s->adam_bc_len;
+      CK(run_openes_tell(t, st));
+      CK(run_inc_counter(s->d_t, st));
+      s->adam_t_host += 1;
+      sigma = s->cfg.openes_sigma;
+      break;
+    }
+    case EVORL_ALGO_ARS: {
+      const int half = n / 2;
+      CK(run_ars_scores(s->d_fitness, half, s->d_scores, st));
+      CK(run_rank(s->d_scores, half, 1, s->d_rank, st));
+      CK(run_ars_select(s->d_fitness, s->d_rank, half, s->cfg.ars_elites, s->cfg.ars_lr, s->d_elite_idx,
+                        s->d_elite_diff, s->d_sel, st));
+      CK(run_ars_update(s->d_mean, s->d, s->p0, s->p1, s->ask_key, s->d_elite_idx, s->d_elite_diff, s->d_sel,
+                        st));
+      CK(cudaMemcpyAsync(&s->h->sel, s->d_sel, sizeof(ArsSel), cudaMemcpyDeviceToHost, st));
+      sigma = s->cfg.ars_sigma;
+      ars = true;
+      break;
+    }
+    case EVORL_ALGO_VES: {
+      CK(run_rank(s->d_fitness, n, 1, s->d_rank, st));
+      CK(run_order_from_rank(s->d_rank, n, s->d_order, st));
+      const int mu = std::min(s->cfg.ves_elites, n);
+      const int base = s->cfg.ves_mirrored ? n / 2 : n;
+      CK(run_ves_tell(s->d_mean, s->d, s->p0, s->p1, s->cfg.ves_sigma, s->cfg.ves_mirrored, base,
+                      s->ask_key, s->d_order, s->d_ves_w, mu, st));
+      sigma = s->cfg.ves_sigma;
+      break;
+    }
+    case EVORL_ALGO_CEM: {
+      CK(run_rank(s->d_fitness, n, 1, s->d_rank, st));
+      CK(run_order_from_rank(s->d_rank, n, s->d_order, st));
+      const int h = std::min(s->cfg.cem_elites, n);
+      CK(run_cem_tell(s->d_mean, s->d_var, s->d, s->p0, s->p1, s->ask_key, s->d_order, h, cem_floor(s), st));
+      s->cem_iter += 1;
+      break;
+    }
+  }
+  CK(run_metrics(s->d_fitness, n, s->d_metrics, st));
+  CK(cudaMemcpyAsync(s->h->metrics, s->d_metrics, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(s->ev_s1, st));
+  CK(cudaStreamSynchronize(st));
+  if (s->cfg.algo == EVORL_ALGO_CEM) {  // es/sigma = sqrt(diag_var.mean()) (proj/src/workflow_es.cpp:162)
+    std::vector<double> v(s->d);
+    CK(cudaMemcpy(v.data(), s->d_var, sizeof(double) * s->d, cudaMemcpyDeviceToHost));
+    double acc = 0.0;
+    for (double x : v) acc += x;
+    sigma = std::sqrt(acc / (double)s->d);
+  }
+  cudaEventElapsedTime(&s->last_rollout_ms, s->ev_r0, s->ev_r1);
+  cudaEventElapsedTime(&s->last_step_ms, s->ev_s0, s->ev_s1);
+  s->env_steps += (long long)s->h->steps;
+  s->episodes += (long long)n * s->count;
+  s->iteration += 1;
+  if (out) {
+    out->fitness_mean = s->h->metrics[0];
+    out->fitness_max = s->h->metrics[1];
+    out->fitness_min = s->h->metrics[2];
+    out->sigma = sigma;
+    out->update_skipped = ars && s->h->sel.skipped ? 1.0 : 0.0;
+  }
+  return EVORL_OK;
+}
+
+// Workflow::step on one GPU: both phases with the full ranges.
+extern "C" int evorl_es_step(evorl_es* s, evorl_step_metrics* out) {
+  if (s->world != 1) return set_err(EVORL_E_INVALID_ARGUMENT, "sharded handle: use the phase API");
+  int rc = evorl_es_phase_rollout(s);
+  if (rc) return rc;
+  return evorl_es_phase_tell(s, out);
+}
+
+extern "C" int evorl_es_set_shard(evorl_es* s, int32_t rank, int32_t world) {
+  if (world < 1 || rank < 0 || rank >= world) return set_err(EVORL_E_INVALID_ARGUMENT, "bad shard");
+  const int n = s->cfg.pop;
+  // Contiguous agent blocks; for mirrored OpenES the block boundary keeps
+  // pairs (i, i+base) on... every rank regenerates its own noise rows, so no
+  // pairing constraint is needed for correctness.
+  s->rank = rank;
+  s->world = world;
+  s->a0 = (int)((long long)n * rank / world);
+  s->a1 = (int)((long long)n * (rank + 1) / world);
+  s->p0 = s->d * rank / world;
+  s->p1 = s->d * (rank + 1) / world;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_es_shard_ranges(const evorl_es* s, int32_t* a0, int32_t* a1, int64_t* p0, int64_t* p1) {
+  *a0 = s->a0;
+  *a1 = s->a1;
+  *p0 = s->p0;
+  *p1 = s->p1;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_es_device_buffers(evorl_es* s, void** fitness, void** mean, void** lane_stats) {
+  if (fitness) *fitness = s->d_fitness;
+  if (mean) *mean = s->d_mean;
+  if (lane_stats) *lane_stats = s->d_lane_stats;
+  return EVORL_OK;
+}
+extern "C" void* evorl_es_stream(evorl_es* s) { return (void*)s->stream; }
+
+extern "C" int evorl_es_last_timings(const evorl_es* s, float* rollout_ms, float* step_ms) {
+  if (rollout_ms) *rollout_ms = s->last_rollout_ms;
+  if (step_ms) *step_ms = s->last_step_ms;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_es_counters(const evorl_es* s, int64_t* it, int64_t* steps, int64_t* eps) {
+  if (it) *it = s->iteration;
+  if (steps) *steps = s->env_steps;
+  if (eps) *eps = s->episodes;
+  return EVORL_OK;
+}
+extern "C" int evorl_es_set_counters(evorl_es* s, int64_t it, int64_t steps, int64_t eps) {
+  s->iteration = it;
+  s->env_steps = steps;
+  s->episodes = eps;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_es_get_mean(evorl_es* s, double* mean) {
+  CK(cudaSetDevice(s->cfg.device));
+  CK(cudaMemcpyAsync(mean, s->d_mean, sizeof(double) * s->d, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return EVORL_OK;
+}
+extern "C" int evorl_es_set_mean(evorl_es* s, const double* mean) {
+  CK(cudaSetDevice(s->cfg.device));
+  CK(cudaMemcpyAsync(s->d_mean, mean, sizeof(double) * s->d, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return EVORL_OK;
+}
+extern "C" int evorl_es_get_adam(evorl_es* s, double* m, double* v, int64_t* t) {
+  CK(cudaSetDevice(s->cfg.device));
+  if (m) CK(cudaMemcpyAsync(m, s->d_m, sizeof(double) * s->d, cudaMemcpyDeviceToHost, s->stream));
+  if (v) CK(cudaMemcpyAsync(v, s->d_v, sizeof(double) * s->d, cudaMemcpyDeviceToHost, s->stream));
+  long long tt = 0;
+  CK(cudaMemcpyAsync(&tt, s->d_t, sizeof tt, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (t) *t = tt;
+  return EVORL_OK;
+}
+extern "C" int evorl_es_set_adam(evorl_es* s, const double* m, const double* v, int64_t t) {
+  CK(cudaSetDevice(s->cfg.device));
+  long long tt = t;
+  CK(cudaMemcpyAsync(s->d_m, m, sizeof(double) * s->d, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(s->d_v, v, sizeof(double) * s->d, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(s->d_t, &tt, sizeof tt, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  s->adam_t_host = t;
+  return EVORL_OK;
+}
+extern "C" int evorl_es_get_fitness(evorl_es* s, double* f) {
+  CK(cudaSetDevice(s->cfg.device));
+  CK(cudaMemcpyAsync(f, s->d_fitness, sizeof(double) * s->cfg.pop, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return EVORL_OK;
+}
+extern "C" int evorl_es_get_obs_norm(evorl_es* s, evorl_obs_norm* o) {
+  CK(cudaSetDevice(s->cfg.device));
+  DevNorm nm{};
+  CK(cudaMemcpyAsync(&nm, s->d_norm, sizeof nm, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  o->mode = nm.mode;
+  o->dim = nm.dim;
+  for (int i = 0; i < 4; ++i) {
+    o->mean[i] = nm.mean[i];
+    o->var[i] = nm.var[i];
+  }
+  o->count = nm.count;
+  return EVORL_OK;
+}
+extern "C" int evorl_es_set_obs_norm(evorl_es* s, const evorl_obs_norm* o) {
+  CK(cudaSetDevice(s->cfg.device));
+  DevNorm nm{};
+  nm.mode = o->mode;
+  nm.dim = o->dim;
+  for (int i = 0; i < 4; ++i) {
+    nm.mean[i] = o->mean[i];
+    nm.var[i] = o->var[i];
+  }
+  nm.count = o->count;
+  CK(cudaMemcpyAsync(s->d_norm, &nm, sizeof nm, cudaMemcpyHostToDevice, s->stream));
+  CK(run_norm_params(s->d_norm, s->d_normp, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return EVORL_OK;
+}
+
+// Workflow::evaluate -> eval_params(m=1, e=episodes) (proj/src/workflow.cpp:103-129)
+extern "C" int evorl_es_evaluate(evorl_es* s, int32_t episodes, uint64_t key_hi, uint64_t key_lo,
+                                 double* mean_return, double* return_std) {
+  CK(cudaSetDevice(s->cfg.device));
+  if (episodes < 1) return set_err(EVORL_E_INVALID_ARGUMENT, "episodes must be positive");
+  SmemPlan plan{};
+  if (!plan_rollout(s->net, s->env.obs_dim, episodes, s->cfg.precision, &plan))
+    return set_err(EVORL_E_UNSUPPORTED, "policy too large for a shared-memory resident team");
+  double* rets = nullptr;
+  long long* steps = nullptr;
+  double* out2 = nullptr;
+  CK(cudaMallocAsync((void**)&rets, sizeof(double) * episodes, s->stream));
+  CK(cudaMallocAsync((void**)&steps, sizeof(long long) * episodes, s->stream));
+  CK(cudaMallocAsync((void**)&out2, sizeof(double) * 2, s->stream));
+  CK(cudaMemsetAsync(s->d_fault, 0xFF, sizeof(unsigned long long), s->stream));
+  RolloutArgs a{};
+  a.env = s->env;
+  a.net = s->net;
+  a.par.src = SRC_EXPLICIT;
+  a.par.params = s->d_mean;
+  a.plan = plan;
+  a.norm = s->d_normp;
+  a.n_agents = 1;
+  a.agent_offset = 0;
+  a.e = episodes;
+  a.count = episodes;
+  a.groups = (episodes + plan.ET - 1) / plan.ET;
+  a.rollout_key = mk(key_hi, key_lo);
+  a.track_stats = 0;
+  a.max_iters = s->env.max_episode_steps + 1;
+  a.ep_returns = rets;
+  a.lane_steps = steps;
+  a.fault = s->d_fault;
+  CK(launch_rollout(a, s->cfg.precision, s->stream));
+  count_launch();
+  CK(run_eval_reduce(rets, episodes, out2, s->stream));
+  CK(cudaMemcpyAsync(s->h->eval, out2, sizeof(double) * 2, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(&s->h->fault, s->d_fault, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaFreeAsync(rets, s->stream));
+  CK(cudaFreeAsync(steps, s->stream));
+  CK(cudaFreeAsync(out2, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  if (s->h->fault != ~0ull) return fault_to_error(s->h->fault);
+  *mean_return = s->h->eval[0];
+  *return_std = s->h->eval[1];
+  return EVORL_OK;
+}
+
+// ================================================================ stateless
+// Scratch device buffers for the stateless (host-buffer) entry points.
+struct Scratch {
+  void* p = nullptr;
+  ~Scratch() {
+    if (p) cudaFree(p);
+  }
+};
+template <typename T>
+static int up(Scratch& s, const T* host, size_t n, T** dev) {
+  CK(cudaMalloc(&s.p, sizeof(T) * (n ? n : 1)));
+  *dev = (T*)s.p;
+  if (host && n) CK(cudaMemcpy(*dev, host, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return EVORL_OK;
+}
+static int ensure_device() {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+    return set_err(EVORL_E_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  return EVORL_OK;
+}
+#define DEV_OR_RETURN()        \
+  do {                         \
+    int _rc = ensure_device(); \
+    if (_rc) return _rc;       \
+  } while (0)
+
+extern "C" int evorl_threefry2x64(const uint64_t* keys, const uint64_t* ctrs, uint64_t* out, int64_t n) {
+  DEV_OR_RETURN();
+  if (n <= 0) return EVORL_OK;
+  Scratch a, b, c;
+  uint64_t *dk, *dc, *dout;
+  if (int rc = up(a, keys, 2 * n, &dk)) return rc;
+  if (int rc = up(b, ctrs, 2 * n, &dc)) return rc;
+  if (int rc = up(c, (const uint64_t*)nullptr, 2 * n, &dout)) return rc;
+  CK(run_threefry_batch(dk, dc, dout, n, 0));
+  CK(cudaMemcpy(out, dout, sizeof(uint64_t) * 2 * n, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_stream_words(uint64_t hi, uint64_t lo, int64_t first, int64_t n, uint64_t* out) {
+  DEV_OR_RETURN();
+  if (n <= 0) return EVORL_OK;
+  Scratch a;
+  uint64_t* d;
+  if (int rc = up(a, (const uint64_t*)nullptr, n, &d)) return rc;
+  CK(run_stream_words(mk(hi, lo), first, n, d, 0));
+  CK(cudaMemcpy(out, d, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_gaussian_matrix(uint64_t hi, uint64_t lo, int64_t rows, int64_t cols, double* out) {
+  DEV_OR_RETURN();
+  if (rows * cols <= 0) return EVORL_OK;
+  Scratch a;
+  double* d;
+  if (int rc = up(a, (const double*)nullptr, rows * cols, &d)) return rc;
+  CK(run_gaussian_matrix(mk(hi, lo), rows, cols, d, 0));
+  CK(cudaMemcpy(out, d, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_centered_ranks(const double* f, int64_t n, double* shaped) {
+  DEV_OR_RETURN();
+  if (n <= 0) return EVORL_OK;
+  Scratch a, b, c;
+  double *df, *ds;
+  int* dr;
+  if (int rc = up(a, f, n, &df)) return rc;
+  if (int rc = up(b, (const int*)nullptr, n, &dr)) return rc;
+  if (int rc = up(c, (const double*)nullptr, n, &ds)) return rc;
+  CK(run_rank(df, (int)n, 0, dr, 0));
+  CK(run_shaped_from_rank(dr, (int)n, ds, 0));
+  CK(cudaMemcpy(shaped, ds, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_rank_desc(const double* f, int64_t n, int32_t* order) {
+  DEV_OR_RETURN();
+  if (n <= 0) return EVORL_OK;
+  Scratch a, b, c;
+  double* df;
+  int *dr, *dord;
+  if (int rc = up(a, f, n, &df)) return rc;
+  if (int rc = up(b, (const int*)nullptr, n, &dr)) return rc;
+  if (int rc = up(c, (const int*)nullptr, n, &dord)) return rc;
+  CK(run_rank(df, (int)n, 1, dr, 0));
+  CK(run_order_from_rank(dr, (int)n, dord, 0));
+  CK(cudaMemcpy(order, dord, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_env_step_batch(int env_id, int fixed_horizon, int max_episode_steps, int64_t n,
+                                    double* phys, int32_t* step_count, const double* action, double* reward,
+                                    int32_t* terminated, int32_t* truncated, int32_t* fault) {
+  DEV_OR_RETURN();
+  if (n <= 0) return EVORL_OK;
+  const EnvDesc env = make_env(env_id, fixed_horizon, max_episode_steps);
+  Scratch a, b, c, d, e, f, g;
+  double *dp, *da, *dr;
+  int *dsc, *dt, *dtr, *df;
+  if (int rc = up(a, phys, 4 * n, &dp)) return rc;
+  if (int rc = up(b, step_count, n, &dsc)) return rc;
+  if (int rc = up(c, action, n, &da)) return rc;
+  if (int rc = up(d, (const double*)nullptr, n, &dr)) return rc;
+  if (int rc = up(e, (const int*)nullptr, n, &dt)) return rc;
+  if (int rc = up(f, (const int*)nullptr, n, &dtr)) return rc;
+  if (int rc = up(g, (const int*)nullptr, n, &df)) return rc;
+  CK(run_env_step_batch(env, n, dp, dsc, da, dr, dt, dtr, df, 0));
+  CK(cudaMemcpy(phys, dp, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(step_count, dsc, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(reward, dr, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(terminated, dt, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(truncated, dtr, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(fault, df, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp_desc* netd,
+                                     const evorl_obs_norm* norm, const double* params, int32_t m, int32_t e,
+                                     int32_t count, uint64_t key_hi, uint64_t key_lo, int32_t precision,
+                                     double* returns, int64_t* steps, double* obs_stats) {
+  DEV_OR_RETURN();
+  if (m <= 0) return EVORL_OK;
+  if (e < 1 || count < 0) return set_err(EVORL_E_INVALID_ARGUMENT, "envs_per_agent must be positive");
+  const EnvDesc env = make_env(envd->env_id, envd->fixed_horizon, envd->max_episode_steps);
+  NetDesc net{};
+  if (int rc = make_net(*netd, &net)) return rc;
+  if (netd->input_dim != env.obs_dim) return set_err(EVORL_E_INVALID_ARGUMENT, "net input_dim != obs_dim");
+  SmemPlan plan{};
+  if (!plan_rollout(net, env.obs_dim, e, precision, &plan))
+    return set_err(EVORL_E_UNSUPPORTED, "policy too large for a shared-memory resident team");
+  const long long d = net.d;
+  Scratch sp, sr, ss, sst, sag, sn, sf;
+  double *dparams, *drets, *dstats, *dagent;
+  long long* dsteps;
+  NormParams* dnorm = nullptr;
+  unsigned long long* dfault;
+  if (int rc = up(sp, params, (size_t)m * d, &dparams)) return rc;
+  if (int rc = up(sr, (const double*)nullptr, (size_t)m * std::max(count, 1), &drets)) return rc;
+  if (int rc = up(ss, (const long long*)nullptr, (size_t)m * e, &dsteps)) return rc;
+  if (int rc = up(sst, (const double*)nullptr, (size_t)m * e * 9, &dstats)) return rc;
+  if (int rc = up(sag, (const double*)nullptr, (size_t)m * 9, &dagent)) return rc;
+  if (int rc = up(sf, (const unsigned long long*)nullptr, 1, &dfault)) return rc;
+  if (norm && norm->mode != EVORL_NORM_NONE) {
+    NormParams np{};
+    np.active = norm->count != 0.0;
+    np.dim = norm->dim;
+    for (int i = 0; i < 4; ++i) {
+      np.mean[i] = norm->mean[i];
+      const double sd = std::sqrt(norm->var[i]);
+      np.den[i] = sd > 1e-8 ? sd : 1e-8;
+    }
+    if (int rc = up(sn, &np, 1, &dnorm)) return rc;
+  }
+  CK(cudaMemset(dfault, 0xFF, sizeof(unsigned long long)));
+  CK(cudaMemset(dstats, 0, sizeof(double) * m * e * 9));
+  RolloutArgs a{};
+  a.env = env;
+  a.net = net;
+  a.par.src = SRC_EXPLICIT;
+  a.par.params = dparams;
+  a.plan = plan;
+  a.norm = dnorm;
+  a.n_agents = m;
+  a.e = e;
+  a.count = count;
+  a.groups = (e + plan.ET - 1) / plan.ET;
+  a.rollout_key = mk(key_hi, key_lo);
+  a.track_stats = obs_stats != nullptr;
+  a.max_iters = ((count + e - 1) / e) * env.max_episode_steps + 1;
+  a.ep_returns = drets;
+  a.lane_steps = dsteps;
+  a.lane_stats = dstats;
+  a.fault = dfault;
+  CK(launch_rollout(a, precision, 0));
+  count_launch();
+  if (obs_stats) CK(run_agent_stats(dstats, m, e, dagent, 0));
+  CK(cudaDeviceSynchronize());
+  unsigned long long fault = 0;
+  CK(cudaMemcpy(&fault, dfault, sizeof fault, cudaMemcpyDeviceToHost));
+  if (fault != ~0ull) return fault_to_error(fault);
+  if (returns) CK(cudaMemcpy(returns, drets, sizeof(double) * m * count, cudaMemcpyDeviceToHost));
+  if (steps) {
+    std::vector<long long> ls((size_t)m * e);
+    CK(cudaMemcpy(ls.data(), dsteps, sizeof(long long) * m * e, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) {
+      long long acc = 0;
+      for (int j = 0; j < e; ++j) acc += ls[(size_t)i * e + j];
+      steps[i] = acc;
+    }
+  }
+  if (obs_stats) CK(cudaMemcpy(obs_stats, dagent, sizeof(double) * m * 9, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_openes_ask(const double* mean, int64_t d, double sigma, int32_t mirrored, uint64_t hi,
+                                uint64_t lo, int32_t n, double* cand, double* eps) {
+  DEV_OR_RETURN();
+  if (n < 2) return set_err(EVORL_E_INVALID_ARGUMENT, "openes_ask: population must be at least 2");
+  if (mirrored && n % 2)
+    return set_err(EVORL_E_INVALID_ARGUMENT, "openes_ask: mirrored sampling needs an even population");
+  Scratch a, b, c;
+  double *dm, *dc, *de;
+  if (int rc = up(a, mean, d, &dm)) return rc;
+  if (int rc = up(b, (const double*)nullptr, (size_t)n * d, &dc)) return rc;
+  if (int rc = up(c, (const double*)nullptr, (size_t)n * d, &de)) return rc;
+  CK(run_openes_ask(dm, d, sigma, mirrored, mk(hi, lo), n, dc, de, 0));
+  if (cand) CK(cudaMemcpy(cand, dc, sizeof(double) * n * d, cudaMemcpyDeviceToHost));
+  if (eps) CK(cudaMemcpy(eps, de, sizeof(double) * n * d, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_openes_tell(double* mean, double* m, double* v, int64_t* t, int64_t d, double sigma,
+                                 double lr, double wd, int32_t mirrored, uint64_t hi, uint64_t lo,
+                                 const double* fitness, int32_t n) {
+  DEV_OR_RETURN();
+  if (n < 1) return set_err(EVORL_E_INVALID_ARGUMENT, "openes_tell: eps/fitness size mismatch");
+  if (mirrored && n % 2)
+    return set_err(EVORL_E_INVALID_ARGUMENT, "openes_ask: mirrored sampling needs an even population");
+  Scratch a, b, c, f, r, sh, tt, bc;
+  double *dmean, *dm, *dv, *df, *dsh, *dbc;
+  int* dr;
+  long long* dt;
+  long long th = *t;
+  if (int rc = up(a, mean, d, &dmean)) return rc;
+  if (int rc = up(b, m, d, &dm)) return rc;
+  if (int rc = up(c, v, d, &dv)) return rc;
+  if (int rc = up(f, fitness, n, &df)) return rc;
+  if (int rc = up(r, (const int*)nullptr, n, &dr)) return rc;
+  if (int rc = up(sh, (const double*)nullptr, n, &dsh)) return rc;
+  if (int rc = up(tt, &th, 1, &dt)) return rc;
+  const double bch[2] = {1.0 - std::pow(0.9, (double)(th + 1)), 1.0 - std::pow(0.999, (double)(th + 1))};
+  if (int rc = up(bc, bch, 2, &dbc)) return rc;
+  CK(run_rank(df, n, 0, dr, 0));
+  CK(run_shaped_from_rank(dr, n, dsh, 0));
+  OpenEsTellArgs ta{};
+  ta.mean = dmean;
+  ta.m = dm;
+  ta.v = dv;
+  ta.t_dev = dt;
+  ta.d = d;
+  ta.p0 = 0;
+  ta.p1 = d;
+  ta.sigma = sigma;
+  ta.lr = lr;
+  ta.weight_decay = wd;
+  ta.lrwd = lr * wd;
+  ta.beta1 = 0.9;
+  ta.beta2 = 0.999;
+  ta.omb1 = 1.0 - 0.9;
+  ta.omb2 = 1.0 - 0.999;
+  ta.eps = 1e-8;
+  ta.n = n;
+  ta.mirrored = mirrored;
+  ta.base = mirrored ? n / 2 : n;
+  ta.ask_key = mk(hi, lo);
+  ta.shaped = dsh;
+  // single-entry table holding exactly this step's corrections
+  ta.adam_bc = dbc - 2 * th;  // index 2*(t-1) with t = th+1 -> dbc[0]
+  ta.adam_bc_len = th + 1;
+  CK(run_openes_tell(ta, 0));
+  CK(cudaMemcpy(mean, dmean, sizeof(double) * d, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(m, dm, sizeof(double) * d, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(v, dv, sizeof(double) * d, cudaMemcpyDeviceToHost));
+  *t = th + 1;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_ars_ask(const double* mean, int64_t d, double sigma, uint64_t hi, uint64_t lo, int32_t n,
+                             double* deltas, double* cand) {
+  DEV_OR_RETURN();
+  if (n < 2 || n % 2) return set_err(EVORL_E_INVALID_ARGUMENT, "ars_ask: population must be even");
+  Scratch a, b, c;
+  double *dm, *dd, *dc;
+  if (int rc = up(a, mean, d, &dm)) return rc;
+  if (int rc = up(b, (const double*)nullptr, (size_t)(n / 2) * d, &dd)) return rc;
+  if (int rc = up(c, (const double*)nullptr, (size_t)n * d, &dc)) return rc;
+  CK(run_ars_ask(dm, d, sigma, mk(hi, lo), n, dd, dc, 0));
+  if (deltas) CK(cudaMemcpy(deltas, dd, sizeof(double) * (n / 2) * d, cudaMemcpyDeviceToHost));
+  if (cand) CK(cudaMemcpy(cand, dc, sizeof(double) * n * d, cudaMemcpyDeviceToHost));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_ars_tell(double* mean, int64_t d, int32_t elites, double lr, uint64_t hi, uint64_t lo,
+                              const double* fitness, int32_t n, int32_t* updated) {
+  DEV_OR_RETURN();
+  if (n < 2 || n % 2) return set_err(EVORL_E_INVALID_ARGUMENT, "ars_tell: reward/direction size mismatch");
+  const int half = n / 2;
+  Scratch a, f, sc, r, ei, ed, se;
+  double *dm, *df, *dsc, *ded;
+  int *dr, *dei;
+  ArsSel* dsel;
+  if (int rc = up(a, mean, d, &dm)) return rc;
+  if (int rc = up(f, fitness, n, &df)) return rc;
+  if (int rc = up(sc, (const double*)nullptr, half, &dsc)) return rc;
+  if (int rc = up(r, (const int*)nullptr, half, &dr)) return rc;
+  if (int rc = up(ei, (const int*)nullptr, half, &dei)) return rc;
+  if (int rc = up(ed, (const double*)nullptr, half, &ded)) return rc;
+  if (int rc = up(se, (const ArsSel*)nullptr, 1, &dsel)) return rc;
+  CK(run_ars_scores(df, half, dsc, 0));
+  CK(run_rank(dsc, half, 1, dr, 0));
+  CK(run_ars_select(df, dr, half, elites, lr, dei, ded, dsel, 0));
+  CK(run_ars_update(dm, d, 0, d, mk(hi, lo), dei, ded, dsel, 0));
+  ArsSel hs{};
+  CK(cudaMemcpy(&hs, dsel, sizeof hs, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(mean, dm, sizeof(double) * d, cudaMemcpyDeviceToHost));
+  if (updated) *updated = hs.skipped ? 0 : 1;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_measure_fp64_peak(double* tflops) {
+  DEV_OR_RETURN();
+  *tflops = measure_fp64_peak_tflops();
+  CK(cudaGetLastError());
+  return EVORL_OK;
+}

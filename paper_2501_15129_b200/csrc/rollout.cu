@@ -1,0 +1,560 @@
+// rollout.cu -- the fused population rollout.
+//
+// Replaces, for every lane of the m x e grid, the reference's per-lane loop
+// (proj/src/rollout.cpp:94-174: normalize -> forward -> draw_action ->
+// batched_step -> return accumulation) and the lane scheduling of
+// batched_rollout (proj/src/rollout.cpp:176-214).
+//
+// Design (B200):
+//  * One TEAM per (agent, group of ET lanes).  A team is a thread-block
+//    cluster of C CTAs; CTA c owns a row slice of every hidden layer.  The
+//    agent's weights are materialised ONCE into shared memory (regenerated
+//    from the ask key for OpenES/ARS/CEM -- the perturbation is never stored
+//    in HBM) and stay resident for the whole horizon.
+//  * Per env-step each CTA computes its slice of a hidden layer for all ET
+//    lanes as a small register-tiled GEMM (TR rows x ET lanes per thread,
+//    k-split across warps), then scatters the slice to every CTA of the
+//    cluster through DSMEM (st.shared::cluster) and cluster-barriers.  The
+//    output layer is reduced across the cluster in a fixed order, so every
+//    CTA holds bit-identical actions and steps the (replicated, fp64) env
+//    state identically -- no broadcast is needed and control flow stays
+//    uniform across the cluster.
+//  * Env dynamics, returns and RunningStats are fp64 in the reference's
+//    operation order (env.cuh).  The policy GEMM runs in T = double (parity
+//    mode) or float (throughput mode).
+#include <algorithm>
+#include <cstdio>
+
+#include "rollout.cuh"
+
+namespace evorl_b200 {
+
+template <typename T>
+EVB_DEV T to_T(double v);
+template <>
+EVB_DEV double to_T<double>(double v) {
+  return v;
+}
+template <>
+EVB_DEV float to_T<float>(double v) {
+  return __double2float_rn(v);
+}
+
+EVB_DEV uint32_t ld_cluster_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// Candidate parameter p of agent `agent` (global population index).
+EVB_DEV double param_value(const ParamDesc& P, long long d, int agent_local, int agent,
+                           long long p) {
+  switch (P.src) {
+    case SRC_OPENES: {  // proj/src/ec.cpp:87-94: (sigma * eps) + mean, rows [base,n) = -eps
+      long long row = agent;
+      bool neg = false;
+      if (P.mirrored && agent >= P.base) {
+        row = agent - P.base;
+        neg = true;
+      }
+      double eps = normal_at(P.ask_key, (uint64_t)(row * d + p));
+      if (neg) eps = -eps;
+      return dadd(dmul(P.sigma, eps), P.mean[p]);
+    }
+    case SRC_ARS: {  // proj/src/ec.cpp:119-123: interleaved mean +/- sigma*delta_k
+      const long long k = agent >> 1;
+      const double sd = dmul(P.sigma, normal_at(P.ask_key, (uint64_t)(k * d + p)));
+      return (agent & 1) ? dsub(P.mean[p], sd) : dadd(P.mean[p], sd);
+    }
+    case SRC_CEM: {  // proj/src/ec.cpp:306-313: z * sqrt(var) + mean
+      const double z = normal_at(P.ask_key, (uint64_t)((long long)agent * d + p));
+      return dadd(dmul(z, sqrt(P.var[p])), P.mean[p]);
+    }
+    default:
+      return P.params[(long long)agent_local * d + p];
+  }
+}
+
+template <typename T, int N>
+struct VecLoad {
+  EVB_DEV static void load(const T* __restrict__ src, T* dst) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) dst[i] = src[i];
+  }
+};
+// 16-byte vector loads from shared memory.
+template <int N>
+struct VecLoad<double, N> {
+  EVB_DEV static void load(const double* __restrict__ src, double* dst) {
+    if constexpr (N % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < N; i += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(src + i);
+        dst[i] = v.x;
+        dst[i + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) dst[i] = src[i];
+    }
+  }
+};
+template <int N>
+struct VecLoad<float, N> {
+  EVB_DEV static void load(const float* __restrict__ src, float* dst) {
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < N; i += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(src + i);
+        dst[i] = v.x;
+        dst[i + 1] = v.y;
+        dst[i + 2] = v.z;
+        dst[i + 3] = v.w;
+      }
+    } else if constexpr (N % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < N; i += 2) {
+        const float2 v = *reinterpret_cast<const float2*>(src + i);
+        dst[i] = v.x;
+        dst[i + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) dst[i] = src[i];
+    }
+  }
+};
+
+// Partial GEMM of one hidden-layer slice: part[ks][r][e] = sum_{k in chunk ks}
+// W[k][r] * x[k][e].  W is k-major with RSP padded rows (rows contiguous, so a
+// warp reads 32*TR consecutive weights); x[k][0..ET) is warp-uniform (broadcast).
+template <typename T, int TR, int ET>
+EVB_DEV void hidden_partial(const T* __restrict__ Ws, int RSP, int K, int KS,
+                            const T* __restrict__ x, T* __restrict__ part, int tid) {
+  const int nrg = RSP / TR;
+  const int kc = (K + KS - 1) / KS;
+  for (int w = tid; w < nrg * KS; w += ROLLOUT_THREADS) {
+    const int rg = w % nrg, ks = w / nrg;
+    const int k0 = ks * kc;
+    const int k1 = min(K, k0 + kc);
+    T acc[TR][ET];
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int e = 0; e < ET; ++e) acc[i][e] = T(0);
+    const T* wp = Ws + rg * TR;
+#pragma unroll 2
+    for (int k = k0; k < k1; ++k) {
+      T wv[TR], xv[ET];
+      VecLoad<T, TR>::load(wp + (size_t)k * RSP, wv);
+      VecLoad<T, ET>::load(x + (size_t)k * ET, xv);
+#pragma unroll
+      for (int i = 0; i < TR; ++i)
+#pragma unroll
+        for (int e = 0; e < ET; ++e) acc[i][e] = fma(wv[i], xv[e], acc[i][e]);
+    }
+    T* pp = part + ((size_t)ks * RSP + rg * TR) * ET;
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int e = 0; e < ET; ++e) pp[i * ET + e] = acc[i][e];
+  }
+}
+
+template <typename T, int TR, int ET, int C>
+__global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __grid_constant__ RolloutArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemPlan& S = A.plan;
+  const NetDesc& N = A.net;
+  const EnvDesc& E = A.env;
+  const int tid = threadIdx.x;
+  const int crank = C > 1 ? (int)cluster_ctarank() : 0;
+  const int team = blockIdx.x / C;
+  const int agent_local = team / A.groups;
+  const int group = team % A.groups;
+  const int agent = A.agent_offset + agent_local;
+  const int L = N.nlayers;
+  const int nh = L - 1;
+  const int O = N.dims[L];
+
+  // ------------------------------------------------------------ prologue
+  for (int i = tid; i < S.bytes / 4; i += ROLLOUT_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  __syncthreads();
+  for (int l = 0; l < nh; ++l) {
+    const int K = N.dims[l], W = N.dims[l + 1];
+    const int RS = S.RS[l], RSP = S.RSP[l], r0 = crank * RS;
+    const int RSv = max(0, min(RS, W - r0));
+    T* Ws = reinterpret_cast<T*>(smem + S.off_w[l]);
+    T* bs = reinterpret_cast<T*>(smem + S.off_b[l]);
+    for (int i = tid; i < K * RSv; i += ROLLOUT_THREADS) {
+      const int k = i / RSv, r = i % RSv;
+      Ws[(size_t)k * RSP + r] =
+          to_T<T>(param_value(A.par, N.d, agent_local, agent, N.w_off[l] + (long long)k * W + r0 + r));
+    }
+    for (int r = tid; r < RSv; r += ROLLOUT_THREADS)
+      bs[r] = to_T<T>(param_value(A.par, N.d, agent_local, agent, N.b_off[l] + r0 + r));
+  }
+  // Output layer: the rows of its input owned by this CTA (the last hidden
+  // slice, or the whole observation for a linear policy).
+  const int Kout = N.dims[L - 1];
+  const int KRS = nh > 0 ? S.RS[nh - 1] : Kout;
+  const int KRP = nh > 0 ? S.RSP[nh - 1] : Kout;
+  const int k0out = nh > 0 ? crank * KRS : 0;
+  const int KRv = max(0, min(KRS, Kout - k0out));
+  {
+    T* Wo = reinterpret_cast<T*>(smem + S.off_wout);
+    T* bo = reinterpret_cast<T*>(smem + S.off_bout);
+    for (int i = tid; i < KRv * O; i += ROLLOUT_THREADS) {
+      const int k = i / O, o = i % O;
+      Wo[i] = to_T<T>(
+          param_value(A.par, N.d, agent_local, agent, N.w_off[L - 1] + (long long)(k0out + k) * O + o));
+    }
+    for (int o = tid; o < O; o += ROLLOUT_THREADS)
+      bo[o] = to_T<T>(param_value(A.par, N.d, agent_local, agent, N.b_off[L - 1] + o));
+  }
+
+  // ------------------------------------------------------------ lane state
+  const int j = group * ET + tid;  // lane index within the agent
+  const bool is_env = tid < ET;
+  const bool valid = is_env && j < A.e;
+  const int per = A.count / A.e, rem = A.count % A.e;
+  const int eps_this = valid ? per + (j < rem ? 1 : 0) : 0;
+  const int slot0 = valid ? j * per + min(j, rem) : 0;
+  LaneEnv s{};
+  double ep_ret = 0.0, wc = 0.0;
+  double wmean[4] = {0, 0, 0, 0}, wm2[4] = {0, 0, 0, 0};
+  int ep_len = 0, eps_done = 0;
+  long long steps = 0;
+  uint32_t myfault = 0, myfault_layer = 0;
+  if (valid) {
+    const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
+    env_reset(E, fold_in(lane_key, 0), s);  // proj/src/rollout.cpp:104
+  }
+  NormParams nrm;
+  nrm.active = 0;
+  nrm.dim = 0;
+  if (A.norm != nullptr) nrm = *A.norm;
+
+  T* x0 = reinterpret_cast<T*>(smem + S.off_x0);
+  T* part = reinterpret_cast<T*>(smem + S.off_part);
+  T* pout_base = reinterpret_cast<T*>(smem + S.off_pout);
+  uint32_t* mask = reinterpret_cast<uint32_t*>(smem + S.off_mask);
+  const T* Wo = reinterpret_cast<const T*>(smem + S.off_wout);
+  const T* bo = reinterpret_cast<const T*>(smem + S.off_bout);
+  __syncthreads();
+
+  for (int it = 0;; ++it) {
+    if (tid < MAXL) mask[(it & 1) * MAXL + tid] = 0u;  // last used two steps ago
+    const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
+    if (!__syncthreads_or(active)) break;
+    uint32_t* cur_mask = mask + (it & 1) * MAXL;
+    // output partials are double-buffered by step parity: with a single hidden
+    // layer there is no cluster barrier between two steps' output exchanges
+    T* pout = pout_base + (it & 1) * C * O * ET;
+
+    // observation -> (RunningStats) -> normalisation (proj/src/rollout.cpp:124-126)
+    if (is_env) {
+      double raw[4];
+      observe(E, s, raw);
+      if (active && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
+        if (wc == 0.0) {
+          for (int i = 0; i < E.obs_dim; ++i) {
+            wmean[i] = raw[i];
+            wm2[i] = 0.0;
+          }
+          wc = 1.0;
+        } else {
+          wc = dadd(wc, 1.0);
+          for (int i = 0; i < E.obs_dim; ++i) {
+            const double delta = dsub(raw[i], wmean[i]);
+            wmean[i] = dadd(wmean[i], ddiv(delta, wc));
+            wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
+          }
+        }
+      }
+      for (int i = 0; i < E.obs_dim; ++i) {
+        double v = raw[i];
+        if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
+        x0[i * ET + tid] = active ? to_T<T>(v) : T(0);
+      }
+    }
+    __syncthreads();
+
+    // hidden layers (proj/src/net.cpp:86-127): z = W x + b, ReLU
+    for (int l = 0; l < nh; ++l) {
+      const int K = N.dims[l], W = N.dims[l + 1];
+      const int RS = S.RS[l], RSP = S.RSP[l], r0 = crank * RS;
+      const int RSv = max(0, min(RS, W - r0));
+      const T* xin = l == 0 ? x0 : reinterpret_cast<const T*>(smem + S.off_h[l - 1]);
+      hidden_partial<T, TR, ET>(reinterpret_cast<const T*>(smem + S.off_w[l]), RSP, K, S.KS[l], xin,
+                                part, tid);
+      __syncthreads();
+      const T* bs = reinterpret_cast<const T*>(smem + S.off_b[l]);
+      T* hb = reinterpret_cast<T*>(smem + S.off_h[l]);
+      const bool last_hidden = l == nh - 1;
+      const int KSl = S.KS[l];
+      for (int i = tid; i < RSv * ET; i += ROLLOUT_THREADS) {
+        const int r = i / ET, e = i % ET;
+        T z = part[(size_t)r * ET + e];
+        for (int ks = 1; ks < KSl; ++ks) z += part[((size_t)ks * RSP + r) * ET + e];
+        z = z + bs[r];
+        const T h = z > T(0) ? z : T(0);
+        if (!isfinite((double)h)) atomicOr(&cur_mask[l], 1u << e);
+        if (last_hidden || C == 1) {
+          hb[(size_t)(last_hidden ? r : r0 + r) * ET + e] = h;
+        } else {
+          const uint32_t la = smem_u32(hb + (size_t)(r0 + r) * ET + e);
+#pragma unroll
+          for (int c = 0; c < C; ++c) st_cluster<T>(map_cluster(la, (uint32_t)c), h);
+        }
+      }
+      if constexpr (C > 1) {
+        if (!last_hidden) {
+          cluster_sync_all();
+        } else {
+          __syncthreads();
+        }
+      } else {
+        __syncthreads();
+      }
+    }
+
+    // output layer partial over this CTA's rows, reduced across the cluster
+    {
+      const T* xin = nh > 0 ? reinterpret_cast<const T*>(smem + S.off_h[nh - 1]) : x0;
+      const int OE = O * ET;
+      const int KSo = S.KS_out;
+      const int kc = (KRP + KSo - 1) / KSo;
+      for (int w = tid; w < OE * KSo; w += ROLLOUT_THREADS) {
+        const int oe = w % OE, ks = w / OE;
+        const int o = oe / ET, e = oe % ET;
+        const int k0 = ks * kc, k1 = min(KRv, k0 + kc);
+        T acc = T(0);
+        for (int k = k0; k < k1; ++k) acc = fma(Wo[k * O + o], xin[(size_t)k * ET + e], acc);
+        part[w] = acc;
+      }
+      __syncthreads();
+      for (int oe = tid; oe < OE; oe += ROLLOUT_THREADS) {
+        T v = part[oe];
+        for (int ks = 1; ks < KSo; ++ks) v += part[ks * OE + oe];
+        if constexpr (C > 1) {
+          const uint32_t la = smem_u32(pout + crank * OE + oe);
+#pragma unroll
+          for (int c = 0; c < C; ++c) st_cluster<T>(map_cluster(la, (uint32_t)c), v);
+        } else {
+          pout[oe] = v;
+        }
+      }
+      if constexpr (C > 1) {
+        cluster_sync_all();
+      } else {
+        __syncthreads();
+      }
+    }
+
+    // head + env step (proj/src/rollout.cpp:57-90, :131-153)
+    if (active) {
+      double z[8];
+      bool nonfinite_out = false;
+      for (int o = 0; o < O && o < 8; ++o) {
+        T v = pout[o * ET + tid];
+        for (int c = 1; c < C; ++c) v += pout[c * O * ET + o * ET + tid];
+        v = v + bo[o];
+        z[o] = (double)v;
+        if (!isfinite(z[o])) nonfinite_out = true;
+      }
+      // NetFault: the lowest layer with a non-finite activation for this lane
+      int bad_layer = -1;
+      for (int l = 0; l < nh && bad_layer < 0; ++l) {
+        uint32_t m = cur_mask[l];
+        if constexpr (C > 1) {
+          const uint32_t la = smem_u32(&cur_mask[l]);
+          for (int c = 0; c < C; ++c) m |= ld_cluster_u32(map_cluster(la, (uint32_t)c));
+        }
+        if (m & (1u << tid)) bad_layer = l;
+      }
+      if (bad_layer < 0 && nonfinite_out) bad_layer = L - 1;
+      if (bad_layer >= 0) {
+        myfault = FAULT_NET;
+        myfault_layer = (uint32_t)bad_layer;
+      } else {
+        double action;
+        if (N.head == HEAD_CATEGORICAL) {
+          int arg = 0;
+          for (int o = 1; o < O; ++o)
+            if (z[o] > z[arg]) arg = o;  // maxCoeff: first maximum
+          action = (double)arg;
+        } else if (N.head == HEAD_TANH) {
+          action = N.tanh_scale * tanh(z[0]);
+        } else {
+          action = z[0];
+        }
+        double reward = 0.0;
+        bool term = false, trunc = false;
+        const uint32_t f = env_step(E, s, action, reward, term, trunc);
+        if (f) {
+          myfault = f;
+        } else {
+          ep_ret = dadd(ep_ret, reward);  // proj/src/rollout.cpp:143
+          ep_len += 1;
+          steps += 1;
+          if (term || trunc) {
+            if (crank == 0) {
+              const long long slot = (long long)agent_local * A.count + slot0 + eps_done;
+              A.ep_returns[slot] = ep_ret;
+              if (A.ep_lengths) A.ep_lengths[slot] = ep_len;
+            }
+            ep_ret = 0.0;
+            ep_len = 0;
+            eps_done += 1;
+            if (eps_done < eps_this) env_reset(E, s.rng, s);  // auto-reset, env.cpp:163-167
+          }
+        }
+      }
+    }
+  }
+
+  if (valid && crank == 0) {
+    const long long lane = (long long)agent_local * A.e + j;
+    if (A.lane_steps) A.lane_steps[lane] = steps;
+    if (A.track_stats && A.lane_stats) {
+      double* st = A.lane_stats + lane * 9;
+      st[0] = wc;
+      for (int i = 0; i < 4; ++i) {
+        st[1 + i] = wmean[i];
+        st[5 + i] = wm2[i];
+      }
+    }
+    if (myfault) record_fault(A.fault, (uint64_t)((long long)agent * A.e + j), myfault, myfault_layer);
+  }
+  if constexpr (C > 1) cluster_sync_all();  // no CTA may exit while peers still address its SMEM
+}
+
+// ------------------------------------------------------------------ host side
+static int align16(int x) { return (x + 15) & ~15; }
+static int pow2floor(int x) {
+  int p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
+}
+
+static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int tsize, SmemPlan* P) {
+  const int L = net.nlayers, nh = L - 1, O = net.dims[L];
+  if (nh == 0 && C > 1) return false;
+  if (O > 8 || obs_dim > 4) return false;
+  SmemPlan p{};
+  p.C = C;
+  p.TR = TR;
+  p.ET = ET;
+  int off = 0;
+  size_t part = 0;
+  for (int l = 0; l < nh; ++l) {
+    const int K = net.dims[l], W = net.dims[l + 1];
+    if (W < C) return false;
+    const int RS = (W + C - 1) / C;
+    const int RSP = (RS + 32 * TR - 1) / (32 * TR) * (32 * TR);
+    const int nrg = RSP / TR;
+    int KS = nrg >= ROLLOUT_THREADS ? 1 : pow2floor(ROLLOUT_THREADS / nrg);
+    while (KS > 1 && K / KS < 8) KS /= 2;
+    p.RS[l] = RS;
+    p.RSP[l] = RSP;
+    p.KS[l] = KS;
+    p.off_w[l] = off;
+    off = align16(off + K * RSP * tsize);
+    p.off_b[l] = off;
+    off = align16(off + RSP * tsize);
+    part = std::max(part, (size_t)KS * RSP * ET * tsize);
+  }
+  const int KRP = nh > 0 ? p.RSP[nh - 1] : net.dims[0];
+  p.off_wout = off;
+  off = align16(off + KRP * O * tsize);
+  p.off_bout = off;
+  off = align16(off + O * tsize);
+  p.off_x0 = off;
+  off = align16(off + 4 * ET * tsize);
+  for (int l = 0; l < nh; ++l) {
+    p.off_h[l] = off;
+    const int rows = (l == nh - 1) ? p.RSP[l] : net.dims[l + 1];
+    off = align16(off + rows * ET * tsize);
+  }
+  int KSo = pow2floor(std::max(1, ROLLOUT_THREADS / (O * ET)));
+  while (KSo > 1 && KRP / KSo < 4) KSo /= 2;
+  p.KS_out = KSo;
+  part = std::max(part, (size_t)KSo * O * ET * tsize);
+  p.off_part = off;
+  off = align16(off + (int)part);
+  p.off_pout = off;
+  off = align16(off + 2 * C * O * ET * tsize);
+  p.off_mask = off;
+  off = align16(off + 2 * MAXL * 4);
+  p.bytes = off;
+  if (off > 227 * 1024) return false;
+  *P = p;
+  return true;
+}
+
+bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan) {
+  const int ET = e >= 5 ? 16 : (e >= 2 ? 4 : 1);
+  const int tsize = precision == 0 ? 8 : 4;
+  for (int C : {1, 2, 4, 8}) {
+    if (ET == 16 && try_plan(net, obs_dim, ET, 2, C, tsize, plan)) {
+      // TR=2 needs enough row groups x k-splits to occupy the CTA
+      bool ok = true;
+      for (int l = 0; l < net.nlayers - 1; ++l)
+        if ((plan->RSP[l] / 2) * plan->KS[l] < ROLLOUT_THREADS / 2 && net.dims[l] >= 64) ok = false;
+      if (ok) return true;
+    }
+    if (try_plan(net, obs_dim, ET, 1, C, tsize, plan)) return true;
+  }
+  return false;
+}
+
+template <typename T, int TR, int ET, int C>
+static cudaError_t launch_inst(const RolloutArgs& a, cudaStream_t stream) {
+  auto kern = rollout_kernel<T, TR, ET, C>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(a.n_agents * a.groups * C));
+  cfg.blockDim = dim3(ROLLOUT_THREADS);
+  cfg.dynamicSmemBytes = (size_t)a.plan.bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <typename T, int TR, int ET>
+static cudaError_t launch_c(const RolloutArgs& a, cudaStream_t s) {
+  switch (a.plan.C) {
+    case 1: return launch_inst<T, TR, ET, 1>(a, s);
+    case 2: return launch_inst<T, TR, ET, 2>(a, s);
+    case 4: return launch_inst<T, TR, ET, 4>(a, s);
+    case 8: return launch_inst<T, TR, ET, 8>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+static cudaError_t launch_t(const RolloutArgs& a, cudaStream_t s) {
+  if (a.plan.ET == 1) return launch_c<T, 1, 1>(a, s);
+  if (a.plan.ET == 4) return launch_c<T, 1, 4>(a, s);
+  if (a.plan.TR == 2) return launch_c<T, 2, 16>(a, s);
+  return launch_c<T, 1, 16>(a, s);
+}
+
+cudaError_t launch_rollout(const RolloutArgs& a, int precision, cudaStream_t stream) {
+  if (a.n_agents <= 0) return cudaSuccess;
+  return precision == 0 ? launch_t<double>(a, stream) : launch_t<float>(a, stream);
+}
+
+}  // namespace evorl_b200

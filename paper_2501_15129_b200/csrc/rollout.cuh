@@ -1,0 +1,91 @@
+// rollout.cuh -- descriptors shared by the host planner and the fused
+// population-rollout kernel (rollout.cu).
+#pragma once
+
+#include "common.cuh"
+#include "env.cuh"
+
+namespace evorl_b200 {
+
+constexpr int MAXL = 9;  // up to 8 hidden layers + output layer
+constexpr int ROLLOUT_THREADS = 256;
+
+enum : int { HEAD_TANH = 0, HEAD_GAUSSIAN = 1, HEAD_CATEGORICAL = 2, HEAD_LINEAR = 3 };
+
+// Flat parameter layout of proj/src/net.cpp:26-48 (column-major W then b per
+// layer).  Layer norm is not supported on the device path (refused by the
+// host planner).
+struct NetDesc {
+  int nlayers;  // hidden layers + 1
+  int dims[MAXL + 1];
+  long long w_off[MAXL];
+  long long b_off[MAXL];
+  int head;
+  double tanh_scale;
+  long long d;
+};
+
+// Where candidate i's parameters come from.  Only SRC_EXPLICIT reads a stored
+// n x d matrix; the others regenerate the perturbation from the ask key
+// (proj/src/ec.cpp:71-97 OpenES/VES, :113-125 ARS, :306-313 CEM).
+enum : int { SRC_EXPLICIT = 0, SRC_OPENES = 1, SRC_ARS = 2, SRC_CEM = 3 };
+struct ParamDesc {
+  int src;
+  const double* params;  // SRC_EXPLICIT: n_agents x d, row-major
+  const double* mean;    // d
+  const double* var;     // CEM diagonal variance
+  double sigma;
+  DKey ask_key;
+  int base;  // OpenES/VES: number of sampled rows (n/2 when mirrored)
+  int mirrored;
+};
+
+// Observation normaliser frozen for the generation: x = (o - mean) / den,
+// den = max(sqrt(var), 1e-8) (proj/src/obs_norm.cpp:76-79).
+struct NormParams {
+  int active;
+  int dim;
+  double mean[4];
+  double den[4];
+};
+
+struct SmemPlan {
+  int C;             // cluster size (CTAs per team)
+  int TR;            // rows per thread
+  int ET;            // lanes per team
+  int RS[MAXL];      // real rows owned per CTA (hidden layers)
+  int RSP[MAXL];     // padded rows per CTA
+  int KS[MAXL];      // k-split per hidden layer
+  int KS_out;        // k-split of the output layer partial
+  int off_w[MAXL], off_b[MAXL];
+  int off_wout, off_bout, off_x0, off_h[MAXL], off_part, off_pout, off_mask;
+  int bytes;
+};
+
+struct RolloutArgs {
+  EnvDesc env;
+  NetDesc net;
+  ParamDesc par;
+  SmemPlan plan;
+  const NormParams* norm;  // device; may be null (no normalisation)
+  int n_agents;            // agents in this launch
+  int agent_offset;        // global index of agent 0 (population sharding)
+  int e;                   // lanes per agent (envs_per_agent)
+  int count;               // episodes per agent (episodes mode)
+  int groups;              // teams per agent = ceil(e / ET)
+  DKey rollout_key;        // fold_in(step_key, 1) (proj/src/workflow_es.cpp:125)
+  int track_stats;         // RunningStats obs tracking (ARS)
+  int max_iters;           // safety bound on steps per lane
+  double* ep_returns;      // [n_agents][count], lane-major slot order
+  int* ep_lengths;         // [n_agents][count]
+  long long* lane_steps;   // [n_agents * e]
+  double* lane_stats;      // [n_agents * e][9] = count, mean[4], m2[4]
+  unsigned long long* fault;
+};
+
+// Host-side: launch the rollout with the plan's template instance.
+cudaError_t launch_rollout(const RolloutArgs& a, int precision, cudaStream_t stream);
+// Host-side: build the SMEM plan; returns false if no cluster size fits.
+bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan);
+
+}  // namespace evorl_b200

@@ -1,0 +1,413 @@
+"""Reference-facing host API over the C ABI.
+
+Mirrors the reference's C++ seam with the same names,
+argument meaning and error behaviour, so the parity tests read like the
+reference's own tests:
+
+  * ``EsWorkflow``      -- Workflow::init/step/evaluate of proj/src/workflow_es.cpp
+  * ``batched_rollout`` -- proj/src/rollout.cpp:176-214 (deterministic policies)
+  * ``gaussian_matrix``, ``centered_ranks``, ``rank_desc`` -- proj/src/ec.cpp
+  * ``openes_ask``/``openes_tell``, ``ars_ask``/``ars_tell`` -- proj/src/ec.cpp
+  * ``env_step_batch``  -- proj/src/env.cpp:113-155
+
+All compute runs on the GPU through libevorl_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+
+__all__ = ["EsConfig", "EsWorkflow", "StepMetrics", "batched_rollout", "gaussian_matrix",
+           "centered_ranks", "rank_desc", "openes_ask", "openes_tell", "ars_ask", "ars_tell",
+           "env_step_batch", "threefry2x64", "stream_words", "param_count", "mlp_desc",
+           "measure_fp64_peak"]
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _key(key) -> tuple[int, int]:
+    if hasattr(key, "hi"):
+        return int(key.hi), int(key.lo)
+    return int(key[0]), int(key[1])
+
+
+# ----------------------------------------------------------------- config
+@dataclass
+class EsConfig:
+    """Reference config-registry keys (proj/src/config.cpp:23-70) for the ES
+    workflow, with the registry defaults."""
+    algo: str = "openes"                 # ec.algo
+    env: str = "cartpole"                # env.id
+    fixed_horizon: bool = False          # env.fixed_horizon
+    max_episode_steps: int = 0           # env.max_episode_steps
+    hidden: Sequence[int] = (64, 64)     # net.hidden
+    layer_norm: bool = False             # net.layer_norm
+    allow_linear: bool = False           # EXTENSION: hidden=() linear policy
+    pop: int = 128                       # ec.pop
+    fitness_episodes: int = 1            # ec.fitness_episodes
+    obs_norm: str = "auto"               # obs_norm.mode
+    vbn_samples: int = 10000             # obs_norm.vbn_samples
+    openes_sigma: float = 0.02
+    openes_lr: float = 0.01
+    openes_weight_decay: float = 0.005
+    openes_mirrored: bool = True
+    openes_noise_table: bool = False
+    openes_noise_table_size: int = 1 << 22
+    ars_sigma: float = 0.03
+    ars_lr: float = 0.02
+    ars_elites: int = 16
+    ves_sigma: float = 0.02
+    ves_elites: int = 16
+    ves_mirrored: bool = True
+    cmaes_sigma0: float = 0.1
+    cmaes_elites: int = 64
+    cmaes_max_dim: int = 4096
+    cem_elites: int = 5
+    cem_var_init: float = 1e-3
+    cem_noise_start: float = 1e-3
+    cem_noise_end: float = 1e-5
+    cem_decay_iters: int = 2000
+    precision: str = "f64"               # "f64" (parity) | "f32" (throughput)
+    device: int = 0
+
+    def to_c(self) -> _lib.EsConfigC:
+        c = _lib.EsConfigC()
+        _lib.load().evorl_es_default_config(C.byref(c))
+        if self.algo not in _lib.ALGO:
+            raise _lib.ConfigError(f"ec.algo: unknown algorithm '{self.algo}'")
+        c.algo = _lib.ALGO[self.algo]
+        if self.env not in ("cartpole", "pendulum"):
+            raise _lib.InvalidArgument(f"unknown env id: {self.env}")
+        c.env_id = _lib.ENV_CARTPOLE if self.env == "cartpole" else _lib.ENV_PENDULUM
+        c.fixed_horizon = int(self.fixed_horizon)
+        c.max_episode_steps = int(self.max_episode_steps)
+        c.n_hidden = len(self.hidden)
+        for i, h in enumerate(self.hidden):
+            c.hidden[i] = int(h)
+        c.layer_norm = int(self.layer_norm)
+        c.allow_linear = int(self.allow_linear)
+        c.pop = int(self.pop)
+        c.fitness_episodes = int(self.fitness_episodes)
+        if self.obs_norm not in _lib.NORM:
+            raise _lib.ConfigError(f"obs_norm.mode: unknown value '{self.obs_norm}'")
+        c.obs_norm_mode = _lib.NORM[self.obs_norm]
+        c.vbn_samples = int(self.vbn_samples)
+        for k in ("openes_sigma", "openes_lr", "openes_weight_decay", "ars_sigma", "ars_lr",
+                  "ves_sigma", "cmaes_sigma0", "cem_var_init", "cem_noise_start",
+                  "cem_noise_end"):
+            setattr(c, k, float(getattr(self, k)))
+        for k in ("openes_mirrored", "openes_noise_table", "ves_mirrored"):
+            setattr(c, k, int(bool(getattr(self, k))))
+        for k in ("openes_noise_table_size", "ars_elites", "ves_elites", "cmaes_elites",
+                  "cmaes_max_dim", "cem_elites", "cem_decay_iters", "device"):
+            setattr(c, k, int(getattr(self, k)))
+        c.precision = _lib.PREC_F64 if self.precision == "f64" else _lib.PREC_F32
+        return c
+
+
+@dataclass
+class StepMetrics:
+    """StepMetrics of EsWorkflow::step (proj/src/workflow_es.cpp:140-169)."""
+    values: dict = field(default_factory=dict)
+
+    def __getitem__(self, k):
+        return self.values[k]
+
+
+class EsWorkflow:
+    """Device-resident EsWorkflow (proj/src/workflow_es.cpp:26-276)."""
+
+    def __init__(self, cfg: EsConfig):
+        self.L = _lib.load()
+        self.cfg = cfg
+        self._c = cfg.to_c()
+        h = C.c_void_p()
+        check(self.L.evorl_es_create(C.byref(self._c), C.byref(h)))
+        self.h = h
+        self.dim = int(self.L.evorl_es_dim(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.evorl_es_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # Workflow interface --------------------------------------------------
+    def init(self, key) -> "EsWorkflow":
+        hi, lo = _key(key)
+        check(self.L.evorl_es_init(self.h, hi, lo))
+        return self
+
+    def step(self) -> StepMetrics:
+        m = _lib.StepMetricsC()
+        check(self.L.evorl_es_step(self.h, C.byref(m)))
+        return self._metrics(m)
+
+    def evaluate(self, episodes: int, key) -> tuple[float, float]:
+        hi, lo = _key(key)
+        mr, sd = C.c_double(), C.c_double()
+        check(self.L.evorl_es_evaluate(self.h, int(episodes), hi, lo, C.byref(mr), C.byref(sd)))
+        return mr.value, sd.value
+
+    @staticmethod
+    def _metrics(m) -> StepMetrics:
+        return StepMetrics({"fitness/mean": m.fitness_mean, "fitness/max": m.fitness_max,
+                            "fitness/min": m.fitness_min, "es/sigma": m.sigma,
+                            "es/update_skipped": m.update_skipped})
+
+    # state access -------------------------------------------------------
+    def mean(self) -> np.ndarray:
+        out = np.empty(self.dim, np.float64)
+        check(self.L.evorl_es_get_mean(self.h, _p(out)))
+        return out
+
+    def set_mean(self, mean) -> None:
+        m = np.ascontiguousarray(mean, np.float64)
+        assert m.shape == (self.dim,)
+        check(self.L.evorl_es_set_mean(self.h, _p(m)))
+
+    def adam(self):
+        m = np.empty(self.dim, np.float64)
+        v = np.empty(self.dim, np.float64)
+        t = C.c_int64()
+        check(self.L.evorl_es_get_adam(self.h, _p(m), _p(v), C.byref(t)))
+        return m, v, t.value
+
+    def set_adam(self, m, v, t: int) -> None:
+        m = np.ascontiguousarray(m, np.float64)
+        v = np.ascontiguousarray(v, np.float64)
+        check(self.L.evorl_es_set_adam(self.h, _p(m), _p(v), int(t)))
+
+    def fitness(self) -> np.ndarray:
+        out = np.empty(self.cfg.pop, np.float64)
+        check(self.L.evorl_es_get_fitness(self.h, _p(out)))
+        return out
+
+    def obs_norm(self) -> _lib.ObsNormC:
+        o = _lib.ObsNormC()
+        check(self.L.evorl_es_get_obs_norm(self.h, C.byref(o)))
+        return o
+
+    def set_obs_norm(self, o) -> None:
+        oc = _lib.ObsNormC()
+        for k in ("mode", "dim", "count"):
+            setattr(oc, k, getattr(o, k))
+        for i in range(4):
+            oc.mean[i] = o.mean[i]
+            oc.var[i] = o.var[i]
+        check(self.L.evorl_es_set_obs_norm(self.h, C.byref(oc)))
+
+    def counters(self) -> tuple[int, int, int]:
+        it, st, ep = C.c_int64(), C.c_int64(), C.c_int64()
+        check(self.L.evorl_es_counters(self.h, C.byref(it), C.byref(st), C.byref(ep)))
+        return it.value, st.value, ep.value
+
+    def set_counters(self, iteration: int, env_steps: int, episodes: int) -> None:
+        check(self.L.evorl_es_set_counters(self.h, iteration, env_steps, episodes))
+
+    def last_timings(self) -> tuple[float, float]:
+        r, s = C.c_float(), C.c_float()
+        check(self.L.evorl_es_last_timings(self.h, C.byref(r), C.byref(s)))
+        return r.value, s.value
+
+    # sharded phases (see paper_2501_15129_b200.dist) ----------------------
+    def set_shard(self, rank: int, world: int) -> None:
+        check(self.L.evorl_es_set_shard(self.h, rank, world))
+
+    def shard_ranges(self):
+        a0, a1, p0, p1 = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+        check(self.L.evorl_es_shard_ranges(self.h, C.byref(a0), C.byref(a1), C.byref(p0),
+                                           C.byref(p1)))
+        return a0.value, a1.value, p0.value, p1.value
+
+    def phase_rollout(self) -> None:
+        check(self.L.evorl_es_phase_rollout(self.h))
+
+    def phase_tell(self) -> StepMetrics:
+        m = _lib.StepMetricsC()
+        check(self.L.evorl_es_phase_tell(self.h, C.byref(m)))
+        return self._metrics(m)
+
+    def device_buffers(self):
+        f, m, s = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(self.L.evorl_es_device_buffers(self.h, C.byref(f), C.byref(m), C.byref(s)))
+        return f.value, m.value, s.value
+
+    def stream(self) -> int:
+        return self.L.evorl_es_stream(self.h)
+
+
+# -------------------------------------------------------------- stateless
+def mlp_desc(input_dim: int, hidden: Sequence[int], output_dim: int, head: int,
+             tanh_scale: float = 1.0, allow_linear: bool = False) -> _lib.MlpDesc:
+    m = _lib.MlpDesc()
+    m.input_dim = input_dim
+    m.n_hidden = len(hidden)
+    for i, h in enumerate(hidden):
+        m.hidden[i] = h
+    m.output_dim = output_dim
+    m.layer_norm = 0
+    m.head = head
+    m.tanh_scale = tanh_scale
+    m.allow_linear = int(allow_linear)
+    return m
+
+
+def param_count(desc: _lib.MlpDesc) -> int:
+    dims = [desc.input_dim] + [desc.hidden[i] for i in range(desc.n_hidden)] + [desc.output_dim]
+    return sum(a * b + b for a, b in zip(dims[:-1], dims[1:]))
+
+
+def threefry2x64(keys: np.ndarray, ctrs: np.ndarray) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, np.uint64).reshape(-1, 2)
+    ctrs = np.ascontiguousarray(ctrs, np.uint64).reshape(-1, 2)
+    out = np.empty_like(keys)
+    check(_lib.load().evorl_threefry2x64(_p(keys), _p(ctrs), _p(out), len(keys)))
+    return out
+
+
+def stream_words(key, first: int, n: int) -> np.ndarray:
+    hi, lo = _key(key)
+    out = np.empty(n, np.uint64)
+    check(_lib.load().evorl_stream_words(hi, lo, first, n, _p(out)))
+    return out
+
+
+def gaussian_matrix(key, rows: int, cols: int) -> np.ndarray:
+    """proj/src/ec.cpp:22-28"""
+    hi, lo = _key(key)
+    out = np.empty((rows, cols), np.float64)
+    check(_lib.load().evorl_gaussian_matrix(hi, lo, rows, cols, _p(out)))
+    return out
+
+
+def centered_ranks(f) -> np.ndarray:
+    """proj/src/ec.cpp:32-46"""
+    f = np.ascontiguousarray(f, np.float64)
+    out = np.empty_like(f)
+    check(_lib.load().evorl_centered_ranks(_p(f), len(f), _p(out)))
+    return out
+
+
+def rank_desc(f) -> np.ndarray:
+    """proj/src/ec.cpp:14-20"""
+    f = np.ascontiguousarray(f, np.float64)
+    out = np.empty(len(f), np.int32)
+    check(_lib.load().evorl_rank_desc(_p(f), len(f), _p(out)))
+    return out
+
+
+def openes_ask(mean, sigma: float, key, n: int, mirrored: bool = True):
+    """proj/src/ec.cpp:71-97 -> (candidates, eps)"""
+    mean = np.ascontiguousarray(mean, np.float64)
+    d = len(mean)
+    hi, lo = _key(key)
+    cand = np.empty((n, d))
+    eps = np.empty((n, d))
+    check(_lib.load().evorl_openes_ask(_p(mean), d, sigma, int(mirrored), hi, lo, n, _p(cand),
+                                       _p(eps)))
+    return cand, eps
+
+
+def openes_tell(mean, m, v, t: int, sigma: float, lr: float, weight_decay: float, key,
+                fitness, mirrored: bool = True):
+    """proj/src/ec.cpp:99-109 + proj/src/optim.cpp:7-17, eps regenerated from
+    the ask key.  Updates mean, m, v in place; returns the new t."""
+    for a in (mean, m, v):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    f = np.ascontiguousarray(fitness, np.float64)
+    hi, lo = _key(key)
+    tt = C.c_int64(t)
+    check(_lib.load().evorl_openes_tell(_p(mean), _p(m), _p(v), C.byref(tt), len(mean), sigma,
+                                        lr, weight_decay, int(mirrored), hi, lo, _p(f), len(f)))
+    return tt.value
+
+
+def ars_ask(mean, sigma: float, key, n: int):
+    """proj/src/ec.cpp:113-125 -> (deltas, candidates)"""
+    mean = np.ascontiguousarray(mean, np.float64)
+    d = len(mean)
+    hi, lo = _key(key)
+    deltas = np.empty((n // 2, d))
+    cand = np.empty((n, d))
+    check(_lib.load().evorl_ars_ask(_p(mean), d, sigma, hi, lo, n, _p(deltas), _p(cand)))
+    return deltas, cand
+
+
+def ars_tell(mean, elites: int, lr: float, key, fitness) -> bool:
+    """proj/src/ec.cpp:127-154 with deltas regenerated from the ask key;
+    fitness is the interleaved (r+, r-) vector.  Returns False if skipped."""
+    assert mean.dtype == np.float64 and mean.flags.c_contiguous
+    f = np.ascontiguousarray(fitness, np.float64)
+    hi, lo = _key(key)
+    upd = C.c_int32()
+    check(_lib.load().evorl_ars_tell(_p(mean), len(mean), elites, lr, hi, lo, _p(f), len(f),
+                                     C.byref(upd)))
+    return bool(upd.value)
+
+
+def env_step_batch(env: str, phys, step_count, action, fixed_horizon=False,
+                   max_episode_steps=0):
+    """proj/src/env.cpp:113-155 for n states (n x 4 phys)."""
+    phys = np.ascontiguousarray(phys, np.float64).copy()
+    sc = np.ascontiguousarray(step_count, np.int32).copy()
+    a = np.ascontiguousarray(action, np.float64)
+    n = len(a)
+    r = np.empty(n)
+    te = np.empty(n, np.int32)
+    tr = np.empty(n, np.int32)
+    fault = np.empty(n, np.int32)
+    eid = _lib.ENV_CARTPOLE if env == "cartpole" else _lib.ENV_PENDULUM
+    check(_lib.load().evorl_env_step_batch(eid, int(fixed_horizon), int(max_episode_steps), n,
+                                           _p(phys), _p(sc), _p(a), _p(r), _p(te), _p(tr),
+                                           _p(fault)))
+    return phys, sc, r, te, tr, fault
+
+
+def batched_rollout(env: str, net: _lib.MlpDesc, params, envs_per_agent: int, key,
+                    count: Optional[int] = None, obs_norm=None, fixed_horizon=False,
+                    max_episode_steps=0, precision="f64", track_obs_stats=False):
+    """proj/src/rollout.cpp:176-214 (Episodes mode, deterministic policy).
+    Returns (returns m x count, steps m, obs_stats m x 9 or None)."""
+    params = np.ascontiguousarray(params, np.float64)
+    m = params.shape[0]
+    e = int(envs_per_agent)
+    count = e if count is None else int(count)
+    ed = _lib.EnvDescC(_lib.ENV_CARTPOLE if env == "cartpole" else _lib.ENV_PENDULUM,
+                       int(fixed_horizon), int(max_episode_steps))
+    nc = None
+    if obs_norm is not None:
+        nc = _lib.ObsNormC()
+        for k in ("mode", "dim", "count"):
+            setattr(nc, k, getattr(obs_norm, k))
+        for i in range(4):
+            nc.mean[i] = obs_norm.mean[i]
+            nc.var[i] = obs_norm.var[i]
+    hi, lo = _key(key)
+    rets = np.empty((m, count))
+    steps = np.empty(m, np.int64)
+    stats = np.empty((m, 9)) if track_obs_stats else None
+    check(_lib.load().evorl_batched_rollout(
+        C.byref(ed), C.byref(net), C.byref(nc) if nc is not None else None, _p(params), m, e,
+        count, hi, lo, _lib.PREC_F64 if precision == "f64" else _lib.PREC_F32, _p(rets),
+        _p(steps), _p(stats) if stats is not None else None))
+    return rets, steps, stats
+
+
+def measure_fp64_peak() -> float:
+    t = C.c_double()
+    check(_lib.load().evorl_measure_fp64_peak(C.byref(t)))
+    return t.value
