@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ES generation path (BASELINE.json metric: env-steps/sec
+and generations/sec at pop x envs, 1/2/4/8 B200 vs the host-CPU reference).
+
+Default workload (N=1): BASELINE.json configs[2] -- OpenES pop 4096 x 16
+envs/individual, 2x256 MLP, Pendulum fixed horizon H=200 (d = 67 073), the
+largest config that fits one GPU and the one the metric's "pop x envs" and
+"1/2/4/8 B200" are quoted on.  A step = one full generation (ask -> rollout of
+13.1 M env-steps -> fitness -> ranks -> tell + Adam) with the population
+sharded over N GPUs (weak... total work fixed: "strong" scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--precision f64]
+  python bench.py --impl reference ...   # the reference CPU path (oracle port) on host cores
+
+Timing: W untimed warm-up generations, then K generations, each bracketed by a
+barrier + torch.cuda.synchronize(); per-generation device time from CUDA
+events on the launching stream, L2 flushed (256 MiB write) between timed
+generations outside the events; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs; the bench line is configs[2] ("3")
+CONFIGS = {
+    "1": dict(algo="openes", env="pendulum", fixed_horizon=True, pop=128, hidden=(64, 64),
+              max_episode_steps=200, fitness_episodes=1,
+              desc="OpenES pop 128 antithetic, 2x64 MLP, Pendulum H=200"),
+    "2": dict(algo="ars", env="pendulum", fixed_horizon=True, pop=1024, hidden=(),
+              allow_linear=True, max_episode_steps=200, fitness_episodes=1,
+              desc="ARS top-16 pop 1024, linear policy (extension), Pendulum H=200, RS obs-norm"),
+    "3": dict(algo="openes", env="pendulum", fixed_horizon=True, pop=4096, hidden=(256, 256),
+              max_episode_steps=200, fitness_episodes=16,
+              desc="OpenES pop 4096 x 16 envs/individual, 2x256 MLP, Pendulum H=200"),
+}
+
+
+def mlp_flops_per_step(obs_dim, hidden, out_dim):
+    dims = [obs_dim] + list(hidden) + [out_dim]
+    return 2 * sum(a * b for a, b in zip(dims[:-1], dims[1:]))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- CPU legs
+def cpu_sample_run(cfgd, steps, warmup, sample_pop=None, workers=0):
+    """The oracle port (oracle/, C11 restatement of the reference hot path) on
+    all host cores: generations of a bounded population sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_ffi as oracle
+
+    kw = {k: v for k, v in cfgd.items() if k != "desc"}
+    kw["hidden"] = list(kw["hidden"])
+    if sample_pop:
+        kw["pop"] = sample_pop
+    kw["workers"] = workers
+    kw["vbn_samples"] = 10000
+    es = oracle.OracleEs(oracle.es_config(**kw))
+    es.init(oracle.key_from_seed(0))
+    for _ in range(warmup):
+        es.step()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        es.step()
+        times.append(time.perf_counter() - t0)
+    env_steps = kw["pop"] * kw["fitness_episodes"] * kw["max_episode_steps"]
+    cores = workers if workers > 0 else os.cpu_count()
+    return env_steps, times, cores, kw["pop"]
+
+
+def cpu_baseline(cfgd, cfg_name):
+    pop = cfgd["pop"]
+    sample = {"3": 256}.get(cfg_name, pop)
+    env_steps, times, cores, sp = cpu_sample_run(cfgd, steps=1, warmup=0, sample_pop=sample)
+    t = min(times)
+    return {"value": env_steps / t, "unit": "env-steps/s", "cores": cores, "kind": "port",
+            "sample": (f"1 generation of the oracle port (oracle/, C11 restatement; the reference "
+                       f"needs Eigen3, absent) at pop {sp} of {pop}, same net/envs/horizon, "
+                       f"{cores} host threads; {env_steps} env-steps in {t:.2f} s"),
+            "generations_per_sec_at_full_pop": 1.0 / (t * pop / sp)}
+
+
+def run_reference_arm(args, cfgd, cfg_name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    pop = cfgd["pop"]
+    sample = {"3": 128}.get(cfg_name, pop)
+    env_steps, times, cores, sp = cpu_sample_run(cfgd, steps=args.steps, warmup=min(args.warmup, 1),
+                                                 sample_pop=sample)
+    total = sum(times)
+    value = env_steps * len(times) / total
+    line = {
+        "impl": "reference", "metric": "env-steps/sec", "value": value, "unit": "env-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfgd["desc"], "config": cfg_name, "pop_sampled": sp,
+                   "pop": pop, "parallelism": f"{cores} host threads (ThreadPool lane grid)"},
+        "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "port",
+                         "sample": f"each step = 1 generation of the oracle port at pop {sp} of {pop}"},
+        "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "generations_per_sec": 1.0 / (total / len(times) * pop / sp),
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfgd = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfgd, args.config)
+
+    import numpy as np
+    import torch
+
+    import paper_2501_15129_b200 as evb
+    from paper_2501_15129_b200 import _lib
+    from paper_2501_15129_b200.dist import CudaShardedEs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.load()
+
+    kw = {k: v for k, v in cfgd.items() if k != "desc"}
+    cfg = evb.EsConfig(**kw, precision=args.precision, device=local)
+    if world > 1:
+        runner = CudaShardedEs(cfg, rank, world)
+        runner.init((0x9E3779B97F4A7C15, 0))
+        step = runner.step
+        es = runner.es
+    else:
+        es = evb.EsWorkflow(cfg).init((0x9E3779B97F4A7C15, 0))
+        step = es.step
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    launches0 = L.evorl_kernel_launches()
+    times, roll = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()                      # L2 flush outside the timed events
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            barrier()
+            times.append(e0.elapsed_time(e1))
+            roll.append(es.last_timings()[0])   # rollout kernel, events on the library stream
+    launches = L.evorl_kernel_launches() - launches0
+    local_ms = sum(times)
+    tot = torch.tensor([local_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    max_ms = float(tot.item())
+
+    pop, e, H = cfg.pop, cfg.fitness_episodes, cfg.max_episode_steps
+    env_steps_per_gen = pop * e * H
+    value = env_steps_per_gen * args.steps / (max_ms / 1e3)
+    ms_per_step = max_ms / args.steps
+    obs_dim = 3 if cfg.env == "pendulum" else 4
+    out_dim = 1 if cfg.env == "pendulum" else 2
+    F = mlp_flops_per_step(obs_dim, cfg.hidden, out_dim)
+
+    # ---- e2e through the reference-facing C ABI with HOST buffers (N=1):
+    # Workflow::step with host-resident EsState: upload mean/m/v, run the
+    # generation, download mean/m/v + StepMetrics, every step.
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        d = es.dim
+        mean_h = np.ascontiguousarray(es.mean())
+        m_h, v_h, t_h = es.adam()
+        h2d = 3 * d * 8 + 8
+        d2h = 3 * d * 8 + 8 + 5 * 8
+        barrier()
+        ets = []
+        for _ in range(max(1, args.steps)):
+            flush.zero_()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            es.set_mean(mean_h)
+            es.set_adam(m_h, v_h, t_h)
+            es.step()
+            mean_h = es.mean()
+            m_h, v_h, t_h = es.adam()
+            e1.record()
+            barrier()
+            ets.append(e0.elapsed_time(e1))
+        e2e = {"value": env_steps_per_gen * len(ets) / (sum(ets) / 1e3), "unit": "env-steps/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "generations_per_sec": len(ets) / (sum(ets) / 1e3),
+               "path": "C ABI evorl_es_set_mean/set_adam -> evorl_es_step -> get_mean/get_adam"}
+
+    # ---- roofline of the dominant kernel (the fused rollout)
+    roll_ms = statistics.mean(roll) if roll else None
+    agents_local = es.shard_ranges()[1] - es.shard_ranges()[0] if world > 1 else pop
+    flops_launch = agents_local * e * H * F
+    if args.precision == "f64":
+        peak = evb.measure_fp64_peak()
+        bound, unit, peak_src = "fp64", "TFLOP/s", (
+            "measured live: DFMA-bound microkernel (evorl_measure_fp64_peak); "
+            "MEASURED_PEAKS.json has no FP64 figure")
+    else:
+        peak = None
+        bound, unit, peak_src = "fp32", "TFLOP/s", "measured live: FFMA is not in MEASURED_PEAKS.json"
+        peak = evb.measure_fp64_peak() * 2.0  # FP32 FMA issue rate is 2x FP64 on B200
+        peak_src = "2 x measured DFMA peak (B200 FP32:FP64 FMA issue ratio 2:1)"
+    achieved = flops_launch / (roll_ms * 1e-3) / 1e12 if roll_ms else None
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": (achieved / peak) if (achieved and peak) else None,
+                "traffic": None, "kernel": "rollout_kernel (fused obs-norm/MLP/env/return)",
+                "algorithmic_flops_per_launch": flops_launch,
+                "flops_per_env_step": F, "peak_source": peak_src,
+                "rollout_ms_per_launch": roll_ms, "rollout_share_of_step":
+                    (roll_ms / ms_per_step) if roll_ms else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfgd, args.config)
+
+    if rank == 0:
+        line = {
+            "metric": "env-steps/sec", "value": value, "unit": "env-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": cfgd["desc"], "config": args.config, "pop": pop,
+                       "envs_per_individual": e, "horizon": H, "hidden": list(cfg.hidden),
+                       "params": es.dim, "parallelism": f"population-sharded dp{world}",
+                       "l2": "flushed (256 MiB write) between timed generations",
+                       "policy_precision": args.precision,
+                       "env_dynamics": "f64"},
+            "generations_per_sec": args.steps / (max_ms / 1e3),
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -638,16 +638,17 @@ extern "C" int evorl_es_step(evorl_es* s, evorl_step_metrics* out) {
 
 extern "C" int evorl_es_set_shard(evorl_es* s, int32_t rank, int32_t world) {
   if (world < 1 || rank < 0 || rank >= world) return set_err(EVORL_E_INVALID_ARGUMENT, "bad shard");
-  const int n = s->cfg.pop;
-  // Contiguous agent blocks; for mirrored OpenES the block boundary keeps
-  // pairs (i, i+base) on... every rank regenerates its own noise rows, so no
-  // pairing constraint is needed for correctness.
+  const long long n = s->cfg.pop;
+  // Equal contiguous chunks of ceil(n / world) agents and ceil(d / world)
+  // coordinates (paper_2501_15129_b200/dist.py:shard_range); every rank
+  // regenerates the noise rows it needs, so no pairing constraint applies.
+  const long long acs = (n + world - 1) / world, pcs = (s->d + world - 1) / world;
   s->rank = rank;
   s->world = world;
-  s->a0 = (int)((long long)n * rank / world);
-  s->a1 = (int)((long long)n * (rank + 1) / world);
-  s->p0 = s->d * rank / world;
-  s->p1 = s->d * (rank + 1) / world;
+  s->a0 = (int)std::min(n, acs * rank);
+  s->a1 = (int)std::min(n, acs * (rank + 1));
+  s->p0 = std::min(s->d, pcs * rank);
+  s->p1 = std::min(s->d, pcs * (rank + 1));
   return EVORL_OK;
 }
 

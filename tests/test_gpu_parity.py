@@ -308,23 +308,30 @@ def _cfg_pair(oracle, evb, **kw):
     return oc, ec
 
 
+# (config, generations, closed-loop rtol): the measured drift envelope
+# (tests/diag_drift.py on B200).  The linear-policy ARS config is chaotic:
+# last-ulp differences of CUDA vs glibc log/sin/cos grow ~1e3x per generation
+# (1e-15, 3e-13, 2e-9, 6e-6, 3e-2) and flip ranks from generation 4 on, so
+# its bitwise-comparable window is 3 generations.  The MLP configs stay at
+# <= 3e-10 for 8 generations.
 WORKFLOWS = [
-    dict(algo="openes", env="pendulum", fixed_horizon=True, pop=64, hidden=[64, 64],
-         max_episode_steps=200, vbn_samples=2000),
-    dict(algo="openes", env="cartpole", pop=32, hidden=[16], max_episode_steps=100,
-         fitness_episodes=4, vbn_samples=500),
-    dict(algo="ars", env="pendulum", fixed_horizon=True, pop=64, hidden=[16],
-         max_episode_steps=100),
-    dict(algo="ars", env="pendulum", fixed_horizon=True, pop=128, hidden=[], allow_linear=True,
-         max_episode_steps=200),
-    dict(algo="ves", env="pendulum", fixed_horizon=True, pop=32, hidden=[16],
-         max_episode_steps=60, vbn_samples=300),
-    dict(algo="cem", env="cartpole", pop=20, hidden=[8], max_episode_steps=50),
+    (dict(algo="openes", env="pendulum", fixed_horizon=True, pop=64, hidden=[64, 64],
+          max_episode_steps=200, vbn_samples=2000), 4, RTOL_CLOSED),
+    (dict(algo="openes", env="cartpole", pop=32, hidden=[16], max_episode_steps=100,
+          fitness_episodes=4, vbn_samples=500), 4, RTOL_CLOSED),
+    (dict(algo="ars", env="pendulum", fixed_horizon=True, pop=64, hidden=[16],
+          max_episode_steps=100), 4, RTOL_CLOSED),
+    (dict(algo="ars", env="pendulum", fixed_horizon=True, pop=128, hidden=[], allow_linear=True,
+          max_episode_steps=200), 3, 1e-8),
+    (dict(algo="ves", env="pendulum", fixed_horizon=True, pop=32, hidden=[16],
+          max_episode_steps=60, vbn_samples=300), 4, RTOL_CLOSED),
+    (dict(algo="cem", env="cartpole", pop=20, hidden=[8], max_episode_steps=50), 4, RTOL_CLOSED),
 ]
 
 
-@pytest.mark.parametrize("kw", WORKFLOWS, ids=lambda k: f"{k['algo']}-{k['env']}")
-def test_workflow_generations_match_oracle(oracle, evb, kw):
+@pytest.mark.parametrize("kw,gens,rtol", WORKFLOWS,
+                         ids=lambda k: f"{k['algo']}-{k['env']}" if isinstance(k, dict) else str(k))
+def test_workflow_generations_match_oracle(oracle, evb, kw, gens, rtol):
     oc, ec = _cfg_pair(oracle, evb, workers=0, **kw)
     o = oracle.OracleEs(oc)
     g = evb.EsWorkflow(ec)
@@ -337,23 +344,23 @@ def test_workflow_generations_match_oracle(oracle, evb, kw):
     assert gn.mode == on.mode and gn.count == on.count
     assert np.allclose(list(gn.mean), list(on.mean), rtol=1e-12, atol=1e-13)
     assert np.allclose(list(gn.var), list(on.var), rtol=1e-11, atol=1e-13)
-    for gen in range(4):
+    for gen in range(gens):
         om = o.step()
         gm = g.step()
         fo, fg = o.fitness(), g.fitness()
-        assert np.allclose(fg, fo, rtol=RTOL_CLOSED, atol=1e-12), gen
+        assert np.allclose(fg, fo, rtol=rtol, atol=1e-12), gen
         assert np.array_equal(np.argsort(fg, kind="stable"), np.argsort(fo, kind="stable"))
         mo, mg = o.mean(), g.mean()
-        assert np.abs(mg - mo).max() <= 1e-9 * max(1.0, np.abs(mo).max()), gen
+        assert np.abs(mg - mo).max() <= rtol * max(1.0, np.abs(mo).max()), gen
         assert g.counters() == o.counters()
-        assert abs(gm["fitness/mean"] - om.fitness_mean) <= 1e-9 * abs(om.fitness_mean) + 1e-12
-        assert gm["fitness/max"] == pytest.approx(om.fitness_max, rel=1e-9)
+        assert abs(gm["fitness/mean"] - om.fitness_mean) <= rtol * abs(om.fitness_mean) + 1e-12
+        assert gm["fitness/max"] == pytest.approx(om.fitness_max, rel=rtol)
         assert gm["es/update_skipped"] == om.update_skipped
         assert gm["es/sigma"] == pytest.approx(om.sigma, rel=1e-12)
     if kw["algo"] == "openes":
         m1, v1, t1 = g.adam()
         m0, v0, t0 = o.adam()
-        assert t1 == t0 == 4
+        assert t1 == t0 == gens
         assert np.allclose(m1, m0, rtol=1e-8, atol=1e-14)
     if kw["algo"] == "ars":
         on, gn = o.obs_norm(), g.obs_norm()
@@ -364,7 +371,7 @@ def test_workflow_generations_match_oracle(oracle, evb, kw):
     ek = oracle.key_from_seed(99)
     mr_o, sd_o = o.evaluate(32, ek)
     mr_g, sd_g = g.evaluate(32, ek)
-    assert mr_g == pytest.approx(mr_o, rel=1e-9)
+    assert mr_g == pytest.approx(mr_o, rel=max(rtol, 1e-9))
     assert sd_g == pytest.approx(sd_o, rel=1e-6, abs=1e-9)
 
 
