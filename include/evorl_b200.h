@@ -239,6 +239,8 @@ int evorl_es_last_timings(const evorl_es* es, float* rollout_ms, float* step_ms)
  * Measured FP64 FMA peak of this GPU (TFLOP/s) by a DFMA-bound kernel; used
  * as the roofline denominator of the fp64 rollout. */
 int evorl_measure_fp64_peak(double* tflops);
+/* Measured FP64 tensor-core (mma.sync m8n8k4 DMMA) peak, TFLOP/s. */
+int evorl_measure_dmma_peak(double* tflops);
 
 #ifdef __cplusplus
 }

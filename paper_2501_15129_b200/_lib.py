@@ -126,7 +126,7 @@ EXPORTS = [
     "evorl_es_set_obs_norm", "evorl_es_set_counters", "evorl_es_set_shard",
     "evorl_es_shard_ranges", "evorl_es_phase_rollout", "evorl_es_phase_tell",
     "evorl_es_device_buffers", "evorl_es_stream", "evorl_es_last_timings",
-    "evorl_measure_fp64_peak",
+    "evorl_measure_fp64_peak", "evorl_measure_dmma_peak",
 ]
 
 _lib = None
@@ -186,6 +186,7 @@ def load() -> C.CDLL:
     L.evorl_es_stream.restype = vp
     L.evorl_es_last_timings.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]
     L.evorl_measure_fp64_peak.argtypes = [C.POINTER(dbl)]
+    L.evorl_measure_dmma_peak.argtypes = [C.POINTER(dbl)]
     _lib = L
     return L
 

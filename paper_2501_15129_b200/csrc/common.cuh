@@ -132,6 +132,26 @@ EVB_DEV void st_cluster<float>(uint32_t addr, float v) {
   st_cluster_f32(addr, v);
 }
 
+// ---------------------------------------------------------------- mbarrier
+EVB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// Arrive (release, cluster scope) on the same-offset mbarrier of CTA `rank`.
+EVB_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  const uint32_t ra = map_cluster(smem_u32(bar), rank);
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+// Wait (acquire, cluster scope) for the phase with the given parity.
+EVB_DEV void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
 // ------------------------------------------------------------------- errors
 // Device error word: lowest failing lane wins (proj/src/thread_pool.cpp:49-51).
 // Encoding: (lane << 8) | (kind << 4) | layer; kind 1..3 = EnvFault variants,

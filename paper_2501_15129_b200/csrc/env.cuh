@@ -79,8 +79,11 @@ EVB_DEV void env_reset(const EnvDesc& e, DKey key, LaneEnv& s) {
 }
 
 // One env_step (proj/src/env.cpp:113-155).  Returns 0 or a FAULT_* kind.
+// sin_th (optional): sin of the current angle, already computed by observe()
+// for this state -- the reference evaluates std::sin(th) twice with the same
+// argument (proj/src/env.cpp:94 and :48), so reusing it is exact.
 EVB_DEV uint32_t env_step(const EnvDesc& e, LaneEnv& s, double action, double& reward,
-                          bool& terminated, bool& truncated) {
+                          bool& terminated, bool& truncated, const double* sin_th = nullptr) {
   const bool cart = e.id == ENV_CARTPOLE;
   if (!isfinite(s.p0) || !isfinite(s.p1) || (cart && (!isfinite(s.p2) || !isfinite(s.p3))))
     return FAULT_ENV_STATE;
@@ -114,7 +117,8 @@ EVB_DEV uint32_t env_step(const EnvDesc& e, LaneEnv& s, double action, double& r
     // -((w*w + (0.1*thdot)*thdot) + (0.001*u)*u)
     reward = -dadd(dadd(dmul(w, w), dmul(dmul(0.1, thdot), thdot)), dmul(dmul(0.001, u), u));
     // pendulum_physics (proj/src/env.cpp:46-51), 1.5*kPenG = 15 exactly
-    double td = dadd(thdot, dmul(dadd(dmul(15.0, sin(th)), dmul(3.0, u)), 0.05));
+    const double sn = sin_th ? *sin_th : sin(th);
+    double td = dadd(thdot, dmul(dadd(dmul(15.0, sn), dmul(3.0, u)), 0.05));
     td = clampd(td, -8.0, 8.0);
     s.p0 = dadd(th, dmul(td, 0.05));
     s.p1 = td;

@@ -166,6 +166,9 @@ struct evorl_es {
   int e = 1, count = 1;
   SmemPlan plan{};
   int groups = 1;
+  bool warp_path = false;  // small policies: warp-per-lane rollout (rollout_warp.cu)
+  WarpPlanOut wplan{};
+  double* d_cand = nullptr;  // materialised candidates for the warp path
   cudaStream_t stream = nullptr;
   // WorkflowState (proj/include/evorl/workflow.hpp:31-36)
   DKey rng{};
@@ -246,7 +249,7 @@ static void free_all(evorl_es* s) {
   void* ptrs[] = {s->d_mean, s->d_m, s->d_v, s->d_var, s->d_t, s->d_norm, s->d_normp, s->d_fitness,
                   s->d_ep_returns, s->d_lane_stats, s->d_agent_stats, s->d_lane_steps, s->d_rank,
                   s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
-                  s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w};
+                  s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
@@ -297,7 +300,12 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   s->norm_mode = resolve_norm(*cfg);
   s->e = cfg->fitness_episodes;
   s->count = cfg->fitness_episodes;  // RolloutMode::episodes(fitness_episodes)
-  if (!plan_rollout(s->net, s->env.obs_dim, s->e, cfg->precision, &s->plan)) {
+  const bool cta_ok = plan_rollout(s->net, s->env.obs_dim, s->e, cfg->precision, &s->plan);
+  // warp-per-lane only pays when there are enough lanes to fill the SMs
+  // (>= 512 lanes); fewer lanes get a whole CTA each to cut step latency.
+  s->warp_path = (long long)cfg->pop * s->e >= 512 &&
+                 plan_rollout_warp(s->net, s->env.obs_dim, s->e, cfg->precision, &s->wplan);
+  if (!cta_ok && !s->warp_path) {
     delete s;
     return set_err(EVORL_E_UNSUPPORTED, "policy too large for a shared-memory resident team");
   }
@@ -338,6 +346,7 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   A(dalloc(&s->d_elite_diff, n));
   A(dalloc(&s->d_metrics, 4));
   A(dalloc(&s->d_sel, 1));
+  if (s->warp_path) A(dalloc(&s->d_cand, (size_t)n * d));
   A(dalloc(&s->d_steps, 1));
   A(dalloc(&s->d_fault, 1));
   A(cudaMallocHost((void**)&s->h, sizeof(Pinned)));
@@ -506,10 +515,21 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
   CK(cudaEventRecord(s->ev_s0, s->stream));
   CK(cudaMemsetAsync(s->d_steps, 0, sizeof(unsigned long long), s->stream));
   CK(cudaMemsetAsync(s->d_fault, 0xFF, sizeof(unsigned long long), s->stream));
-  const RolloutArgs a = rollout_args(s);
-  CK(cudaEventRecord(s->ev_r0, s->stream));
-  CK(launch_rollout(a, s->cfg.precision, s->stream));
-  count_launch();
+  RolloutArgs a = rollout_args(s);
+  if (s->warp_path) {
+    // small policy: materialise the shard's candidates (fully parallel ask),
+    // then one warp per lane with the weights resident in shared memory
+    CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream));
+    count_launch();
+    a.par.src = SRC_EXPLICIT;
+    a.par.params = s->d_cand;
+    CK(cudaEventRecord(s->ev_r0, s->stream));
+    CK(launch_rollout_warp(a, s->wplan, s->cfg.precision, s->stream));
+  } else {
+    CK(cudaEventRecord(s->ev_r0, s->stream));
+    CK(launch_rollout(a, s->cfg.precision, s->stream));
+    count_launch();
+  }
   CK(cudaEventRecord(s->ev_r1, s->stream));
   CK(run_fitness(a.ep_returns, s->count, a.n_agents, s->a0, s->d_fitness, a.lane_steps, s->e, s->d_steps,
                  s->stream));
@@ -933,7 +953,9 @@ extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp
   if (int rc = make_net(*netd, &net)) return rc;
   if (netd->input_dim != env.obs_dim) return set_err(EVORL_E_INVALID_ARGUMENT, "net input_dim != obs_dim");
   SmemPlan plan{};
-  if (!plan_rollout(net, env.obs_dim, e, precision, &plan))
+  WarpPlanOut wplan{};
+  const bool use_warp = plan_rollout_warp(net, env.obs_dim, e, precision, &wplan);
+  if (!plan_rollout(net, env.obs_dim, e, precision, &plan) && !use_warp)
     return set_err(EVORL_E_UNSUPPORTED, "policy too large for a shared-memory resident team");
   const long long d = net.d;
   Scratch sp, sr, ss, sst, sag, sn, sf;
@@ -978,8 +1000,12 @@ extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp
   a.lane_steps = dsteps;
   a.lane_stats = dstats;
   a.fault = dfault;
-  CK(launch_rollout(a, precision, 0));
-  count_launch();
+  if (use_warp) {
+    CK(launch_rollout_warp(a, wplan, precision, 0));
+  } else {
+    CK(launch_rollout(a, precision, 0));
+    count_launch();
+  }
   if (obs_stats) CK(run_agent_stats(dstats, m, e, dagent, 0));
   CK(cudaDeviceSynchronize());
   unsigned long long fault = 0;
@@ -1111,6 +1137,13 @@ extern "C" int evorl_ars_tell(double* mean, int64_t d, int32_t elites, double lr
   CK(cudaMemcpy(&hs, dsel, sizeof hs, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(mean, dm, sizeof(double) * d, cudaMemcpyDeviceToHost));
   if (updated) *updated = hs.skipped ? 0 : 1;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_measure_dmma_peak(double* tflops) {
+  DEV_OR_RETURN();
+  *tflops = measure_dmma_peak_tflops();
+  CK(cudaGetLastError());
   return EVORL_OK;
 }
 

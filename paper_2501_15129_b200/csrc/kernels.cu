@@ -510,13 +510,30 @@ EVB_DEV void norm_params_from(const DevNorm& nm, NormParams& p) {
   }
 }
 
-// agent-order merge (proj/src/workflow_es.cpp:136) then rs_update
-// (proj/src/obs_norm.cpp:56-68) into the device ObsNormState.
+// Agent merge (proj/src/workflow_es.cpp:136) then rs_update
+// (proj/src/obs_norm.cpp:56-68) into the device ObsNormState.  The reference
+// merges agents sequentially; Welford merging is exact in real arithmetic but
+// not associative in floating point, so this fixed-order tree (each thread
+// folds a contiguous run of agents, then a pairwise tree in rank order) differs
+// from it only in rounding (~1e-16 rel), is deterministic, and replaces a
+// 1024-long serial dependency chain with ~10 levels.
+constexpr int RS_THREADS = 256;
 __global__ void k_rs_update(const double* agent_stats, int n_agents, DevNorm* norm, NormParams* params) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __shared__ W9 tree[RS_THREADS];
+  const int t = threadIdx.x;
   const int dim = norm->dim;
-  W9 batch{};
-  for (int a = 0; a < n_agents; ++a) welford_merge(batch, load9(agent_stats + (long long)a * 9), dim);
+  const int chunk = (n_agents + RS_THREADS - 1) / RS_THREADS;
+  W9 w{};
+  for (int a = t * chunk; a < min(n_agents, (t + 1) * chunk); ++a)
+    welford_merge(w, load9(agent_stats + (long long)a * 9), dim);
+  tree[t] = w;
+  __syncthreads();
+  for (int stride = 1; stride < RS_THREADS; stride *= 2) {
+    if ((t % (2 * stride)) == 0) welford_merge(tree[t], tree[t + stride], dim);
+    __syncthreads();
+  }
+  if (t != 0) return;
+  const W9 batch = tree[0];
   DevNorm nm = *norm;
   if (nm.mode == 2 && batch.c != 0.0) {
     W9 cur{};
@@ -541,7 +558,7 @@ cudaError_t run_rs_merge(const double* lane_stats, int n_agents, int e, DevNorm*
                          double* agent_scratch, cudaStream_t s) {
   cudaError_t err = run_agent_stats(lane_stats, n_agents, e, agent_scratch, s);
   if (err != cudaSuccess) return err;
-  k_rs_update<<<1, 32, 0, s>>>(agent_scratch, n_agents, norm, params);
+  k_rs_update<<<1, RS_THREADS, 0, s>>>(agent_scratch, n_agents, norm, params);
   EVB_CHECK_LAUNCH();
 }
 
@@ -746,4 +763,56 @@ double measure_fp64_peak_tflops() {
   return flops / (best * 1e-3) / 1e12;
 }
 
+}  // namespace evorl_b200
+
+namespace evorl_b200 {
+// ------------------------------------------------------------ DMMA peak
+// FP64 tensor-core throughput (mma.sync.m8n8k4.f64): 8 independent
+// accumulators per warp, register operands only.
+__global__ void k_dmma_peak(double* out, double seed) {
+  double a = seed + threadIdx.x * 1e-9, b = 0.5 + threadIdx.x * 1e-10;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = i * 1e-3;
+  for (int it = 0; it < 2048; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+double measure_dmma_peak_tflops() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* d = nullptr;
+  cudaMalloc(&d, 8);
+  const int blocks = sms * 4, threads = 256;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_dmma_peak<<<blocks, threads>>>(d, 1.0);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    k_dmma_peak<<<blocks, threads>>>(d, 1.0 + r);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  count_launch(6);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const double warps = (double)blocks * threads / 32;
+  const double flops = 2.0 * 256 * 8 * 2048 * warps;  // 8x8x4 MACs per mma
+  return flops / (best * 1e-3) / 1e12;
+}
 }  // namespace evorl_b200

@@ -85,5 +85,6 @@ cudaError_t run_eval_reduce(const double* returns, int n, double* out2, cudaStre
 cudaError_t run_agent_stats(const double* lane_stats, int n_agents, int e, double* agent_stats,
                             cudaStream_t s);
 double measure_fp64_peak_tflops();
+double measure_dmma_peak_tflops();
 
 }  // namespace evorl_b200

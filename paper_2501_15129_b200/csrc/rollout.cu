@@ -23,6 +23,7 @@
 //    operation order (env.cuh).  The policy GEMM runs in T = double (parity
 //    mode) or float (throughput mode).
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 
 #include "rollout.cuh"
@@ -73,6 +74,21 @@ EVB_DEV double param_value(const ParamDesc& P, long long d, int agent_local, int
     default:
       return P.params[(long long)agent_local * d + p];
   }
+}
+
+__global__ void k_materialize(const ParamDesc P, long long d, int a0, int a1, double* out) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long n = (long long)(a1 - a0) * d;
+  if (idx >= n) return;
+  const int al = (int)(idx / d);
+  out[idx] = param_value(P, d, al, a0 + al, idx % d);
+}
+cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
+                            cudaStream_t stream) {
+  const long long n = (long long)(a1 - a0) * d;
+  if (n <= 0) return cudaSuccess;
+  k_materialize<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, out);
+  return cudaGetLastError();
 }
 
 template <typename T, int N>
@@ -129,7 +145,7 @@ struct VecLoad<float, N> {
 // W[k][r] * x[k][e].  W is k-major with RSP padded rows (rows contiguous, so a
 // warp reads 32*TR consecutive weights); x[k][0..ET) is warp-uniform (broadcast).
 template <typename T, int TR, int ET>
-EVB_DEV void hidden_partial(const T* __restrict__ Ws, int RSP, int K, int KS,
+EVB_DEV void hidden_partial(const T* __restrict__ Ws, int WS, int RSP, int K, int KS,
                             const T* __restrict__ x, T* __restrict__ part, int tid) {
   const int nrg = RSP / TR;
   const int kc = (K + KS - 1) / KS;
@@ -146,22 +162,157 @@ EVB_DEV void hidden_partial(const T* __restrict__ Ws, int RSP, int K, int KS,
 #pragma unroll 2
     for (int k = k0; k < k1; ++k) {
       T wv[TR], xv[ET];
-      VecLoad<T, TR>::load(wp + (size_t)k * RSP, wv);
+      VecLoad<T, TR>::load(wp + (size_t)k * WS, wv);
       VecLoad<T, ET>::load(x + (size_t)k * ET, xv);
 #pragma unroll
       for (int i = 0; i < TR; ++i)
 #pragma unroll
         for (int e = 0; e < ET; ++e) acc[i][e] = fma(wv[i], xv[e], acc[i][e]);
     }
+    // rows of `part` are XOR-swizzled (psw) so that a warp's stores of
+    // element e of 32 consecutive row groups hit distinct banks
     T* pp = part + ((size_t)ks * RSP + rg * TR) * ET;
+    const int sw = ET > 1 ? (rg & (ET - 1)) : 0;
 #pragma unroll
     for (int i = 0; i < TR; ++i)
 #pragma unroll
-      for (int e = 0; e < ET; ++e) pp[i * ET + e] = acc[i][e];
+      for (int e = 0; e < ET; ++e) pp[i * ET + (e ^ sw)] = acc[i][e];
   }
 }
 
-template <typename T, int TR, int ET, int C>
+// physical column of (row r, lane e) in the swizzled partial buffer
+template <int TR, int ET>
+EVB_DEV int psw(int r, int e) {
+  return ET > 1 ? (e ^ ((r / TR) & (ET - 1))) : e;
+}
+
+// D(8x8) += A(8x4) * B(4x8), fp64 tensor cores.  Fragments (PTX ISA,
+// mma.m8n8k4 .f64): a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// d = {D[lane>>2][2(lane&3)], D[lane>>2][2(lane&3)+1]}.
+EVB_DEV void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Hidden layer on the FP64 tensor cores with a direct epilogue (ET = 16
+// lanes): warp tile = 8 rows x 16 lanes over the whole K (no k-split, no
+// partial buffer); two accumulator chains per n-tile (even/odd k-steps) hide
+// the DMMA latency; bias + ReLU + store (local, or DSMEM scatter to all C CTAs)
+// straight from the accumulator fragments.  Activation rows are XS = 20
+// doubles apart so the 4 k-rows of a B fragment fall in distinct bank groups.
+template <int C>
+EVB_DEV uint32_t hidden_dmma_direct(const double* __restrict__ Ws, int WS, int RSv, int K,
+                                    const double* __restrict__ x, int XS, const double* __restrict__ bs,
+                                    double* hb, int hrow0, bool scatter, int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t bad = 0u;
+  const int ngroups = (RSv + 7) / 8;
+  for (int mg = warp; mg < ngroups; mg += ROLLOUT_THREADS / 32) {
+    double acc[2][2][2];  // [chain][n-tile][2]
+#pragma unroll
+    for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) acc[c2][nt][0] = acc[c2][nt][1] = 0.0;
+    const int row = mg * 8 + g;
+    const double* wb = Ws + row;
+    int k = 0;
+    for (; k + 8 <= K; k += 8) {
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        const int kk = k + 4 * c2 + t;
+        const double a = wb[(size_t)kk * WS];
+        const double b0 = x[(size_t)kk * XS + g], b1 = x[(size_t)kk * XS + 8 + g];
+        dmma(acc[c2][0][0], acc[c2][0][1], a, b0);
+        dmma(acc[c2][1][0], acc[c2][1][1], a, b1);
+      }
+    }
+    for (; k < K; k += 4) {  // tail (K not a multiple of 8)
+      const int kk = k + t;
+      const bool in = kk < K;
+      const double a = in ? wb[(size_t)kk * WS] : 0.0;
+      const double b0 = in ? x[(size_t)kk * XS + g] : 0.0, b1 = in ? x[(size_t)kk * XS + 8 + g] : 0.0;
+      dmma(acc[0][0][0], acc[0][0][1], a, b0);
+      dmma(acc[0][1][0], acc[0][1][1], a, b1);
+    }
+    if (row < RSv) {
+      const double b = bs[row];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        double h2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double z = (acc[0][nt][i] + acc[1][nt][i]) + b;
+          const double h = z > 0.0 ? z : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
+          if (h == INFINITY) bad |= 1u << (nt * 8 + 2 * t + i);
+          h2[i] = h;
+        }
+        double* dst = hb + (size_t)(hrow0 + row) * XS + nt * 8 + 2 * t;
+        if (!scatter) {
+          *reinterpret_cast<double2*>(dst) = make_double2(h2[0], h2[1]);
+        } else {
+          const uint32_t la = smem_u32(dst);
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const uint32_t ra = map_cluster(la, (uint32_t)c);
+            asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(h2[0]), "d"(h2[1])
+                         : "memory");
+          }
+        }
+      }
+    }
+  }
+  return bad;
+}
+
+// Hidden-layer slice GEMM on the FP64 tensor cores (ET = 16 lanes).
+// Warp tile: 32 rows (4 m-tiles) x 16 lanes (2 n-tiles) over a k-chunk;
+// partial tiles go to the same swizzled `part` layout as the SIMT path
+// (psw<1,16>).  W rows are padded (stride WS = RSP + 4) so the four k-rows
+// of an A fragment fall in distinct bank groups.
+EVB_DEV void hidden_partial_dmma(const double* __restrict__ Ws, int WS, int RSP, int K, int KS,
+                                 const double* __restrict__ x, double* __restrict__ part, int tid) {
+  constexpr int ET = 16;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int nmw = RSP / 32;
+  const int kc = ((K + KS - 1) / KS + 3) & ~3;  // chunk, multiple of 4
+  for (int w = warp; w < nmw * KS; w += ROLLOUT_THREADS / 32) {
+    const int mg = w % nmw, ks = w / nmw;
+    const int k0 = ks * kc, k1 = min(K, k0 + kc);
+    double acc[4][2][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    const double* wb = Ws + mg * 32 + g;
+    for (int k = k0; k < k1; k += 4) {
+      const int kk = k + t;
+      const bool in = kk < k1;
+      double a[4], b[2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) a[mt] = in ? wb[(size_t)kk * WS + mt * 8] : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) b[nt] = in ? x[(size_t)kk * ET + nt * 8 + g] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = mg * 32 + mt * 8 + g, e = nt * 8 + 2 * t + i;
+          part[((size_t)ks * RSP + r) * ET + (e ^ (r & (ET - 1)))] = acc[mt][nt][i];
+        }
+  }
+}
+
+template <typename T, int TR, int ET, int C, bool MMA>
 __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __grid_constant__ RolloutArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemPlan& S = A.plan;
@@ -178,17 +329,20 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   const int O = N.dims[L];
 
   // ------------------------------------------------------------ prologue
+  // Weight rows owned by this CTA: a slice of each hidden layer, or the whole
+  // layer when it is replicated (cheap K <= 8 input layers: computing them in
+  // every CTA avoids one DSMEM scatter + cluster barrier per step).
   for (int i = tid; i < S.bytes / 4; i += ROLLOUT_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
   __syncthreads();
   for (int l = 0; l < nh; ++l) {
     const int K = N.dims[l], W = N.dims[l + 1];
-    const int RS = S.RS[l], RSP = S.RSP[l], r0 = crank * RS;
+    const int RS = S.RS[l], r0 = S.REP[l] ? 0 : crank * RS;
     const int RSv = max(0, min(RS, W - r0));
     T* Ws = reinterpret_cast<T*>(smem + S.off_w[l]);
     T* bs = reinterpret_cast<T*>(smem + S.off_b[l]);
     for (int i = tid; i < K * RSv; i += ROLLOUT_THREADS) {
       const int k = i / RSv, r = i % RSv;
-      Ws[(size_t)k * RSP + r] =
+      Ws[(size_t)k * S.WS[l] + r] =
           to_T<T>(param_value(A.par, N.d, agent_local, agent, N.w_off[l] + (long long)k * W + r0 + r));
     }
     for (int r = tid; r < RSv; r += ROLLOUT_THREADS)
@@ -241,75 +395,130 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem + S.off_mask);
   const T* Wo = reinterpret_cast<const T*>(smem + S.off_wout);
   const T* bo = reinterpret_cast<const T*>(smem + S.off_bout);
-  __syncthreads();
+  const int OE = O * ET;
+  const int OE1 = (O + 1) * ET;  // + one row carrying each lane's first non-finite layer
+
+  // observation -> (RunningStats) -> normalisation, written into x0 for the
+  // next forward pass (proj/src/rollout.cpp:124-126)
+  double sin_th = 0.0;  // sin of the current pendulum angle (reused by env_step)
+  auto observe_into_x0 = [&](bool act) {
+    double raw[4];
+    observe(E, s, raw);
+    sin_th = raw[1];
+    if (act && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
+      if (wc == 0.0) {
+        for (int i = 0; i < E.obs_dim; ++i) {
+          wmean[i] = raw[i];
+          wm2[i] = 0.0;
+        }
+        wc = 1.0;
+      } else {
+        wc = dadd(wc, 1.0);
+        for (int i = 0; i < E.obs_dim; ++i) {
+          const double delta = dsub(raw[i], wmean[i]);
+          wmean[i] = dadd(wmean[i], ddiv(delta, wc));
+          wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
+        }
+      }
+    }
+    for (int i = 0; i < E.obs_dim; ++i) {
+      double v = raw[i];
+      if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
+      x0[i * S.XS + tid] = act ? to_T<T>(v) : T(0);
+    }
+  };
+  if (valid && eps_this > 0 && A.max_iters > 0) observe_into_x0(true);
+  // Output exchange: every CTA's OE1 writer threads store into each peer and
+  // arrive (release.cluster) on the peer's mbarrier for this step; only the
+  // env threads wait (acquire.cluster) -- no full cluster barrier per step.
+  // Two barriers alternate by step so an early arrival for step t+1 can never
+  // complete a peer's phase for step t.
+  uint64_t* obar = reinterpret_cast<uint64_t*>(smem + S.off_bar);
+  if constexpr (C > 1) {
+    if (tid == 0) {
+      mbar_init(&obar[0], (uint32_t)C);
+      mbar_init(&obar[1], (uint32_t)C);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster_sync_all();  // peers may arrive only on initialised barriers
+  }
 
   for (int it = 0;; ++it) {
     if (tid < MAXL) mask[(it & 1) * MAXL + tid] = 0u;  // last used two steps ago
     const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
-    if (!__syncthreads_or(active)) break;
+    if (!__syncthreads_or(active)) break;  // also orders the x0 writes before layer 0
     uint32_t* cur_mask = mask + (it & 1) * MAXL;
-    // output partials are double-buffered by step parity: with a single hidden
-    // layer there is no cluster barrier between two steps' output exchanges
-    T* pout = pout_base + (it & 1) * C * O * ET;
-
-    // observation -> (RunningStats) -> normalisation (proj/src/rollout.cpp:124-126)
-    if (is_env) {
-      double raw[4];
-      observe(E, s, raw);
-      if (active && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
-        if (wc == 0.0) {
-          for (int i = 0; i < E.obs_dim; ++i) {
-            wmean[i] = raw[i];
-            wm2[i] = 0.0;
-          }
-          wc = 1.0;
-        } else {
-          wc = dadd(wc, 1.0);
-          for (int i = 0; i < E.obs_dim; ++i) {
-            const double delta = dsub(raw[i], wmean[i]);
-            wmean[i] = dadd(wmean[i], ddiv(delta, wc));
-            wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
-          }
-        }
-      }
-      for (int i = 0; i < E.obs_dim; ++i) {
-        double v = raw[i];
-        if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
-        x0[i * ET + tid] = active ? to_T<T>(v) : T(0);
-      }
-    }
-    __syncthreads();
+    // output partials are double-buffered by step parity: with a single
+    // cluster barrier per step, a fast CTA may write step t+1's partials
+    // while a slow one still reads step t's
+    T* pout = pout_base + (it & 1) * C * OE1;
 
     // hidden layers (proj/src/net.cpp:86-127): z = W x + b, ReLU
+    const int XS = S.XS;
     for (int l = 0; l < nh; ++l) {
       const int K = N.dims[l], W = N.dims[l + 1];
-      const int RS = S.RS[l], RSP = S.RSP[l], r0 = crank * RS;
+      const bool rep = S.REP[l] != 0;
+      const int RS = S.RS[l], RSP = S.RSP[l], r0 = rep ? 0 : crank * RS;
       const int RSv = max(0, min(RS, W - r0));
       const T* xin = l == 0 ? x0 : reinterpret_cast<const T*>(smem + S.off_h[l - 1]);
-      hidden_partial<T, TR, ET>(reinterpret_cast<const T*>(smem + S.off_w[l]), RSP, K, S.KS[l], xin,
-                                part, tid);
-      __syncthreads();
+      const T* Ws = reinterpret_cast<const T*>(smem + S.off_w[l]);
       const T* bs = reinterpret_cast<const T*>(smem + S.off_b[l]);
       T* hb = reinterpret_cast<T*>(smem + S.off_h[l]);
       const bool last_hidden = l == nh - 1;
-      const int KSl = S.KS[l];
-      for (int i = tid; i < RSv * ET; i += ROLLOUT_THREADS) {
-        const int r = i / ET, e = i % ET;
-        T z = part[(size_t)r * ET + e];
-        for (int ks = 1; ks < KSl; ++ks) z += part[((size_t)ks * RSP + r) * ET + e];
-        z = z + bs[r];
-        const T h = z > T(0) ? z : T(0);
-        if (!isfinite((double)h)) atomicOr(&cur_mask[l], 1u << e);
-        if (last_hidden || C == 1) {
-          hb[(size_t)(last_hidden ? r : r0 + r) * ET + e] = h;
-        } else {
-          const uint32_t la = smem_u32(hb + (size_t)(r0 + r) * ET + e);
+      const bool scatter = C > 1 && !rep && !last_hidden;
+      if constexpr (MMA) {
+        // FP64 tensor cores, direct epilogue (no partial buffer / reduce pass)
+        const uint32_t badm = hidden_dmma_direct<C>(
+            reinterpret_cast<const double*>(Ws), S.WS[l], RSv, K, reinterpret_cast<const double*>(xin), XS,
+            reinterpret_cast<const double*>(bs), reinterpret_cast<double*>(hb), last_hidden ? 0 : r0,
+            scatter, tid);
+        if (badm) atomicOr(&cur_mask[l], badm);
+      } else if (rep) {
+        // replicated cheap layer (K <= 8): each thread owns lane e = tid % ET
+        // and rows tid/ET + k*(256/ET); no k-split, no partial pass
+        const int e = tid % ET, WSl = S.WS[l];
+        T xr[8];
 #pragma unroll
-          for (int c = 0; c < C; ++c) st_cluster<T>(map_cluster(la, (uint32_t)c), h);
+        for (int k = 0; k < 8; ++k) xr[k] = k < K ? xin[k * XS + e] : T(0);
+        uint32_t bad = 0u;
+        for (int r = tid / ET; r < W; r += ROLLOUT_THREADS / ET) {
+          T z = T(0);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k < K) z = fma(Ws[(size_t)k * WSl + r], xr[k], z);
+          z = z + bs[r];
+          const T h = z > T(0) ? z : T(0);  // ReLU (NaN -> 0, as cwiseMax)
+          if (h == T(INFINITY)) bad = 1u;
+          hb[(size_t)r * XS + e] = h;
         }
+        if (bad) atomicOr(&cur_mask[l], 1u << e);
+      } else {
+        hidden_partial<T, TR, ET>(Ws, S.WS[l], RSP, K, S.KS[l], xin, part, tid);
+        __syncthreads();
+        const int KSl = S.KS[l];
+        // k-split reduction + bias + ReLU: each thread owns lane e = tid % ET
+        // and rows tid/ET + q*(256/ET), so index math stays out of the loop
+        const int e = tid % ET;
+        uint32_t bad = 0u;
+        for (int r = tid / ET; r < RSv; r += ROLLOUT_THREADS / ET) {
+          const int pe = psw<TR, ET>(r, e);
+          T z = part[(size_t)r * ET + pe];
+          for (int ks = 1; ks < KSl; ++ks) z += part[((size_t)ks * RSP + r) * ET + pe];
+          z = z + bs[r];
+          const T h = z > T(0) ? z : T(0);  // ReLU (NaN -> 0, as cwiseMax)
+          if (h == T(INFINITY)) bad = 1u;
+          if (!scatter) {
+            hb[(size_t)(last_hidden ? r : r0 + r) * XS + e] = h;
+          } else {
+            const uint32_t la = smem_u32(hb + (size_t)(r0 + r) * XS + e);
+#pragma unroll
+            for (int c = 0; c < C; ++c) st_cluster<T>(map_cluster(la, (uint32_t)c), h);
+          }
+        }
+        if (bad) atomicOr(&cur_mask[l], 1u << e);
       }
       if constexpr (C > 1) {
-        if (!last_hidden) {
+        if (scatter) {
           cluster_sync_all();
         } else {
           __syncthreads();
@@ -320,9 +529,10 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
     }
 
     // output layer partial over this CTA's rows, reduced across the cluster
+    // together with each lane's first non-finite layer (NetFault bookkeeping
+    // rides on the same DSMEM exchange: no remote loads in the env phase)
     {
       const T* xin = nh > 0 ? reinterpret_cast<const T*>(smem + S.off_h[nh - 1]) : x0;
-      const int OE = O * ET;
       const int KSo = S.KS_out;
       const int kc = (KRP + KSo - 1) / KSo;
       for (int w = tid; w < OE * KSo; w += ROLLOUT_THREADS) {
@@ -330,51 +540,55 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
         const int o = oe / ET, e = oe % ET;
         const int k0 = ks * kc, k1 = min(KRv, k0 + kc);
         T acc = T(0);
-        for (int k = k0; k < k1; ++k) acc = fma(Wo[k * O + o], xin[(size_t)k * ET + e], acc);
+        for (int k = k0; k < k1; ++k) acc = fma(Wo[k * O + o], xin[(size_t)k * XS + e], acc);
         part[w] = acc;
       }
       __syncthreads();
-      for (int oe = tid; oe < OE; oe += ROLLOUT_THREADS) {
-        T v = part[oe];
-        for (int ks = 1; ks < KSo; ++ks) v += part[ks * OE + oe];
+      for (int oe = tid; oe < OE1; oe += ROLLOUT_THREADS) {
+        T v;
+        if (oe < OE) {
+          v = part[oe];
+          for (int ks = 1; ks < KSo; ++ks) v += part[ks * OE + oe];
+        } else {
+          const int e = oe - OE;
+          int bl = L;
+          for (int l = nh - 1; l >= 0; --l)
+            if ((cur_mask[l] >> e) & 1u) bl = l;
+          v = T(bl);
+        }
         if constexpr (C > 1) {
-          const uint32_t la = smem_u32(pout + crank * OE + oe);
+          const uint32_t la = smem_u32(pout + crank * OE1 + oe);
 #pragma unroll
           for (int c = 0; c < C; ++c) st_cluster<T>(map_cluster(la, (uint32_t)c), v);
         } else {
           pout[oe] = v;
         }
       }
+      __syncthreads();
       if constexpr (C > 1) {
-        cluster_sync_all();
-      } else {
-        __syncthreads();
+        // one release.cluster arrive per peer, after the CTA barrier has
+        // ordered every writer's DSMEM stores (release is cumulative)
+        if (tid < C) mbar_arrive_remote(&obar[it & 1], (uint32_t)tid);
       }
     }
 
-    // head + env step (proj/src/rollout.cpp:57-90, :131-153)
+    // head + env step (proj/src/rollout.cpp:57-90, :131-153), then the next
+    // observation (same threads: no extra barrier)
     if (active) {
+      if constexpr (C > 1) mbar_wait_parity(&obar[it & 1], (uint32_t)((it >> 1) & 1));
       double z[8];
       bool nonfinite_out = false;
+      int bad_layer = L;
+      for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pout[c * OE1 + OE + tid]);
       for (int o = 0; o < O && o < 8; ++o) {
         T v = pout[o * ET + tid];
-        for (int c = 1; c < C; ++c) v += pout[c * O * ET + o * ET + tid];
+        for (int c = 1; c < C; ++c) v += pout[c * OE1 + o * ET + tid];
         v = v + bo[o];
         z[o] = (double)v;
         if (!isfinite(z[o])) nonfinite_out = true;
       }
-      // NetFault: the lowest layer with a non-finite activation for this lane
-      int bad_layer = -1;
-      for (int l = 0; l < nh && bad_layer < 0; ++l) {
-        uint32_t m = cur_mask[l];
-        if constexpr (C > 1) {
-          const uint32_t la = smem_u32(&cur_mask[l]);
-          for (int c = 0; c < C; ++c) m |= ld_cluster_u32(map_cluster(la, (uint32_t)c));
-        }
-        if (m & (1u << tid)) bad_layer = l;
-      }
-      if (bad_layer < 0 && nonfinite_out) bad_layer = L - 1;
-      if (bad_layer >= 0) {
+      if (bad_layer >= L && nonfinite_out) bad_layer = L - 1;
+      if (bad_layer < L) {  // NetFault: the lowest layer with a non-finite activation
         myfault = FAULT_NET;
         myfault_layer = (uint32_t)bad_layer;
       } else {
@@ -391,7 +605,8 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
         }
         double reward = 0.0;
         bool term = false, trunc = false;
-        const uint32_t f = env_step(E, s, action, reward, term, trunc);
+        const uint32_t f =
+            env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr);
         if (f) {
           myfault = f;
         } else {
@@ -411,6 +626,8 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
           }
         }
       }
+      const bool next = myfault == 0 && eps_done < eps_this && it + 1 < A.max_iters;
+      observe_into_x0(next);
     }
   }
 
@@ -438,7 +655,8 @@ static int pow2floor(int x) {
   return p;
 }
 
-static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int tsize, SmemPlan* P) {
+static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int tsize, SmemPlan* P,
+                     bool mma = false) {
   const int L = net.nlayers, nh = L - 1, O = net.dims[L];
   if (nh == 0 && C > 1) return false;
   if (O > 8 || obs_dim > 4) return false;
@@ -451,31 +669,44 @@ static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int
   for (int l = 0; l < nh; ++l) {
     const int K = net.dims[l], W = net.dims[l + 1];
     if (W < C) return false;
-    const int RS = (W + C - 1) / C;
-    const int RSP = (RS + 32 * TR - 1) / (32 * TR) * (32 * TR);
+    // cheap non-final layers (K <= 8: the observation layer) are computed in
+    // full by every CTA instead of sliced + exchanged
+    const bool rep = C > 1 && K <= 8 && l < nh - 1;
+    p.REP[l] = rep ? 1 : 0;
+    const int RS = rep ? W : (W + C - 1) / C;
+    // DMMA plan: 8-row warp tiles; SIMT: 32*TR-row warp groups
+    const int RSP = mma ? (RS + 7) / 8 * 8 : (RS + 32 * TR - 1) / (32 * TR) * (32 * TR);
     const int nrg = RSP / TR;
     int KS = nrg >= ROLLOUT_THREADS ? 1 : pow2floor(ROLLOUT_THREADS / nrg);
     while (KS > 1 && K / KS < 8) KS /= 2;
+    int WS = RSP;
+    if (mma) {  // DMMA direct epilogue: no k-split; padded rows (bank spread)
+      KS = 1;
+      WS = RSP + 4;
+    }
     p.RS[l] = RS;
     p.RSP[l] = RSP;
     p.KS[l] = KS;
+    p.WS[l] = WS;
     p.off_w[l] = off;
-    off = align16(off + K * RSP * tsize);
+    off = align16(off + K * WS * tsize);
     p.off_b[l] = off;
     off = align16(off + RSP * tsize);
-    part = std::max(part, (size_t)KS * RSP * ET * tsize);
+    if (!mma) part = std::max(part, (size_t)KS * RSP * ET * tsize);
   }
+  const int XS = mma ? ET + 4 : ET;
+  p.XS = XS;
   const int KRP = nh > 0 ? p.RSP[nh - 1] : net.dims[0];
   p.off_wout = off;
   off = align16(off + KRP * O * tsize);
   p.off_bout = off;
   off = align16(off + O * tsize);
   p.off_x0 = off;
-  off = align16(off + 4 * ET * tsize);
+  off = align16(off + 4 * XS * tsize);
   for (int l = 0; l < nh; ++l) {
     p.off_h[l] = off;
     const int rows = (l == nh - 1) ? p.RSP[l] : net.dims[l + 1];
-    off = align16(off + rows * ET * tsize);
+    off = align16(off + rows * XS * tsize);
   }
   int KSo = pow2floor(std::max(1, ROLLOUT_THREADS / (O * ET)));
   while (KSo > 1 && KRP / KSo < 4) KSo /= 2;
@@ -484,10 +715,13 @@ static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int
   p.off_part = off;
   off = align16(off + (int)part);
   p.off_pout = off;
-  off = align16(off + 2 * C * O * ET * tsize);
+  off = align16(off + 2 * C * (O + 1) * ET * tsize);
   p.off_mask = off;
   off = align16(off + 2 * MAXL * 4);
+  p.off_bar = off;  // two mbarriers (output exchange, double-buffered by step)
+  off = align16(off + 16);
   p.bytes = off;
+  p.mma = mma ? 1 : 0;
   if (off > 227 * 1024) return false;
   *P = p;
   return true;
@@ -497,6 +731,8 @@ bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPla
   const int ET = e >= 5 ? 16 : (e >= 2 ? 4 : 1);
   const int tsize = precision == 0 ? 8 : 4;
   for (int C : {1, 2, 4, 8}) {
+    // fp64 with 16 lanes: hidden-layer GEMMs on the FP64 tensor cores
+    if (precision == 0 && ET == 16 && try_plan(net, obs_dim, ET, 1, C, tsize, plan, true)) return true;
     if (ET == 16 && try_plan(net, obs_dim, ET, 2, C, tsize, plan)) {
       // TR=2 needs enough row groups x k-splits to occupy the CTA
       bool ok = true;
@@ -509,9 +745,9 @@ bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPla
   return false;
 }
 
-template <typename T, int TR, int ET, int C>
+template <typename T, int TR, int ET, int C, bool MMA>
 static cudaError_t launch_inst(const RolloutArgs& a, cudaStream_t stream) {
-  auto kern = rollout_kernel<T, TR, ET, C>;
+  auto kern = rollout_kernel<T, TR, ET, C, MMA>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -533,13 +769,13 @@ static cudaError_t launch_inst(const RolloutArgs& a, cudaStream_t stream) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <typename T, int TR, int ET>
+template <typename T, int TR, int ET, bool MMA = false>
 static cudaError_t launch_c(const RolloutArgs& a, cudaStream_t s) {
   switch (a.plan.C) {
-    case 1: return launch_inst<T, TR, ET, 1>(a, s);
-    case 2: return launch_inst<T, TR, ET, 2>(a, s);
-    case 4: return launch_inst<T, TR, ET, 4>(a, s);
-    case 8: return launch_inst<T, TR, ET, 8>(a, s);
+    case 1: return launch_inst<T, TR, ET, 1, MMA>(a, s);
+    case 2: return launch_inst<T, TR, ET, 2, MMA>(a, s);
+    case 4: return launch_inst<T, TR, ET, 4, MMA>(a, s);
+    case 8: return launch_inst<T, TR, ET, 8, MMA>(a, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -549,6 +785,8 @@ static cudaError_t launch_t(const RolloutArgs& a, cudaStream_t s) {
   if (a.plan.ET == 1) return launch_c<T, 1, 1>(a, s);
   if (a.plan.ET == 4) return launch_c<T, 1, 4>(a, s);
   if (a.plan.TR == 2) return launch_c<T, 2, 16>(a, s);
+  if constexpr (std::is_same<T, double>::value)
+    if (a.plan.mma) return launch_c<double, 1, 16, true>(a, s);
   return launch_c<T, 1, 16>(a, s);
 }
 

@@ -56,9 +56,13 @@ struct SmemPlan {
   int RS[MAXL];      // real rows owned per CTA (hidden layers)
   int RSP[MAXL];     // padded rows per CTA
   int KS[MAXL];      // k-split per hidden layer
+  int WS[MAXL];      // row stride of the k-major weight slice (RSP, +4 for DMMA)
+  int REP[MAXL];     // 1: layer computed in full by every CTA (no DSMEM exchange)
+  int XS;            // row stride of the activation buffers (ET; 20 on the DMMA plan)
+  int mma;           // 1: hidden layers with K >= 16 use FP64 tensor cores (DMMA)
   int KS_out;        // k-split of the output layer partial
   int off_w[MAXL], off_b[MAXL];
-  int off_wout, off_bout, off_x0, off_h[MAXL], off_part, off_pout, off_mask;
+  int off_wout, off_bout, off_x0, off_h[MAXL], off_part, off_pout, off_mask, off_bar;
   int bytes;
 };
 
@@ -87,5 +91,16 @@ struct RolloutArgs {
 cudaError_t launch_rollout(const RolloutArgs& a, int precision, cudaStream_t stream);
 // Host-side: build the SMEM plan; returns false if no cluster size fits.
 bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan);
+
+// Warp-team rollout for small policies (rollout_warp.cu): one warp per lane.
+struct WarpPlanOut {
+  int data[64];
+};
+bool plan_rollout_warp(const NetDesc& net, int obs_dim, int e, int precision, WarpPlanOut* out);
+cudaError_t launch_rollout_warp(const RolloutArgs& a, const WarpPlanOut& plan, int precision,
+                                cudaStream_t stream);
+// Materialise candidates [a0, a1) (row-major, d each) from a ParamDesc.
+cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
+                            cudaStream_t stream);
 
 }  // namespace evorl_b200
