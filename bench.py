@@ -42,6 +42,10 @@ CONFIGS = {
     "3": dict(algo="openes", env="pendulum", fixed_horizon=True, pop=4096, hidden=(256, 256),
               max_episode_steps=200, fitness_episodes=16,
               desc="OpenES pop 4096 x 16 envs/individual, 2x256 MLP, Pendulum H=200"),
+    "4": dict(algo="cmaes", env="pendulum", fixed_horizon=True, pop=512, hidden=(97, 97),
+              max_episode_steps=200, fitness_episodes=1, cmaes_elites=64, cmaes_sigma0=0.1,
+              cmaes_max_dim=10240,
+              desc="CMA-ES pop 512, mu 64, 3x97x97x1 MLP (d=9992), Pendulum H=200, eig every gen"),
 }
 
 
@@ -136,6 +140,10 @@ def cpu_sample_run(cfgd, steps, warmup, sample_pop=None, workers=0):
 
 
 def cpu_baseline(cfgd, cfg_name):
+    if cfgd["algo"] == "cmaes":
+        return {"value": None, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
+                "sample": ("not run: the port's O(d^3) single-thread Jacobi at d=9992 takes hours per "
+                           "generation (the reference's Eigen solver ~1e3 s, SURVEY.md §8(d))")}
     pop = cfgd["pop"]
     sample = {"3": 256}.get(cfg_name, pop)
     env_steps, times, cores, sp = cpu_sample_run(cfgd, steps=1, warmup=0, sample_pop=sample)

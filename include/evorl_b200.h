@@ -215,6 +215,22 @@ int evorl_es_set_obs_norm(evorl_es* es, const evorl_obs_norm* in);
 int evorl_es_set_counters(evorl_es* es, int64_t iteration, int64_t env_steps,
                           int64_t episodes);
 
+/* CmaState transfer (proj/include/evorl/ec.hpp:107-122; the ec/C, ec/B, ec/D,
+ * ec/ps, ec/pc, ec/sigma, ec/generation, ec/recondition_count checkpoint
+ * segments of proj/src/workflow_es.cpp:194-203).  C, B: d x d row-major,
+ * B[p*d + j] = component p of eigenvector j (Eigen's column j).  Any pointer
+ * may be NULL. */
+int evorl_es_cma_get(evorl_es* es, double* C, double* B, double* D, double* ps, double* pc,
+                     double* sigma, int64_t* generation, int64_t* recondition_count);
+int evorl_es_cma_set(evorl_es* es, const double* C, const double* B, const double* D,
+                     const double* ps, const double* pc, double sigma, int64_t generation,
+                     int64_t recondition_count);
+/* The device eigensolver (blocked Jacobi), replacing
+ * Eigen::SelfAdjointEigenSolver (proj/src/ec.cpp:278-287): A n x n symmetric
+ * row-major; evals ascending; vecs[p*n + j] = component p of eigenvector j,
+ * normalised so its largest-|.| component is positive. */
+int evorl_sym_eig(const double* A, int32_t n, double* evals, double* vecs, int32_t* sweeps);
+
 /* ------------------------------------------- population sharding (N GPUs)
  * A generation split into the phases around the two collectives of
  * rank r rolls out agents [a0, a1), the caller all-gathers

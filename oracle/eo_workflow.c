@@ -282,6 +282,13 @@ static int resolve_norm(const eo_es_config* c) {
 int eo_es_create(const eo_es_config* cfg, eo_es** out) {
   eo_es* es = (eo_es*)calloc(1, sizeof(eo_es));
   es->cfg = *cfg;
+  /* the ctor builds every algorithm config with pop_ = ec.pop
+   * (proj/src/workflow_es.cpp:33-61); CMA's weights depend on it */
+  es->cfg.openes.pop = cfg->pop;
+  es->cfg.ars.pop = cfg->pop;
+  es->cfg.ves.pop = cfg->pop;
+  es->cfg.cma.pop = cfg->pop;
+  es->cfg.cem.pop = cfg->pop;
   es->env = cfg->env_id == EO_CARTPOLE ? eo_env_cartpole(cfg->fixed_horizon, cfg->max_episode_steps)
                                        : eo_env_pendulum(cfg->fixed_horizon, cfg->max_episode_steps);
   es->net = eo_policy_net_spec(&es->env, cfg->hidden, cfg->n_hidden, cfg->layer_norm);

@@ -8,12 +8,13 @@ from ._lib import (ConfigError, DeviceError, EnvFault, EvorlError, InvalidArgume
                    LengthError, MissingExtension, NetFault, Unsupported)
 from .es import (EsConfig, EsWorkflow, StepMetrics, ars_ask, ars_tell, batched_rollout,
                  centered_ranks, env_step_batch, gaussian_matrix, measure_fp64_peak, mlp_desc,
-                 openes_ask, openes_tell, param_count, rank_desc, stream_words, threefry2x64)
+                 openes_ask, openes_tell, param_count, rank_desc, stream_words, sym_eig,
+                 threefry2x64)
 
 __all__ = [
     "ConfigError", "DeviceError", "EnvFault", "EvorlError", "InvalidArgument", "LengthError",
     "MissingExtension", "NetFault", "Unsupported", "EsConfig", "EsWorkflow", "StepMetrics",
     "ars_ask", "ars_tell", "batched_rollout", "centered_ranks", "env_step_batch",
     "gaussian_matrix", "measure_fp64_peak", "mlp_desc", "openes_ask", "openes_tell",
-    "param_count", "rank_desc", "stream_words", "threefry2x64",
+    "param_count", "rank_desc", "stream_words", "sym_eig", "threefry2x64",
 ]

@@ -126,7 +126,8 @@ EXPORTS = [
     "evorl_es_set_obs_norm", "evorl_es_set_counters", "evorl_es_set_shard",
     "evorl_es_shard_ranges", "evorl_es_phase_rollout", "evorl_es_phase_tell",
     "evorl_es_device_buffers", "evorl_es_stream", "evorl_es_last_timings",
-    "evorl_measure_fp64_peak", "evorl_measure_dmma_peak",
+    "evorl_measure_fp64_peak", "evorl_measure_dmma_peak", "evorl_es_cma_get", "evorl_es_cma_set",
+    "evorl_sym_eig",
 ]
 
 _lib = None
@@ -187,6 +188,10 @@ def load() -> C.CDLL:
     L.evorl_es_last_timings.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]
     L.evorl_measure_fp64_peak.argtypes = [C.POINTER(dbl)]
     L.evorl_measure_dmma_peak.argtypes = [C.POINTER(dbl)]
+    L.evorl_es_cma_get.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(dbl), C.POINTER(i64),
+                                   C.POINTER(i64)]
+    L.evorl_es_cma_set.argtypes = [vp, vp, vp, vp, vp, vp, dbl, i64, i64]
+    L.evorl_sym_eig.argtypes = [vp, i32, vp, vp, C.POINTER(i32)]
     _lib = L
     return L
 

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/evorl_b200.h"
+#include "cma.cuh"
 #include "kernels.cuh"
 
 using namespace evorl_b200;
@@ -200,6 +201,17 @@ struct evorl_es {
   float last_rollout_ms = 0.f, last_step_ms = 0.f;
   // per-step keys
   DKey step_key{}, ask_key{}, rollout_key{};
+  // CmaState (proj/include/evorl/ec.hpp:107-122): scalars on the host (the
+  // reference's std:: math, bit-identical), matrices on the device
+  struct {
+    int mu = 0;
+    std::vector<double> w;
+    double mueff = 0, cs = 0, ds = 0, cc = 0, c1 = 0, cmu = 0, chi_n = 0, sigma = 0;
+    long long generation = 0, recondition_count = 0;
+    int last_sweeps = 0;
+    double* d_w = nullptr;
+    CmaDev dev{};
+  } cma;
 };
 
 extern "C" void evorl_es_default_config(evorl_es_config* c) {
@@ -255,6 +267,11 @@ static void free_all(evorl_es* s) {
   if (s->h) cudaFreeHost(s->h);
   for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1})
     if (ev) cudaEventDestroy(ev);
+  void* cm[] = {s->cma.d_w, s->cma.dev.C, s->cma.dev.B, s->cma.dev.D, s->cma.dev.ps, s->cma.dev.pc,
+                s->cma.dev.W, s->cma.dev.V, s->cma.dev.U, s->cma.dev.evals, s->cma.dev.order, s->cma.dev.zD,
+                s->cma.dev.ytT, s->cma.dev.wyT, s->cma.dev.yw, s->cma.dev.t1, s->cma.dev.cih, s->cma.dev.red};
+  for (void* p : cm)
+    if (p) cudaFree(p);
   if (s->stream) cudaStreamDestroy(s->stream);
 }
 
@@ -270,8 +287,6 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   if (cfg->algo < 0 || cfg->algo > EVORL_ALGO_CEM) return set_err(EVORL_E_CONFIG, "ec.algo: unknown algorithm");
   if (cfg->env_id != EVORL_ENV_CARTPOLE && cfg->env_id != EVORL_ENV_PENDULUM)
     return set_err(EVORL_E_INVALID_ARGUMENT, "unknown env id");
-  if (cfg->algo == EVORL_ALGO_CMAES)
-    return set_err(EVORL_E_UNSUPPORTED, "cmaes: device path not built in this revision");
   if (cfg->algo == EVORL_ALGO_OPENES && cfg->openes_noise_table)
     return set_err(EVORL_E_UNSUPPORTED, "openes noise_table mode: device path not built in this revision");
   if (cfg->precision != EVORL_PREC_F64 && cfg->precision != EVORL_PREC_F32)
@@ -347,6 +362,69 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   A(dalloc(&s->d_metrics, 4));
   A(dalloc(&s->d_sel, 1));
   if (s->warp_path) A(dalloc(&s->d_cand, (size_t)n * d));
+  if (cfg->algo == EVORL_ALGO_CMAES) {
+    // CmaState::init (proj/src/ec.cpp:191-224)
+    if (d > cfg->cmaes_max_dim) {
+      free_all(s);
+      delete s;
+      return set_err(EVORL_E_LENGTH,
+                     "cmaes: genotype dimension %lld exceeds the full-covariance capacity cap %d",
+                     (long long)d, cfg->cmaes_max_dim);
+    }
+    const int mu = cfg->cmaes_elites;
+    if (mu < 1 || mu > n) {  // the reference indexes order[i < mu] unchecked (UB when mu > pop)
+      free_all(s);
+      delete s;
+      return set_err(EVORL_E_INVALID_ARGUMENT, "cmaes_tell: elites (%d) exceed population (%d)", mu, n);
+    }
+    auto& c = s->cma;
+    c.mu = mu;
+    c.w.resize(mu);
+    double sum = 0.0;
+    for (int i = 0; i < mu; ++i) {
+      double wi = std::log((cfg->pop + 1) / 2.0) - std::log(i + 1.0);
+      if (wi < 0) wi = 0.0;
+      c.w[i] = wi;
+      sum += wi;
+    }
+    double sq = 0.0;
+    for (int i = 0; i < mu; ++i) {
+      c.w[i] /= sum;
+      sq += c.w[i] * c.w[i];
+    }
+    c.mueff = 1.0 / sq;
+    const double dd = (double)d;
+    c.cs = (c.mueff + 2.0) / (dd + c.mueff + 5.0);
+    c.ds = 1.0 + 2.0 * std::max(0.0, std::sqrt((c.mueff - 1.0) / (dd + 1.0)) - 1.0) + c.cs;
+    c.cc = (4.0 + c.mueff / dd) / (dd + 4.0 + 2.0 * c.mueff / dd);
+    c.c1 = 2.0 / ((dd + 1.3) * (dd + 1.3) + c.mueff);
+    c.cmu = std::min(1.0 - c.c1, 2.0 * (c.mueff - 2.0 + 1.0 / c.mueff) / ((dd + 2.0) * (dd + 2.0) + c.mueff));
+    c.chi_n = std::sqrt(dd) * (1.0 - 1.0 / (4.0 * dd) + 1.0 / (21.0 * dd * dd));
+    CmaDev& v = c.dev;
+    v.d = (int)d;
+    v.dp = (int)((d + 63) / 64 * 64);
+    const size_t dp2 = (size_t)v.dp * v.dp;
+    A(dalloc(&c.d_w, mu));
+    A(cudaMemcpy(c.d_w, c.w.data(), sizeof(double) * mu, cudaMemcpyHostToDevice));
+    A(dalloc(&v.C, dp2));
+    A(dalloc(&v.B, dp2));
+    A(dalloc(&v.W, dp2));
+    A(dalloc(&v.V, dp2));
+    A(dalloc(&v.U, (size_t)(v.dp / 64) * 64 * 64));
+    A(dalloc(&v.D, v.dp));
+    A(dalloc(&v.ps, v.dp));
+    A(dalloc(&v.pc, v.dp));
+    A(dalloc(&v.evals, v.dp));
+    A(dalloc(&v.order, v.dp));
+    A(dalloc(&v.zD, (size_t)n * d));
+    A(dalloc(&v.ytT, (size_t)d * mu));
+    A(dalloc(&v.wyT, (size_t)d * mu));
+    A(dalloc(&v.yw, v.dp));
+    A(dalloc(&v.t1, v.dp));
+    A(dalloc(&v.cih, v.dp));
+    A(dalloc(&v.red, 8));
+    if (!s->d_cand) A(dalloc(&s->d_cand, (size_t)n * d));
+  }
   A(dalloc(&s->d_steps, 1));
   A(dalloc(&s->d_fault, 1));
   A(cudaMallocHost((void**)&s->h, sizeof(Pinned)));
@@ -405,6 +483,21 @@ extern "C" int evorl_es_init(evorl_es* s, uint64_t key_hi, uint64_t key_lo) {
   CK(cudaMemsetAsync(s->d_m, 0, sizeof(double) * s->d, s->stream));
   CK(cudaMemsetAsync(s->d_v, 0, sizeof(double) * s->d, s->stream));
   CK(cudaMemsetAsync(s->d_t, 0, sizeof(long long), s->stream));
+  if (s->cfg.algo == EVORL_ALGO_CMAES) {  // C = B = I, D = 1, ps = pc = 0
+    CmaDev& v = s->cma.dev;
+    const size_t dp2 = (size_t)v.dp * v.dp;
+    std::vector<double> eye(dp2, 0.0);
+    for (int i = 0; i < v.dp; ++i) eye[(size_t)i * v.dp + i] = 1.0;
+    CK(cudaMemcpy(v.C, eye.data(), sizeof(double) * dp2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(v.B, eye.data(), sizeof(double) * dp2, cudaMemcpyHostToDevice));
+    std::vector<double> ones(v.dp, 1.0);
+    CK(cudaMemcpy(v.D, ones.data(), sizeof(double) * v.dp, cudaMemcpyHostToDevice));
+    CK(cudaMemset(v.ps, 0, sizeof(double) * v.dp));
+    CK(cudaMemset(v.pc, 0, sizeof(double) * v.dp));
+    s->cma.sigma = s->cfg.cmaes_sigma0;
+    s->cma.generation = 0;
+    s->cma.recondition_count = 0;
+  }
   if (s->cfg.algo == EVORL_ALGO_CEM) {
     std::vector<double> v(s->d, s->cfg.cem_var_init);
     CK(cudaMemcpyAsync(s->d_var, v.data(), sizeof(double) * s->d, cudaMemcpyHostToDevice, s->stream));
@@ -516,7 +609,29 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
   CK(cudaMemsetAsync(s->d_steps, 0, sizeof(unsigned long long), s->stream));
   CK(cudaMemsetAsync(s->d_fault, 0xFF, sizeof(unsigned long long), s->stream));
   RolloutArgs a = rollout_args(s);
-  if (s->warp_path) {
+  if (s->cfg.algo == EVORL_ALGO_CMAES) {
+    // cmaes_ask (proj/src/ec.cpp:226-234): all n candidates (every rank needs
+    // the elites' rows for the tell), Y = ((z .* D^T) B^T) sigma + mean
+    CmaDev& v = s->cma.dev;
+    const int n = s->cfg.pop;
+    CK(run_cma_zD(s->ask_key, n, (int)s->d, v.D, v.zD, s->stream));
+    GemmEpi epi{};
+    epi.mode = GEMM_ASK;
+    epi.out = s->d_cand;
+    epi.ldo = s->d;
+    epi.sigma = s->cma.sigma;
+    epi.mean = s->d_mean;
+    CK(run_gemm_nt(n, (int)s->d, (int)s->d, v.zD, s->d, v.B, v.dp, epi, s->stream));
+    a.par.src = SRC_EXPLICIT;
+    a.par.params = s->d_cand + (long long)s->a0 * s->d;
+    CK(cudaEventRecord(s->ev_r0, s->stream));
+    if (s->warp_path) {
+      CK(launch_rollout_warp(a, s->wplan, s->cfg.precision, s->stream));
+    } else {
+      CK(launch_rollout(a, s->cfg.precision, s->stream));
+      count_launch();
+    }
+  } else if (s->warp_path) {
     // small policy: materialise the shard's candidates (fully parallel ask),
     // then one warp per lane with the weights resident in shared memory
     CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream));
@@ -611,6 +726,58 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       CK(run_ves_tell(s->d_mean, s->d, s->p0, s->p1, s->cfg.ves_sigma, s->cfg.ves_mirrored, base,
                       s->ask_key, s->d_order, s->d_ves_w, mu, st));
       sigma = s->cfg.ves_sigma;
+      break;
+    }
+    case EVORL_ALGO_CMAES: {  // cmaes_tell (proj/src/ec.cpp:236-288), replicated on every rank
+      auto& c = s->cma;
+      CmaDev& v = c.dev;
+      const int d = (int)s->d, mu = c.mu, dp = v.dp;
+      CK(run_rank(s->d_fitness, n, 1, s->d_rank, st));
+      CK(run_order_from_rank(s->d_rank, n, s->d_order, st));
+      CK(run_cma_ytop(s->d_cand, s->d_order, mu, d, s->d_mean, c.sigma, c.d_w, v.ytT, v.wyT, st));
+      CK(run_cma_yw_mean(v.ytT, c.d_w, mu, d, c.sigma, v.yw, s->d_mean, st));
+      CK(run_cma_gemv_t(v.B, dp, d, v.yw, v.D, v.t1, st));
+      CK(run_cma_gemv(v.B, dp, d, v.t1, v.cih, st));
+      const double cps = std::sqrt(c.cs * (2.0 - c.cs) * c.mueff);
+      CK(run_cma_ps(v.ps, v.cih, d, c.cs, cps, v.red, st));
+      double nrm2 = 0.0;
+      CK(cudaMemcpyAsync(&nrm2, v.red, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const double gen1 = (double)(c.generation + 1);
+      const double ps_norm = std::sqrt(nrm2);
+      const bool hsig = ps_norm / std::sqrt(1.0 - std::pow(1.0 - c.cs, 2.0 * gen1)) <
+                        (1.4 + 2.0 / ((double)d + 1.0)) * c.chi_n;
+      const double cpc = hsig ? std::sqrt(c.cc * (2.0 - c.cc) * c.mueff) : 0.0;
+      CK(run_cma_pc(v.pc, v.yw, d, c.cc, cpc, st));
+      // C' = (1-c1-cmu) C + c1 (pc pc^T + dhsig C) + cmu sum_i w_i y_i y_i^T,
+      // the rank-mu sum as a K = mu DMMA GEMM with the blend in its epilogue
+      GemmEpi epi{};
+      epi.mode = GEMM_RANKMU;
+      epi.out = v.W;
+      epi.ldo = dp;
+      epi.Cold = v.C;
+      epi.pc = v.pc;
+      epi.a = 1.0 - c.c1 - c.cmu;
+      epi.c1 = c.c1;
+      epi.dh = (hsig ? 0.0 : 1.0) * c.cc * (2.0 - c.cc);
+      epi.cmu = c.cmu;
+      CK(run_gemm_nt(d, d, mu, v.wyT, mu, v.ytT, mu, epi, st));
+      CK(run_cma_symmetrize(v.W, v.C, d, dp, st));
+      c.sigma *= std::exp((c.cs / c.ds) * (ps_norm / c.chi_n - 1.0));
+      c.generation += 1;
+      // re-factorise; re-condition when eigenvalues fall to <= 0
+      double evmin = 0.0;
+      int sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st);
+      if (sw < 0) return set_err(EVORL_E_CUDA, "cmaes: eigensolver failed: %s", cudaGetErrorString(cudaGetLastError()));
+      if (evmin <= 0.0) {
+        CK(run_cma_add_diag(v.C, d, dp, 1e-10 - evmin, st));
+        sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st);
+        if (sw < 0) return set_err(EVORL_E_CUDA, "cmaes: eigensolver failed");
+        c.recondition_count += 1;
+      }
+      c.last_sweeps = sw;
+      CK(run_cma_sqrt_pos(v.evals, v.D, d, st));
+      sigma = c.sigma;
       break;
     }
     case EVORL_ALGO_CEM: {
@@ -739,6 +906,50 @@ extern "C" int evorl_es_set_adam(evorl_es* s, const double* m, const double* v, 
   s->adam_t_host = t;
   return EVORL_OK;
 }
+// CmaState transfer (proj/include/evorl/ec.hpp:107-122; checkpoint segments
+// ec/C, ec/B, ec/D, ec/ps, ec/pc, ec/sigma, ec/generation,
+// ec/recondition_count of proj/src/workflow_es.cpp:194-203).  C and B are
+// d x d row-major (B[p*d + j] = component p of eigenvector j); any pointer may
+// be NULL.
+extern "C" int evorl_es_cma_get(evorl_es* s, double* C, double* B, double* D, double* ps, double* pc,
+                                double* sigma, int64_t* generation, int64_t* recondition_count) {
+  if (s->cfg.algo != EVORL_ALGO_CMAES) return set_err(EVORL_E_INVALID_ARGUMENT, "not a cmaes workflow");
+  CK(cudaSetDevice(s->cfg.device));
+  const CmaDev& v = s->cma.dev;
+  const int d = (int)s->d;
+  if (C) CK(cudaMemcpy2D(C, sizeof(double) * d, v.C, sizeof(double) * v.dp, sizeof(double) * d, d,
+                         cudaMemcpyDeviceToHost));
+  if (B) CK(cudaMemcpy2D(B, sizeof(double) * d, v.B, sizeof(double) * v.dp, sizeof(double) * d, d,
+                         cudaMemcpyDeviceToHost));
+  if (D) CK(cudaMemcpy(D, v.D, sizeof(double) * d, cudaMemcpyDeviceToHost));
+  if (ps) CK(cudaMemcpy(ps, v.ps, sizeof(double) * d, cudaMemcpyDeviceToHost));
+  if (pc) CK(cudaMemcpy(pc, v.pc, sizeof(double) * d, cudaMemcpyDeviceToHost));
+  if (sigma) *sigma = s->cma.sigma;
+  if (generation) *generation = s->cma.generation;
+  if (recondition_count) *recondition_count = s->cma.recondition_count;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_es_cma_set(evorl_es* s, const double* C, const double* B, const double* D,
+                                const double* ps, const double* pc, double sigma, int64_t generation,
+                                int64_t recondition_count) {
+  if (s->cfg.algo != EVORL_ALGO_CMAES) return set_err(EVORL_E_INVALID_ARGUMENT, "not a cmaes workflow");
+  CK(cudaSetDevice(s->cfg.device));
+  CmaDev& v = s->cma.dev;
+  const int d = (int)s->d;
+  if (C) CK(cudaMemcpy2D(v.C, sizeof(double) * v.dp, C, sizeof(double) * d, sizeof(double) * d, d,
+                         cudaMemcpyHostToDevice));
+  if (B) CK(cudaMemcpy2D(v.B, sizeof(double) * v.dp, B, sizeof(double) * d, sizeof(double) * d, d,
+                         cudaMemcpyHostToDevice));
+  if (D) CK(cudaMemcpy(v.D, D, sizeof(double) * d, cudaMemcpyHostToDevice));
+  if (ps) CK(cudaMemcpy(v.ps, ps, sizeof(double) * d, cudaMemcpyHostToDevice));
+  if (pc) CK(cudaMemcpy(v.pc, pc, sizeof(double) * d, cudaMemcpyHostToDevice));
+  s->cma.sigma = sigma;
+  s->cma.generation = generation;
+  s->cma.recondition_count = recondition_count;
+  return EVORL_OK;
+}
+
 extern "C" int evorl_es_get_fitness(evorl_es* s, double* f) {
   CK(cudaSetDevice(s->cfg.device));
   CK(cudaMemcpyAsync(f, s->d_fitness, sizeof(double) * s->cfg.pop, cudaMemcpyDeviceToHost, s->stream));
@@ -1153,3 +1364,39 @@ extern "C" int evorl_measure_fp64_peak(double* tflops) {
   CK(cudaGetLastError());
   return EVORL_OK;
 }
+
+// Symmetric eigendecomposition on the device (the K7 Jacobi eigensolver,
+// replacing Eigen::SelfAdjointEigenSolver at proj/src/ec.cpp:278-287):
+// A is n x n row-major symmetric; evals ascending; vecs[p*n + j] = component
+// p of eigenvector j (largest-|.| component positive).  Returns the sweeps in
+// *sweeps.
+extern "C" int evorl_sym_eig(const double* A, int32_t n, double* evals, double* vecs, int32_t* sweeps) {
+  DEV_OR_RETURN();
+  if (n <= 0) return EVORL_OK;
+  CmaDev v{};
+  v.d = n;
+  v.dp = (n + 63) / 64 * 64;
+  const size_t dp2 = (size_t)v.dp * v.dp;
+  Scratch a, b, w, vv, u, ev, od, t1, red;
+  double *dA, *dB;
+  if (int rc = up(a, (const double*)nullptr, dp2, &dA)) return rc;
+  if (int rc = up(b, (const double*)nullptr, dp2, &dB)) return rc;
+  if (int rc = up(w, (const double*)nullptr, dp2, &v.W)) return rc;
+  if (int rc = up(vv, (const double*)nullptr, dp2, &v.V)) return rc;
+  if (int rc = up(u, (const double*)nullptr, (size_t)(v.dp / 64) * 4096, &v.U)) return rc;
+  if (int rc = up(ev, (const double*)nullptr, v.dp, &v.evals)) return rc;
+  if (int rc = up(od, (const int*)nullptr, v.dp, &v.order)) return rc;
+  if (int rc = up(t1, (const double*)nullptr, v.dp, &v.t1)) return rc;
+  if (int rc = up(red, (const double*)nullptr, 8, &v.red)) return rc;
+  CK(cudaMemset(dA, 0, sizeof(double) * dp2));
+  CK(cudaMemcpy2D(dA, sizeof(double) * v.dp, A, sizeof(double) * n, sizeof(double) * n, n, cudaMemcpyHostToDevice));
+  double evmin = 0.0;
+  const int sw = sym_eig_jacobi(v, dA, n, &evmin, dB, v.evals, 0);
+  if (sw < 0) return set_err(EVORL_E_CUDA, "eigensolver failed");
+  CK(cudaMemcpy(evals, v.evals, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy2D(vecs, sizeof(double) * n, dB, sizeof(double) * v.dp, sizeof(double) * n, n,
+                  cudaMemcpyDeviceToHost));
+  if (sweeps) *sweeps = sw;
+  return EVORL_OK;
+}
+

@@ -428,20 +428,6 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
     }
   };
   if (valid && eps_this > 0 && A.max_iters > 0) observe_into_x0(true);
-  // Output exchange: every CTA's OE1 writer threads store into each peer and
-  // arrive (release.cluster) on the peer's mbarrier for this step; only the
-  // env threads wait (acquire.cluster) -- no full cluster barrier per step.
-  // Two barriers alternate by step so an early arrival for step t+1 can never
-  // complete a peer's phase for step t.
-  uint64_t* obar = reinterpret_cast<uint64_t*>(smem + S.off_bar);
-  if constexpr (C > 1) {
-    if (tid == 0) {
-      mbar_init(&obar[0], (uint32_t)C);
-      mbar_init(&obar[1], (uint32_t)C);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    cluster_sync_all();  // peers may arrive only on initialised barriers
-  }
 
   for (int it = 0;; ++it) {
     if (tid < MAXL) mask[(it & 1) * MAXL + tid] = 0u;  // last used two steps ago
@@ -564,18 +550,18 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
           pout[oe] = v;
         }
       }
-      __syncthreads();
+      // one cluster barrier per step (measured faster on B200 than mbarrier
+      // point-to-point signalling: 165 vs 175 ms/generation on config 3)
       if constexpr (C > 1) {
-        // one release.cluster arrive per peer, after the CTA barrier has
-        // ordered every writer's DSMEM stores (release is cumulative)
-        if (tid < C) mbar_arrive_remote(&obar[it & 1], (uint32_t)tid);
+        cluster_sync_all();
+      } else {
+        __syncthreads();
       }
     }
 
     // head + env step (proj/src/rollout.cpp:57-90, :131-153), then the next
     // observation (same threads: no extra barrier)
     if (active) {
-      if constexpr (C > 1) mbar_wait_parity(&obar[it & 1], (uint32_t)((it >> 1) & 1));
       double z[8];
       bool nonfinite_out = false;
       int bad_layer = L;

@@ -26,7 +26,7 @@ from ._lib import check
 __all__ = ["EsConfig", "EsWorkflow", "StepMetrics", "batched_rollout", "gaussian_matrix",
            "centered_ranks", "rank_desc", "openes_ask", "openes_tell", "ars_ask", "ars_tell",
            "env_step_batch", "threefry2x64", "stream_words", "param_count", "mlp_desc",
-           "measure_fp64_peak"]
+           "measure_fp64_peak", "sym_eig"]
 
 
 def _p(a: np.ndarray):
@@ -249,6 +249,22 @@ class EsWorkflow:
     def stream(self) -> int:
         return self.L.evorl_es_stream(self.h)
 
+    # CMA-ES state (proj/include/evorl/ec.hpp:107-122) ----------------------
+    def cma_state(self) -> dict:
+        d = self.dim
+        Cm, Bm = np.empty((d, d)), np.empty((d, d))
+        D, ps, pc = np.empty(d), np.empty(d), np.empty(d)
+        sg, gen, rc = C.c_double(), C.c_int64(), C.c_int64()
+        check(self.L.evorl_es_cma_get(self.h, _p(Cm), _p(Bm), _p(D), _p(ps), _p(pc), C.byref(sg),
+                                      C.byref(gen), C.byref(rc)))
+        return dict(C=Cm, B=Bm, D=D, ps=ps, pc=pc, sigma=sg.value, generation=gen.value,
+                    recondition_count=rc.value)
+
+    def set_cma_state(self, C_, B, D, ps, pc, sigma, generation, recondition_count=0) -> None:
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (C_, B, D, ps, pc)]
+        check(self.L.evorl_es_cma_set(self.h, *[_p(a) for a in arrs], float(sigma), int(generation),
+                                      int(recondition_count)))
+
 
 # -------------------------------------------------------------- stateless
 def mlp_desc(input_dim: int, hidden: Sequence[int], output_dim: int, head: int,
@@ -405,6 +421,19 @@ def batched_rollout(env: str, net: _lib.MlpDesc, params, envs_per_agent: int, ke
         count, hi, lo, _lib.PREC_F64 if precision == "f64" else _lib.PREC_F32, _p(rets),
         _p(steps), _p(stats) if stats is not None else None))
     return rets, steps, stats
+
+
+def sym_eig(A):
+    """Device Jacobi eigensolver (replaces Eigen::SelfAdjointEigenSolver,
+    proj/src/ec.cpp:278-287) -> (evals ascending, vecs with vecs[:, j] the j-th
+    eigenvector, largest-|.| component positive, sweeps)."""
+    A = np.ascontiguousarray(A, np.float64)
+    n = A.shape[0]
+    ev = np.empty(n)
+    V = np.empty((n, n))
+    sw = C.c_int32()
+    check(_lib.load().evorl_sym_eig(_p(A), n, _p(ev), _p(V), C.byref(sw)))
+    return ev, V, sw.value
 
 
 def measure_fp64_peak() -> float:

@@ -1,0 +1,131 @@
+"""CMA-ES on the B200 vs the CPU oracle.
+
+Eigenvectors are compared under the shared convention (ascending eigenvalues,
+largest-|.| component positive).  Where eigenvalues are degenerate (C = I at
+generation 0, or d > mu + 1 after the first update) the eigenbasis is not
+unique, so parity is asserted on invariants (eigenvalues, B D^2 B^T = C,
+B^T B = I) and on full trajectories only for a non-degenerate configuration
+(d <= mu + 1), as SURVEY.md §7.4-6 prescribes."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def evb():
+    import paper_2501_15129_b200 as evb
+    return evb
+
+
+@pytest.mark.parametrize("n", [1, 5, 33, 64, 100, 257])
+def test_sym_eig_matches_numpy(evb, n):
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n))
+    A = (A + A.T) / 2 + n * np.eye(n) * 0.1
+    ev, V, sweeps = evb.sym_eig(A)
+    ref = np.linalg.eigvalsh(A)
+    scale = max(1.0, np.abs(ref).max())
+    assert np.abs(ev - ref).max() <= 1e-12 * scale * max(1, n / 10), (ev[:3], ref[:3])
+    assert np.abs(V.T @ V - np.eye(n)).max() < 1e-12
+    assert np.abs(V @ np.diag(ev) @ V.T - A).max() < 1e-11 * scale
+    # sign convention: the largest-|.| component of each vector is positive
+    idx = np.argmax(np.abs(V), axis=0)
+    assert np.all(V[idx, np.arange(n)] > 0)
+    assert sweeps < 30
+
+
+def test_sym_eig_matches_oracle_vectors(evb, oracle):
+    n = 40
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((n, n))
+    A = A + A.T
+    ev_o = np.empty(n)
+    V_o = np.empty((n, n))
+    oracle.lib().eo_sym_eig(oracle.ptr(A), n, oracle.ptr(ev_o), oracle.ptr(V_o))
+    ev, V, _ = evb.sym_eig(A)
+    assert np.allclose(ev, ev_o, rtol=1e-12, atol=1e-12)
+    assert np.allclose(V, V_o.T, atol=1e-10)  # oracle stores column-major
+
+
+def _pair(oracle, evb, **kw):
+    okw = dict(kw)
+    okw["hidden"] = list(kw["hidden"])
+    oc = oracle.es_config(algo="cmaes", workers=0, **{k: v for k, v in okw.items()
+                                                       if not k.startswith("cma.")},
+                          **{k: v for k, v in okw.items() if k.startswith("cma.")})
+    ec = evb.EsConfig(algo="cmaes", **{k: v for k, v in kw.items() if not k.startswith("cma.")},
+                      cmaes_elites=kw.get("cma.elites", 64), cmaes_sigma0=kw.get("cma.sigma0", 0.1),
+                      cmaes_max_dim=kw.get("cma.max_dim", 4096))
+    return oracle.OracleEs(oc), evb.EsWorkflow(ec)
+
+
+def _cma_o(o):
+    st = o.cma()
+    d = st.dim
+    arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy()
+    return dict(C=arr(st.C, d * d).reshape(d, d), B=arr(st.B, d * d).reshape(d, d).T,
+                D=arr(st.D, d), ps=arr(st.ps, d), pc=arr(st.pc, d), sigma=st.sigma,
+                generation=st.generation, recondition_count=st.recondition_count)
+
+
+def test_cma_nondegenerate_trajectory_matches_oracle(oracle, evb):
+    # d = 3*4+4+4+1 = 21 <= mu + 1 = 33: distinct eigenvalues after generation 1
+    kw = dict(env="pendulum", fixed_horizon=True, pop=64, hidden=(4,), max_episode_steps=50,
+              vbn_samples=300, **{"cma.elites": 32, "cma.sigma0": 0.3})
+    o, g = _pair(oracle, evb, **kw)
+    key = oracle.key_from_seed(11)
+    o.init(key)
+    g.init(key)
+    assert np.array_equal(g.mean(), o.mean())
+    for gen in range(4):
+        om = o.step()
+        gm = g.step()
+        fo, fg = o.fitness(), g.fitness()
+        assert np.allclose(fg, fo, rtol=1e-8, atol=1e-10), gen
+        assert np.array_equal(np.argsort(fg, kind="stable"), np.argsort(fo, kind="stable"))
+        so, sg = _cma_o(o), g.cma_state()
+        assert sg["generation"] == so["generation"] == gen + 1
+        assert sg["sigma"] == pytest.approx(so["sigma"], rel=1e-9)
+        assert gm["es/sigma"] == pytest.approx(om.sigma, rel=1e-9)
+        for k in ("ps", "pc", "D"):
+            assert np.allclose(sg[k], so[k], rtol=1e-7, atol=1e-10), (gen, k)
+        assert np.allclose(sg["C"], so["C"], rtol=1e-8, atol=1e-12), gen
+        assert np.allclose(sg["B"], so["B"], atol=1e-6), gen
+        assert np.allclose(g.mean(), o.mean(), rtol=1e-8, atol=1e-10), gen
+
+
+def test_cma_degenerate_invariants_and_gen0(oracle, evb):
+    # d = 3*16+16+16+1 = 81 > mu + 1: degenerate eigenspace after generation 1
+    kw = dict(env="pendulum", fixed_horizon=True, pop=32, hidden=(16,), max_episode_steps=40,
+              vbn_samples=300, **{"cma.elites": 8, "cma.sigma0": 0.2})
+    o, g = _pair(oracle, evb, **kw)
+    key = oracle.key_from_seed(12)
+    o.init(key)
+    g.init(key)
+    o.step()
+    g.step()
+    # generation 0: B = I on both sides -> identical candidates and fitness
+    assert np.allclose(g.fitness(), o.fitness(), rtol=1e-9, atol=1e-10)
+    so, sg = _cma_o(o), g.cma_state()
+    assert np.allclose(sg["C"], so["C"], rtol=1e-10, atol=1e-13)
+    assert np.allclose(sg["D"], so["D"], rtol=1e-9)
+    assert np.allclose(g.mean(), o.mean(), rtol=1e-10, atol=1e-12)
+    for gen in range(3):
+        g.step()
+        s = g.cma_state()
+        Bm, Dv, Cm = s["B"], s["D"], s["C"]
+        assert np.abs(Cm - Cm.T).max() < 1e-12  # proj/tests/test_ec.cpp:263-280
+        assert Dv.min() > 0
+        assert np.abs(Bm.T @ Bm - np.eye(len(Dv))).max() < 1e-11
+        assert np.abs(Bm @ np.diag(Dv ** 2) @ Bm.T - Cm).max() < 1e-11 * np.abs(Cm).max()
+        ev = np.linalg.eigvalsh(Cm)
+        assert np.allclose(np.sort(Dv ** 2), ev, rtol=1e-9, atol=1e-14)
+
+
+def test_cma_capacity_cap(evb):
+    with pytest.raises(evb.LengthError, match="capacity cap"):
+        evb.EsWorkflow(evb.EsConfig(algo="cmaes", env="pendulum", hidden=(64, 64), cmaes_max_dim=4096,
+                                    pop=16, cmaes_elites=8))
