@@ -181,6 +181,10 @@ typedef struct {
   int64_t cem_decay_iters;
   int32_t precision; /* EVORL_PREC_* (not a reference key) */
   int32_t device;    /* CUDA ordinal (not a reference key) */
+  /* EXTENSION (BASELINE config 4): re-factorise C every k-th generation
+   * (lazy CMA-ES).  k = 1 (default) is the reference behaviour
+   * (proj/src/ec.cpp:276-287); B and D stay fixed in between. */
+  int32_t cmaes_eig_every;
 } evorl_es_config;
 
 /* StepMetrics of EsWorkflow::step (proj/src/workflow_es.cpp:140-169) */

@@ -105,7 +105,7 @@ class EsConfigC(C.Structure):
                 ("cmaes_max_dim", C.c_int32), ("cem_elites", C.c_int32),
                 ("cem_var_init", C.c_double), ("cem_noise_start", C.c_double),
                 ("cem_noise_end", C.c_double), ("cem_decay_iters", C.c_int64),
-                ("precision", C.c_int32), ("device", C.c_int32)]
+                ("precision", C.c_int32), ("device", C.c_int32), ("cmaes_eig_every", C.c_int32)]
 
 
 class StepMetricsC(C.Structure):

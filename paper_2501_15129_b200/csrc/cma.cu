@@ -16,6 +16,8 @@
 //    total (fp64 round-off level).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "cma.cuh"
@@ -501,8 +503,33 @@ __global__ void k_eig_finish(const double* V, int dp, int d, const int* rank, co
   if (lane == 0) evs[j] = ev[src];
 }
 
+// out = in^T over the dp x dp square (32x32 tiles through shared memory)
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int dp) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) tile[j][threadIdx.x] = in[(long long)(by + j) * dp + bx + threadIdx.x];
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) out[(long long)(bx + j) * dp + by + threadIdx.x] = tile[threadIdx.x][j];
+}
+
+// W = 0.5 (T + T^T) on the d x d block, decoupled identity padding; V = I
+__global__ void k_warm_init(double* T_then_V, double* W, int d, int dp) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)dp * dp) return;
+  const int r = (int)(i / dp), c = (int)(i % dp);
+  if (r < d && c < d) {
+    W[i] = 0.5 * (T_then_V[i] + T_then_V[(long long)c * dp + r]);
+  } else {
+    W[i] = r == c ? 1.0 : 0.0;
+  }
+}
+__global__ void k_eye(double* V, int dp) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < (long long)dp * dp) V[i] = (i / dp == i % dp) ? 1.0 : 0.0;
+}
+
 int sym_eig_jacobi(CmaDev& w, const double* A, int d, double* evals_min, double* vecs, double* evals,
-                   cudaStream_t s) {
+                   cudaStream_t s, const double* warm_B) {
   const int dp = w.dp;
   const int nb = dp / JB;  // even: dp is a multiple of 64
   const long long n2 = (long long)dp * dp;
@@ -513,33 +540,89 @@ int sym_eig_jacobi(CmaDev& w, const double* A, int d, double* evals_min, double*
     cudaFuncSetAttribute(k_jacobi_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply);
     attr = true;
   }
-  k_eig_init<<<nblk(n2, 256), 256, 0, s>>>(A, w.W, w.V, d, dp);
-  count_launch(1);
+  const double* Vsrc = w.V;
+  static const bool trace = getenv("EVORL_EIG_TRACE") != nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr;
+  if (trace) {
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventCreate(&t2);
+    cudaEventRecord(t0, s);
+  }
+  if (warm_B != nullptr) {
+    // warm start: W = B^T A B with B the previous eigenvectors (nearly
+    // diagonal when A changed little), rotations accumulate into V, and the
+    // final eigenvectors are B V.  Bt and Tt are scratch (dp x dp).
+    k_transpose<<<dim3(dp / 32, dp / 32), dim3(32, 8), 0, s>>>(warm_B, w.Bt, dp);
+    GemmEpi e{};
+    e.mode = GEMM_STORE;
+    e.ldo = dp;
+    e.out = w.Tt;  // Tt[n][k] = sum_p B[p][n] A[k][p] = (B^T A)[n][k]
+    run_gemm_nt(d, d, d, w.Bt, dp, A, dp, e, s);
+    e.out = w.V;  // (B^T A B)[m][n] = sum_k Bt[m][k] Tt[n][k]
+    run_gemm_nt(d, d, d, w.Bt, dp, w.Tt, dp, e, s);
+    k_warm_init<<<nblk(n2, 256), 256, 0, s>>>(w.V, w.W, d, dp);  // symmetrise + pad
+    k_eye<<<nblk(n2, 256), 256, 0, s>>>(w.V, dp);                // V = I
+    count_launch(3);
+  } else {
+    k_eig_init<<<nblk(n2, 256), 256, 0, s>>>(A, w.W, w.V, d, dp);
+    count_launch(1);
+  }
+  if (trace) cudaEventRecord(t1, s);
   int sweep = 0;
   std::vector<double> h(2);
+  // Stop when the off-diagonal mass reaches fp64 round-off for this size
+  // (each of the d^2 entries carries ~eps |lambda| of noise, so the floor of
+  // off/tot is ~d eps^2), or when a sweep stops making progress.
+  const double eps = 1.1102230246251565e-16;
+  const double tol = std::max(1e-30, 16.0 * d * eps * eps);
+  double prev_off = INFINITY;
   for (; sweep < 30; ++sweep) {
     cudaMemsetAsync(w.red, 0, 2 * sizeof(double), s);
     k_offdiag<<<296, 256, 0, s>>>(w.W, d, dp, w.red);
     count_launch(1);
     cudaMemcpyAsync(h.data(), w.red, 2 * sizeof(double), cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
-    if (h[0] <= 1e-28 * h[1] || h[0] == 0.0) break;
+    if (h[0] <= tol * h[1] || h[0] == 0.0) break;
+    if (h[0] >= 0.9 * prev_off && h[0] <= 1e-20 * h[1]) break;  // stagnated at the noise floor
+    prev_off = h[0];
     for (int r = 0; r < nb - 1; ++r) {
-      k_jacobi_pairs<<<nb / 2, 256, sm_pairs, s>>>(w.W, dp, nb, r, w.U, 12);
+      k_jacobi_pairs<<<nb / 2, 256, sm_pairs, s>>>(w.W, dp, nb, r, w.U, 6);
       k_jacobi_apply<<<dim3(dp / JP, nb / 2), 256, sm_apply, s>>>(w.W, dp, nb, r, w.U, 1);
       k_jacobi_apply<<<dim3(dp / JP, nb / 2), 256, sm_apply, s>>>(w.W, dp, nb, r, w.U, 0);
       k_jacobi_apply<<<dim3(dp / JP, nb / 2), 256, sm_apply, s>>>(w.V, dp, nb, r, w.U, 1);
       count_launch(4);
     }
   }
+  if (trace) cudaEventRecord(t2, s);
+  if (warm_B != nullptr) {  // eigenvectors = B_prev V: Tt = V^T, Bt = B_prev Tt^T
+    k_transpose<<<dim3(dp / 32, dp / 32), dim3(32, 8), 0, s>>>(w.V, w.Tt, dp);
+    GemmEpi e{};
+    e.mode = GEMM_STORE;
+    e.ldo = dp;
+    e.out = w.Bt;
+    run_gemm_nt(d, d, d, warm_B, dp, w.Tt, dp, e, s);
+    count_launch(1);
+    Vsrc = w.Bt;
+  }
   k_eig_diag<<<nblk(d, 256), 256, 0, s>>>(w.W, dp, d, w.t1);
   count_launch(1);
   run_rank(w.t1, d, 0, w.order, s);  // ascending, ties by index
-  k_eig_finish<<<nblk(d, 8), 256, 0, s>>>(w.V, dp, d, w.order, w.t1, vecs, evals);
+  k_eig_finish<<<nblk(d, 8), 256, 0, s>>>(Vsrc, dp, d, w.order, w.t1, vecs, evals);
   count_launch(1);
   cudaMemcpyAsync(evals_min, evals, sizeof(double), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
   if (cudaGetLastError() != cudaSuccess) return -1;
+  if (trace) {
+    float pre = 0, sw = 0;
+    cudaEventElapsedTime(&pre, t0, t1);
+    cudaEventElapsedTime(&sw, t1, t2);
+    fprintf(stderr, "[eig] d=%d warm=%d sweeps=%d prologue=%.1f ms sweeps=%.1f ms (%.1f ms/sweep)\n", d,
+            warm_B != nullptr, sweep, pre, sw, sweep ? sw / sweep : 0.f);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaEventDestroy(t2);
+  }
   return sweep;
 }
 

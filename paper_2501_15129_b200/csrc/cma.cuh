@@ -34,6 +34,8 @@ struct CmaDev {
   double* pc;           // d
   double* W;            // dp x dp Jacobi work (A)
   double* V;            // dp x dp Jacobi rotations
+  double* Bt;           // dp x dp scratch (warm start)
+  double* Tt;           // dp x dp scratch (warm start)
   double* U;            // (dp/64) * 64 * 64: per-pair 64x64 rotations
   double* evals;        // dp
   int* order;           // dp
@@ -73,7 +75,9 @@ cudaError_t run_cma_add_diag(double* C, int d, int dp, double v, cudaStream_t s)
 // each normalised so its largest-|.| component is positive (the oracle's
 // convention; Eigen's signs are arbitrary).  Work buffers from CmaDev.
 // Returns the number of sweeps used, or < 0 on error.
+// warm_B (optional, dp x dp): previous eigenvectors; Jacobi then runs on
+// B^T A B (nearly diagonal when A changed little) and returns B V.
 int sym_eig_jacobi(CmaDev& w, const double* A, int d, double* evals_host_min, double* vecs, double* evals,
-                   cudaStream_t s);
+                   cudaStream_t s, const double* warm_B = nullptr);
 
 }  // namespace evorl_b200

@@ -250,6 +250,7 @@ extern "C" void evorl_es_default_config(evorl_es_config* c) {
   c->cem_decay_iters = 2000;
   c->precision = EVORL_PREC_F64;
   c->device = 0;
+  c->cmaes_eig_every = 1;
 }
 
 template <typename T>
@@ -268,7 +269,7 @@ static void free_all(evorl_es* s) {
   for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1})
     if (ev) cudaEventDestroy(ev);
   void* cm[] = {s->cma.d_w, s->cma.dev.C, s->cma.dev.B, s->cma.dev.D, s->cma.dev.ps, s->cma.dev.pc,
-                s->cma.dev.W, s->cma.dev.V, s->cma.dev.U, s->cma.dev.evals, s->cma.dev.order, s->cma.dev.zD,
+                s->cma.dev.W, s->cma.dev.V, s->cma.dev.Bt, s->cma.dev.Tt, s->cma.dev.U, s->cma.dev.evals, s->cma.dev.order, s->cma.dev.zD,
                 s->cma.dev.ytT, s->cma.dev.wyT, s->cma.dev.yw, s->cma.dev.t1, s->cma.dev.cih, s->cma.dev.red};
   for (void* p : cm)
     if (p) cudaFree(p);
@@ -410,6 +411,8 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
     A(dalloc(&v.B, dp2));
     A(dalloc(&v.W, dp2));
     A(dalloc(&v.V, dp2));
+    A(dalloc(&v.Bt, dp2));
+    A(dalloc(&v.Tt, dp2));
     A(dalloc(&v.U, (size_t)(v.dp / 64) * 64 * 64));
     A(dalloc(&v.D, v.dp));
     A(dalloc(&v.ps, v.dp));
@@ -766,12 +769,18 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       c.sigma *= std::exp((c.cs / c.ds) * (ps_norm / c.chi_n - 1.0));
       c.generation += 1;
       // re-factorise; re-condition when eigenvalues fall to <= 0
+      // (EXTENSION: only every cmaes_eig_every-th generation; 1 = reference)
+      const int k_eig = std::max(1, s->cfg.cmaes_eig_every);
+      if (c.generation % k_eig != 0) {
+        sigma = c.sigma;
+        break;
+      }
       double evmin = 0.0;
-      int sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st);
+      int sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st, v.B);
       if (sw < 0) return set_err(EVORL_E_CUDA, "cmaes: eigensolver failed: %s", cudaGetErrorString(cudaGetLastError()));
       if (evmin <= 0.0) {
         CK(run_cma_add_diag(v.C, d, dp, 1e-10 - evmin, st));
-        sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st);
+        sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st, v.B);
         if (sw < 0) return set_err(EVORL_E_CUDA, "cmaes: eigensolver failed");
         c.recondition_count += 1;
       }

@@ -1,6 +1,7 @@
 // kernels.cu -- noise, ranks, fitness reduction, EC tells, observation
 // statistics and init for the B200 generation path.  Every kernel cites the
 // reference function it restates.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 
@@ -103,9 +104,122 @@ __global__ void k_rank(const double* keys, int n, int desc, int* rank) {
   }
   if (i < n) rank[i] = r;
 }
+// Stable LSD radix sort (4-bit digits) of the order-preserving key images in
+// one CTA of 1024 threads: thread t owns a contiguous chunk; per pass a
+// digit-major / thread-minor histogram is exclusive-scanned, so equal digits
+// keep thread order then chunk order (stability, i.e. std::stable_sort's tie
+// rule).  Passes whose digit is constant over all keys are skipped.  Output:
+// rank[i] = position of i.  Scratch: 2n u64 + 2n int in global memory.
+constexpr int RADIX_T = 1024;
+__global__ void __launch_bounds__(RADIX_T) k_radix_rank(const double* keys, int n, int desc, uint64_t* kb,
+                                                        int* ib, int* rank) {
+  __shared__ uint16_t hist[16][RADIX_T];
+  __shared__ uint32_t wsum[RADIX_T / 32];
+  __shared__ int any_split;
+  const int t = threadIdx.x;
+  const int chunk = (n + RADIX_T - 1) / RADIX_T;
+  const int i0 = min(n, t * chunk), i1 = min(n, i0 + chunk);
+  uint64_t* k0 = kb;
+  uint64_t* k1 = kb + n;
+  int* x0 = ib;
+  int* x1 = ib + n;
+  for (int i = i0; i < i1; ++i) {
+    const uint64_t k = ordered_key(keys[i]);
+    k0[i] = desc ? ~k : k;
+    x0[i] = i;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 16; ++pass) {
+    const int shift = 4 * pass;
+    for (int d = 0; d < 16; ++d) hist[d][t] = 0;
+    if (t == 0) any_split = 0;
+    __syncthreads();
+    for (int i = i0; i < i1; ++i) ++hist[(k0[i] >> shift) & 15][t];
+    __syncthreads();
+    // skip the pass if one digit holds every key (common for high bits)
+    if (t < 16) {
+      uint32_t c = 0;
+      for (int q = 0; q < RADIX_T; ++q) c += hist[t][q];
+      if (c != 0 && c != (uint32_t)n) any_split = 1;
+    }
+    __syncthreads();
+    if (!any_split) continue;
+    // exclusive scan of the 16 x 1024 counts in (digit, thread) order:
+    // thread t owns linear entries [16t, 16t + 16)
+    uint16_t* flat = &hist[0][0];
+    uint32_t local = 0;
+    for (int q = 0; q < 16; ++q) local += flat[16 * t + q];
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((t & 31) >= o) incl += v;
+    }
+    if ((t & 31) == 31) wsum[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+      uint32_t w = wsum[t];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, w, o);
+        if (t >= o) w += v;
+      }
+      wsum[t] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    // exclusive start offset of each owned (digit, thread) entry; the 16x1024
+    // offsets (u32: they exceed u16) are published through the idle output
+    // key buffer k1 (>= 8192 u64 = 16384 u32 since n >= 8192 on this path)
+    uint32_t run = incl - local + ((t >> 5) ? wsum[(t >> 5) - 1] : 0u);
+    uint32_t* offs = reinterpret_cast<uint32_t*>(k1);
+    for (int q = 0; q < 16; ++q) {
+      offs[16 * t + q] = run;
+      run += flat[16 * t + q];
+    }
+    __syncthreads();
+    // this thread's column (d, t) lives at linear 1024*d + t
+    uint32_t my[16];
+    for (int d = 0; d < 16; ++d) my[d] = offs[RADIX_T * d + t];
+    __syncthreads();  // k1 is overwritten by the scatter below
+    for (int i = i0; i < i1; ++i) {
+      const uint64_t k = k0[i];
+      const int d = (int)((k >> shift) & 15);
+      const uint32_t p = my[d]++;
+      k1[p] = k;
+      x1[p] = x0[i];
+    }
+    __syncthreads();
+    uint64_t* tk = k0;
+    k0 = k1;
+    k1 = tk;
+    int* tx = x0;
+    x0 = x1;
+    x1 = tx;
+  }
+  for (int i = i0; i < i1; ++i) rank[x0[i]] = i;
+}
+
+static uint64_t* g_radix_k = nullptr;
+static int* g_radix_i = nullptr;
+static int g_radix_cap = 0;
+
 cudaError_t run_rank(const double* keys, int n, int desc, int* rank, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_rank<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, desc, rank);
+  if (n < 8192) {  // O(n^2 / P) counting is faster than 16 serial passes here
+    k_rank<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, desc, rank);
+    EVB_CHECK_LAUNCH();
+  }
+  if (n > g_radix_cap) {
+    cudaStreamSynchronize(s);
+    if (g_radix_k) cudaFree(g_radix_k);
+    if (g_radix_i) cudaFree(g_radix_i);
+    // k needs 2n u64 (+ the 16 x 1024 u32 offset table in the spare half)
+    const size_t kn = std::max<size_t>(2 * (size_t)n, (size_t)n + 16 * RADIX_T / 2 + 1);
+    if (cudaMalloc(&g_radix_k, sizeof(uint64_t) * kn) != cudaSuccess) return cudaErrorMemoryAllocation;
+    if (cudaMalloc(&g_radix_i, sizeof(int) * 2 * (size_t)n) != cudaSuccess) return cudaErrorMemoryAllocation;
+    g_radix_cap = n;
+  }
+  k_radix_rank<<<1, RADIX_T, 0, s>>>(keys, n, desc, g_radix_k, g_radix_i, rank);
   EVB_CHECK_LAUNCH();
 }
 

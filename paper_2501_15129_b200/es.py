@@ -77,6 +77,7 @@ class EsConfig:
     cem_decay_iters: int = 2000
     precision: str = "f64"               # "f64" (parity) | "f32" (throughput)
     device: int = 0
+    cmaes_eig_every: int = 1             # EXTENSION: lazy CMA-ES eigendecomposition period
 
     def to_c(self) -> _lib.EsConfigC:
         c = _lib.EsConfigC()
@@ -107,7 +108,7 @@ class EsConfig:
         for k in ("openes_mirrored", "openes_noise_table", "ves_mirrored"):
             setattr(c, k, int(bool(getattr(self, k))))
         for k in ("openes_noise_table_size", "ars_elites", "ves_elites", "cmaes_elites",
-                  "cmaes_max_dim", "cem_elites", "cem_decay_iters", "device"):
+                  "cmaes_max_dim", "cem_elites", "cem_decay_iters", "device", "cmaes_eig_every"):
             setattr(c, k, int(getattr(self, k)))
         c.precision = _lib.PREC_F64 if self.precision == "f64" else _lib.PREC_F32
         return c

@@ -79,7 +79,7 @@ def test_gaussian_matrix_counter_addressed(oracle, evb):
 
 
 # ---------------------------------------------------------------- P1 ranks
-@pytest.mark.parametrize("n", [1, 2, 3, 7, 128, 1000, 4096, 20000])
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 128, 1000, 4096, 8192, 20000, 65536])
 def test_ranks_bitexact(oracle, evb, n):
     rng = np.random.default_rng(n)
     f = rng.standard_normal(n)
