@@ -189,7 +189,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32", "tc"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -306,6 +306,14 @@ def main():
         bound, unit, peak_src = "fp64", "TFLOP/s", (
             "measured live: DFMA-bound microkernel (evorl_measure_fp64_peak); "
             "MEASURED_PEAKS.json has no FP64 figure")
+    elif args.precision == "tc":
+        # the dense W2 x W1 layer runs on tcgen05 (kind::f16, 3 passes); the
+        # roof is the dense 16-bit tensor peak of MEASURED_PEAKS.json (fp16 and
+        # bf16 run at the same rate), counting only the useful (1-pass) flops
+        peak = load_peaks().get("bf16_tflops")
+        bound, unit, peak_src = "tensor", "TFLOP/s", (
+            "MEASURED_PEAKS.json bf16_tflops (burst; fp16 kind::f16 same rate); achieved counts "
+            "the MLP's algorithmic flops, not the 3x hi/lo split passes")
     else:
         peak = None
         bound, unit, peak_src = "fp32", "TFLOP/s", "measured live: FFMA is not in MEASURED_PEAKS.json"
@@ -314,7 +322,8 @@ def main():
     achieved = flops_launch / (roll_ms * 1e-3) / 1e12 if roll_ms else None
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                 "frac": (achieved / peak) if (achieved and peak) else None,
-                "traffic": None, "kernel": "rollout_kernel (fused obs-norm/MLP/env/return)",
+                "traffic": None, "kernel": ("rollout_tc_kernel (tcgen05 hidden layer, fused obs-norm/MLP/env/return)"
+                          if args.precision == "tc" else "rollout_kernel (fused obs-norm/MLP/env/return)"),
                 "algorithmic_flops_per_launch": flops_launch,
                 "flops_per_env_step": F, "peak_source": peak_src,
                 "rollout_ms_per_launch": roll_ms, "rollout_share_of_step":

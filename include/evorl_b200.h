@@ -22,7 +22,11 @@
  *    one orchestrating thread, proj/include/evorl/thread_pool.hpp:27-29).
  *  - Precision: EVORL_PREC_F64 evaluates the policy in fp64 (parity mode, same
  *    arithmetic type as the reference); EVORL_PREC_F32 evaluates the policy
- *    GEMMs in fp32 (env dynamics, returns, noise and the EC update stay fp64).
+ *    GEMMs in fp32 (env dynamics, returns, noise and the EC update stay fp64);
+ *    EVORL_PREC_TC runs the dense hidden layer of obs -> W1 -> W2 -> O policies
+ *    (W2 a multiple of 128, W1 <= 256) on the tcgen05 tensor cores as a
+ *    3-pass fp16 hi/lo split with fp32 accumulation in TMEM (fp32-level
+ *    accuracy) and the other layers in fp32; other shapes run as EVORL_PREC_F32.
  */
 #ifndef EVORL_B200_H
 #define EVORL_B200_H
@@ -47,7 +51,7 @@ enum {
   EVORL_E_UNSUPPORTED = 7       /* valid reference input the device path refuses */
 };
 
-enum { EVORL_PREC_F64 = 0, EVORL_PREC_F32 = 1 };
+enum { EVORL_PREC_F64 = 0, EVORL_PREC_F32 = 1, EVORL_PREC_TC = 2 };
 enum { EVORL_ENV_CARTPOLE = 0, EVORL_ENV_PENDULUM = 1 };
 enum { EVORL_ALGO_OPENES = 0, EVORL_ALGO_ARS = 1, EVORL_ALGO_VES = 2, EVORL_ALGO_CMAES = 3,
        EVORL_ALGO_CEM = 4 };

@@ -23,7 +23,8 @@ EVORL_E_CONFIG = 5
 EVORL_E_CUDA = 6
 EVORL_E_UNSUPPORTED = 7
 
-PREC_F64, PREC_F32 = 0, 1
+PREC_F64, PREC_F32, PREC_TC = 0, 1, 2
+PRECISIONS = {"f64": PREC_F64, "f32": PREC_F32, "tc": PREC_TC}
 ENV_CARTPOLE, ENV_PENDULUM = 0, 1
 ALGO = {"openes": 0, "ars": 1, "ves": 2, "cmaes": 3, "cem": 4}
 NORM = {"auto": -1, "none": 0, "vbn": 1, "running_stats": 2}

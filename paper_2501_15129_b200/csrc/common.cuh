@@ -155,12 +155,13 @@ EVB_DEV void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
 // ------------------------------------------------------------------- errors
 // Device error word: lowest failing lane wins (proj/src/thread_pool.cpp:49-51).
 // Encoding: (lane << 8) | (kind << 4) | layer; kind 1..3 = EnvFault variants,
-// kind 4 = NetFault.  0xFFFF... = no error.
+// kind 4 = NetFault, kind 5 = tcgen05 operand range (EVORL_PREC_TC only).  0xFFFF... = no error.
 enum : uint32_t {
   FAULT_ENV_STATE = 1,
   FAULT_ENV_ACTION = 2,
   FAULT_ENV_SUCCESSOR = 3,
   FAULT_NET = 4,
+  FAULT_TC_RANGE = 5,  // EVORL_PREC_TC: a finite activation beyond the fp16 split's range
 };
 EVB_DEV void record_fault(unsigned long long* word, uint64_t lane, uint32_t kind, uint32_t layer) {
   const unsigned long long code = (lane << 8) | ((uint64_t)kind << 4) | (layer & 15u);

@@ -144,6 +144,11 @@ static int fault_to_error(unsigned long long code) {
     case FAULT_ENV_SUCCESSOR:
       return set_err(EVORL_E_ENV_FAULT,
                      "env_step: non-finite successor state (numeric divergence) [lane 0]");
+    case FAULT_TC_RANGE:
+      return set_err(EVORL_E_UNSUPPORTED,
+                     "precision tc: an activation of layer %u exceeds the fp16 hi/lo operand range "
+                     "(|h| > 60000); use EVORL_PREC_F32 or EVORL_PREC_F64",
+                     layer);
     default:
       return set_err(EVORL_E_NET_FAULT, "forward: non-finite activations at layer %u", layer);
   }
@@ -290,8 +295,8 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
     return set_err(EVORL_E_INVALID_ARGUMENT, "unknown env id");
   if (cfg->algo == EVORL_ALGO_OPENES && cfg->openes_noise_table)
     return set_err(EVORL_E_UNSUPPORTED, "openes noise_table mode: device path not built in this revision");
-  if (cfg->precision != EVORL_PREC_F64 && cfg->precision != EVORL_PREC_F32)
-    return set_err(EVORL_E_INVALID_ARGUMENT, "precision must be EVORL_PREC_F64 or EVORL_PREC_F32");
+  if (cfg->precision != EVORL_PREC_F64 && cfg->precision != EVORL_PREC_F32 && cfg->precision != EVORL_PREC_TC)
+    return set_err(EVORL_E_INVALID_ARGUMENT, "precision must be EVORL_PREC_F64, EVORL_PREC_F32 or EVORL_PREC_TC");
   if (cfg->pop < 1 || cfg->fitness_episodes < 1)
     return set_err(EVORL_E_INVALID_ARGUMENT, "ec.pop and ec.fitness_episodes must be positive");
   auto* s = new evorl_es();
@@ -319,7 +324,7 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   const bool cta_ok = plan_rollout(s->net, s->env.obs_dim, s->e, cfg->precision, &s->plan);
   // warp-per-lane only pays when there are enough lanes to fill the SMs
   // (>= 512 lanes); fewer lanes get a whole CTA each to cut step latency.
-  s->warp_path = (long long)cfg->pop * s->e >= 512 &&
+  s->warp_path = !(cta_ok && s->plan.tc) && (long long)cfg->pop * s->e >= 512 &&
                  plan_rollout_warp(s->net, s->env.obs_dim, s->e, cfg->precision, &s->wplan);
   if (!cta_ok && !s->warp_path) {
     delete s;
@@ -1174,8 +1179,11 @@ extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp
   if (netd->input_dim != env.obs_dim) return set_err(EVORL_E_INVALID_ARGUMENT, "net input_dim != obs_dim");
   SmemPlan plan{};
   WarpPlanOut wplan{};
-  const bool use_warp = plan_rollout_warp(net, env.obs_dim, e, precision, &wplan);
-  if (!plan_rollout(net, env.obs_dim, e, precision, &plan) && !use_warp)
+  if (precision < EVORL_PREC_F64 || precision > EVORL_PREC_TC)
+    return set_err(EVORL_E_INVALID_ARGUMENT, "unknown precision");
+  const bool cta_ok = plan_rollout(net, env.obs_dim, e, precision, &plan);
+  const bool use_warp = !(cta_ok && plan.tc) && plan_rollout_warp(net, env.obs_dim, e, precision, &wplan);
+  if (!cta_ok && !use_warp)
     return set_err(EVORL_E_UNSUPPORTED, "policy too large for a shared-memory resident team");
   const long long d = net.d;
   Scratch sp, sr, ss, sst, sag, sn, sf;

@@ -47,35 +47,6 @@ EVB_DEV uint32_t ld_cluster_u32(uint32_t addr) {
   return v;
 }
 
-// Candidate parameter p of agent `agent` (global population index).
-EVB_DEV double param_value(const ParamDesc& P, long long d, int agent_local, int agent,
-                           long long p) {
-  switch (P.src) {
-    case SRC_OPENES: {  // proj/src/ec.cpp:87-94: (sigma * eps) + mean, rows [base,n) = -eps
-      long long row = agent;
-      bool neg = false;
-      if (P.mirrored && agent >= P.base) {
-        row = agent - P.base;
-        neg = true;
-      }
-      double eps = normal_at(P.ask_key, (uint64_t)(row * d + p));
-      if (neg) eps = -eps;
-      return dadd(dmul(P.sigma, eps), P.mean[p]);
-    }
-    case SRC_ARS: {  // proj/src/ec.cpp:119-123: interleaved mean +/- sigma*delta_k
-      const long long k = agent >> 1;
-      const double sd = dmul(P.sigma, normal_at(P.ask_key, (uint64_t)(k * d + p)));
-      return (agent & 1) ? dsub(P.mean[p], sd) : dadd(P.mean[p], sd);
-    }
-    case SRC_CEM: {  // proj/src/ec.cpp:306-313: z * sqrt(var) + mean
-      const double z = normal_at(P.ask_key, (uint64_t)((long long)agent * d + p));
-      return dadd(dmul(z, sqrt(P.var[p])), P.mean[p]);
-    }
-    default:
-      return P.params[(long long)agent_local * d + p];
-  }
-}
-
 __global__ void k_materialize(const ParamDesc P, long long d, int a0, int a1, double* out) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long n = (long long)(a1 - a0) * d;
@@ -715,6 +686,16 @@ static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int
 
 bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan) {
   const int ET = e >= 5 ? 16 : (e >= 2 ? 4 : 1);
+  if (precision == 2) {  // EVORL_PREC_TC: tcgen05 team if the shape fits, else the fp32 team
+    if (plan_rollout_tc(net, obs_dim, e, &plan->tcp)) {
+      plan->tc = 1;
+      plan->ET = 16;
+      plan->C = plan->tcp.data[0];
+      return true;
+    }
+    precision = 1;
+  }
+  plan->tc = 0;
   const int tsize = precision == 0 ? 8 : 4;
   for (int C : {1, 2, 4, 8}) {
     // fp64 with 16 lanes: hidden-layer GEMMs on the FP64 tensor cores
@@ -778,6 +759,7 @@ static cudaError_t launch_t(const RolloutArgs& a, cudaStream_t s) {
 
 cudaError_t launch_rollout(const RolloutArgs& a, int precision, cudaStream_t stream) {
   if (a.n_agents <= 0) return cudaSuccess;
+  if (a.plan.tc) return launch_rollout_tc(a, a.plan.tcp, stream);
   return precision == 0 ? launch_t<double>(a, stream) : launch_t<float>(a, stream);
 }
 

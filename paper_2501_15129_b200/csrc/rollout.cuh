@@ -49,6 +49,39 @@ struct NormParams {
   double den[4];
 };
 
+// Candidate parameter p of agent `agent` (global population index).
+EVB_DEV double param_value(const ParamDesc& P, long long d, int agent_local, int agent,
+                           long long p) {
+  switch (P.src) {
+    case SRC_OPENES: {  // proj/src/ec.cpp:87-94: (sigma * eps) + mean, rows [base,n) = -eps
+      long long row = agent;
+      bool neg = false;
+      if (P.mirrored && agent >= P.base) {
+        row = agent - P.base;
+        neg = true;
+      }
+      double eps = normal_at(P.ask_key, (uint64_t)(row * d + p));
+      if (neg) eps = -eps;
+      return dadd(dmul(P.sigma, eps), P.mean[p]);
+    }
+    case SRC_ARS: {  // proj/src/ec.cpp:119-123: interleaved mean +/- sigma*delta_k
+      const long long k = agent >> 1;
+      const double sd = dmul(P.sigma, normal_at(P.ask_key, (uint64_t)(k * d + p)));
+      return (agent & 1) ? dsub(P.mean[p], sd) : dadd(P.mean[p], sd);
+    }
+    case SRC_CEM: {  // proj/src/ec.cpp:306-313: z * sqrt(var) + mean
+      const double z = normal_at(P.ask_key, (uint64_t)((long long)agent * d + p));
+      return dadd(dmul(z, sqrt(P.var[p])), P.mean[p]);
+    }
+    default:
+      return P.params[(long long)agent_local * d + p];
+  }
+}
+
+struct TcPlanOut {
+  int data[32];  // TcPlan (rollout_tc.cu); data[0] = cluster size
+};
+
 struct SmemPlan {
   int C;             // cluster size (CTAs per team)
   int TR;            // rows per thread
@@ -64,6 +97,8 @@ struct SmemPlan {
   int off_w[MAXL], off_b[MAXL];
   int off_wout, off_bout, off_x0, off_h[MAXL], off_part, off_pout, off_mask, off_bar;
   int bytes;
+  int tc;         // 1: EVORL_PREC_TC tcgen05 team (rollout_tc.cu), plan in tcp
+  TcPlanOut tcp;
 };
 
 struct RolloutArgs {
@@ -102,5 +137,10 @@ cudaError_t launch_rollout_warp(const RolloutArgs& a, const WarpPlanOut& plan, i
 // Materialise candidates [a0, a1) (row-major, d each) from a ParamDesc.
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
                             cudaStream_t stream);
+
+// Tensor-core rollout (rollout_tc.cu, precision EVORL_PREC_TC): obs -> W1 -> W2 -> O
+// policies with W2 a multiple of 128; the W2 x W1 layer runs on tcgen05.
+bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out);
+cudaError_t launch_rollout_tc(const RolloutArgs& a, const TcPlanOut& plan, cudaStream_t stream);
 
 }  // namespace evorl_b200

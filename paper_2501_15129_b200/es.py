@@ -75,7 +75,7 @@ class EsConfig:
     cem_noise_start: float = 1e-3
     cem_noise_end: float = 1e-5
     cem_decay_iters: int = 2000
-    precision: str = "f64"               # "f64" (parity) | "f32" (throughput)
+    precision: str = "f64"               # "f64" (parity) | "f32" | "tc" (tcgen05 hidden layer)
     device: int = 0
     cmaes_eig_every: int = 1             # EXTENSION: lazy CMA-ES eigendecomposition period
 
@@ -110,7 +110,7 @@ class EsConfig:
         for k in ("openes_noise_table_size", "ars_elites", "ves_elites", "cmaes_elites",
                   "cmaes_max_dim", "cem_elites", "cem_decay_iters", "device", "cmaes_eig_every"):
             setattr(c, k, int(getattr(self, k)))
-        c.precision = _lib.PREC_F64 if self.precision == "f64" else _lib.PREC_F32
+        c.precision = _lib.PRECISIONS[self.precision]
         return c
 
 
@@ -419,7 +419,7 @@ def batched_rollout(env: str, net: _lib.MlpDesc, params, envs_per_agent: int, ke
     stats = np.empty((m, 9)) if track_obs_stats else None
     check(_lib.load().evorl_batched_rollout(
         C.byref(ed), C.byref(net), C.byref(nc) if nc is not None else None, _p(params), m, e,
-        count, hi, lo, _lib.PREC_F64 if precision == "f64" else _lib.PREC_F32, _p(rets),
+        count, hi, lo, _lib.PRECISIONS[precision], _p(rets),
         _p(steps), _p(stats) if stats is not None else None))
     return rets, steps, stats
 
