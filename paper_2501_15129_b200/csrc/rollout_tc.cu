@@ -12,12 +12,19 @@
 //     lo = fp16((x - hi) * 2^11); D0 = Ahi.Bhi and D1 = Ahi.Blo + Alo.Bhi are
 //     accumulated in fp32 in TMEM and combined as D0 + D1 * 2^-11 (~22
 //     significant bits: fp32-level, within RTOL_F32 of the fp64 reference).
-//   * Operands: A = this CTA's 128-row slice of W2 (hi and lo, 128 KB) stays in
-//     shared memory for the horizon in the canonical no-swizzle K-major UMMA
-//     layout (8-row x 16-byte core matrices); B = the 16-lane activation block
-//     is rewritten every step by the layer-0 threads.  One thread issues the
-//     3 x K/16 MMAs, tcgen05.commit arrives on an mbarrier, and four warps
-//     read the accumulator lanes back with tcgen05.ld.32x32b.
+//   * Operand residency (per CTA, for the whole horizon): A_hi (this CTA's
+//     128 weight rows) in TENSOR MEMORY, written once by tcgen05.st; A_lo in
+//     shared memory in the canonical no-swizzle K-major layout.  TMEM holds
+//     256 columns (D0, D1, A_hi) and SMEM ~100 KB, so two teams share an SM
+//     and one team's env phase overlaps the other's GEMM.
+//   * Per k-step of 16: one TS MMA  D[0:32] += A_hi . [B_hi | B_lo]  (N = 32,
+//     A from TMEM) and one SS MMA  D[16:32] += A_lo . B_hi  (N = 16), issued
+//     by one thread; tcgen05.commit arrives on an mbarrier.
+//   * Epilogue on all 8 warps (tcgen05.ld.32x32b.x8: warp w reads TMEM lanes
+//     32(w%4).. and lane columns 8(w/4)..), bias + ReLU, and the output layer
+//     fused in: each thread's row contributes W2o[r] * h to the (o, lane)
+//     outputs, reduced across the warp by a shuffle reduce-scatter and across
+//     the 4 row-quadrants and the cluster in a fixed order.
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -29,17 +36,18 @@ namespace evorl_b200 {
 
 constexpr int TC_THREADS = 256;
 constexpr int TC_M = 128;  // rows per CTA (UMMA M)
-constexpr int TC_N = 16;   // lanes per team (UMMA N)
+constexpr int TC_N = 16;   // lanes per team
+constexpr int TC_TMEM_COLS = 256;
+constexpr int TC_COL_A = 32;  // A_hi starts at TMEM column 32 (D0 = 0..15, D1 = 16..31)
 constexpr float TC_LO_SCALE = 2048.0f;
 constexpr int TC_RANGE_ROW = 8;  // bad-layer row value: operand out of the split's range
 constexpr int TC_OK_ROW = 15;    // bad-layer row value: no fault
+constexpr int TC_MAXO = 8;
 
 struct TcPlan {
   int C;       // cluster size = W2 / 128
   int W1, W2;  // hidden widths
-  int KSo;     // output-layer k-split
-  int off_Ahi, off_Alo, off_Bhi, off_Blo, off_W0, off_b0, off_b1, off_W2o, off_b2, off_x0, off_h2,
-      off_part, off_pout, off_mask, off_bar, off_tslot;
+  int off_Alo, off_B, off_W0, off_b0, off_x0, off_red, off_pout, off_mask, off_bar, off_tslot;
   int bytes;
 };
 
@@ -55,58 +63,83 @@ EVB_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1, SWIZZLE_NONE
 }
 
-// kind::f16, A = B = f16 (K-major), D = f32, M = 128, N = 16
-constexpr uint32_t TC_IDESC = (1u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+// kind::f16 instruction descriptor: A = B = f16 (K-major), D = f32
+constexpr uint32_t tc_idesc(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 
-EVB_DEV void tc_mma(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+EVB_DEV void tc_mma_ss(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
-      "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
-
-EVB_DEV void tc_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
+EVB_DEV void tc_mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
-EVB_DEV void split_store(unsigned char* hi_base, unsigned char* lo_base, uint32_t off, float x) {
-  const __half h = __float2half_rn(x);
-  const __half l = __float2half_rn((x - __half2float(h)) * TC_LO_SCALE);
-  *reinterpret_cast<__half*>(hi_base + off) = h;
-  *reinterpret_cast<__half*>(lo_base + off) = l;
+EVB_DEV void tc_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+}
+EVB_DEV void tc_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+EVB_DEV void split_f16(float x, __half& h, __half& l) {
+  h = __float2half_rn(x);
+  l = __float2half_rn((x - __half2float(h)) * TC_LO_SCALE);
+}
+EVB_DEV uint32_t pack2(__half a, __half b) {  // element k in the low half, k+1 in the high half
+  return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
 }
 
 template <int C>
-__global__ void __launch_bounds__(TC_THREADS, 1) rollout_tc_kernel(const __grid_constant__ RolloutArgs A,
+__global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_constant__ RolloutArgs A,
                                                                    const __grid_constant__ TcPlan P) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const NetDesc& N = A.net;
   const EnvDesc& E = A.env;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant, column half
   const int crank = C > 1 ? (int)cluster_ctarank() : 0;
   const int team = blockIdx.x / C;
   const int agent_local = team / A.groups;
   const int group = team % A.groups;
   const int agent = A.agent_offset + agent_local;
-  const int W1 = P.W1, W2 = P.W2, O = N.dims[3];
-  const int r0 = crank * TC_M;  // this CTA's rows of layer 1
+  const int W1 = P.W1, W2 = P.W2, O = N.dims[3], K0 = N.dims[0];
+  const int r0 = crank * TC_M;       // this CTA's rows of layer 1
+  const int row = quad * 32 + lane;  // the layer-1 row this thread owns in the epilogue
 
   for (int i = tid; i < P.bytes / 4; i += TC_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
   __syncthreads();
-  float* W0 = reinterpret_cast<float*>(smem + P.off_W0);   // [k][W1]
-  float* b0 = reinterpret_cast<float*>(smem + P.off_b0);   // W1
-  float* b1 = reinterpret_cast<float*>(smem + P.off_b1);   // TC_M (slice)
-  float* W2o = reinterpret_cast<float*>(smem + P.off_W2o); // [k_local][O]
-  float* b2 = reinterpret_cast<float*>(smem + P.off_b2);   // O
-  const int K0 = N.dims[0];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(TC_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  float* W0 = reinterpret_cast<float*>(smem + P.off_W0);  // [k][W1]
+  float* b0 = reinterpret_cast<float*>(smem + P.off_b0);  // W1
+  unsigned char* Alo = smem + P.off_Alo;
+  unsigned char* Bs = smem + P.off_B;  // 32 x W1: rows 0..15 = B_hi, 16..31 = B_lo
   // ---- prologue: this agent's parameters (regenerated or explicit)
   for (int i = tid; i < K0 * W1; i += TC_THREADS) {
     const int k = i / W1, r = i % W1;
@@ -114,37 +147,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rollout_tc_kernel(const __grid_
   }
   for (int r = tid; r < W1; r += TC_THREADS)
     b0[r] = (float)param_value(A.par, N.d, agent_local, agent, N.b_off[0] + r);
-  for (int i = tid; i < TC_M * W1; i += TC_THREADS) {  // A = W2 rows [r0, r0+128) x K = W1
-    const int r = i % TC_M, k = i / TC_M;
-    const float w =
-        (float)param_value(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + r);
-    split_store(smem + P.off_Ahi, smem + P.off_Alo, umma_off(r, k, TC_M), w);
+  // layer-1 weights of row `row`: A_hi -> TMEM (lanes = rows, 2 halves per
+  // column), A_lo -> SMEM.  Warp halves take alternate 16-wide k chunks.
+  for (int c = half; c < W1 / 16; c += 2) {
+    uint32_t packed[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      __half h[2], l[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = c * 16 + 2 * q + u;
+        const float w =
+            (float)param_value(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + row);
+        split_f16(w, h[u], l[u]);
+        *reinterpret_cast<__half*>(Alo + umma_off(row, k, TC_M)) = l[u];
+      }
+      packed[q] = pack2(h[0], h[1]);
+    }
+    tc_st8(tmem + ((uint32_t)(quad * 32) << 16) + TC_COL_A + c * 8, packed);
   }
-  for (int r = tid; r < TC_M; r += TC_THREADS)
-    b1[r] = (float)param_value(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + r);
-  for (int i = tid; i < TC_M * O; i += TC_THREADS) {
-    const int k = i / O, o = i % O;
-    W2o[i] = (float)param_value(A.par, N.d, agent_local, agent, N.w_off[2] + (long long)(r0 + k) * O + o);
-  }
-  for (int o = tid; o < O; o += TC_THREADS)
-    b2[o] = (float)param_value(A.par, N.d, agent_local, agent, N.b_off[2] + o);
-
-  // ---- TMEM (32 columns: D0 at 0, D1 at 16) and the MMA-completion mbarrier
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    mbar_init(mbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A visible to the tensor core
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  const float b1r = (float)param_value(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row);
+  float w2r[TC_MAXO];
+#pragma unroll
+  for (int o = 0; o < TC_MAXO; ++o)
+    w2r[o] = o < O ? (float)param_value(A.par, N.d, agent_local, agent,
+                                        N.w_off[2] + (long long)(r0 + row) * O + o)
+                   : 0.0f;
+  float b2[TC_MAXO];
+#pragma unroll
+  for (int o = 0; o < TC_MAXO; ++o)
+    b2[o] = o < O ? (float)param_value(A.par, N.d, agent_local, agent, N.b_off[2] + o) : 0.0f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A_lo visible to the tensor core
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tslot;
   if constexpr (C > 1) cluster_sync_all();
 
   // ---- lane state
@@ -167,8 +203,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rollout_tc_kernel(const __grid_
   nrm.active = 0;
   if (A.norm != nullptr) nrm = *A.norm;
   float* x0 = reinterpret_cast<float*>(smem + P.off_x0);    // [4][16]
-  float* h2 = reinterpret_cast<float*>(smem + P.off_h2);    // [TC_M][16]
-  float* part = reinterpret_cast<float*>(smem + P.off_part);
+  float* red = reinterpret_cast<float*>(smem + P.off_red);  // [4 quadrants][O][16]
   float* pout_base = reinterpret_cast<float*>(smem + P.off_pout);
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem + P.off_mask);
   const int OE = O * TC_N, OE1 = (O + 1) * TC_N;
@@ -201,47 +236,63 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rollout_tc_kernel(const __grid_
   };
   if (valid && eps_this > 0 && A.max_iters > 0) observe_into_x0(true);
 
+  const uint32_t id32 = tc_idesc(TC_M, 32), id16 = tc_idesc(TC_M, 16);
   for (int it = 0;; ++it) {
     if (tid < MAXL) mask[tid] = 0u;
     const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
     if (!__syncthreads_or(active)) break;
     float* pout = pout_base + (it & 1) * C * OE1;
 
-    // layer 0, replicated: h1 = relu(W0 x0 + b0) -> B operand (fp16 hi/lo)
+    // layer 0, replicated: h1 = relu(W0 x0 + b0) -> B operand (fp16 hi/lo).
+    // A warp stores one 8-lane x 8-row core matrix per unit as 32 packed
+    // words (one per bank): lane -> (lane e&7 = lane&7, row pair = lane>>3).
     {
-      const int e = tid & (TC_N - 1);
-      float xr[4];
+      const int el = lane & 7, rp = lane >> 3;
+      float xr[2][4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) xr[k] = k < K0 ? x0[k * TC_N + e] : 0.0f;
+      for (int eh = 0; eh < 2; ++eh)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xr[eh][k] = k < K0 ? x0[k * TC_N + eh * 8 + el] : 0.0f;
       uint32_t bad = 0u, range = 0u;
-      for (int r = tid >> 4; r < W1; r += TC_THREADS / TC_N) {
-        float z = 0.0f;
+      for (int u = warp; u < W1 / 4; u += TC_THREADS / 32) {
+        const int eh = u & 1, g = u >> 1;
+        const int e = eh * 8 + el, r = g * 8 + rp * 2;
+        __half hh[2], ll[2];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k < K0) z = fmaf(W0[k * W1 + r], xr[k], z);
-        z = z + b0[r];
-        const float h = z > 0.0f ? z : 0.0f;
-        if (h == INFINITY) bad = 1u;
-        else if (h > 60000.0f) range = 1u;  // finite but beyond the fp16 split's range
-        split_store(smem + P.off_Bhi, smem + P.off_Blo, umma_off(e, r, TC_N), h);
+        for (int v = 0; v < 2; ++v) {
+          float z = 0.0f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < K0) z = fmaf(W0[k * W1 + r + v], xr[eh][k], z);
+          z = z + b0[r + v];
+          const float h = z > 0.0f ? z : 0.0f;  // ReLU (NaN -> 0, as cwiseMax)
+          if (h == INFINITY) {
+            bad |= 1u << e;
+          } else if (h > 60000.0f) {
+            range |= 1u << e;  // finite but beyond the fp16 split's range
+          }
+          split_f16(h, hh[v], ll[v]);
+        }
+        *reinterpret_cast<uint32_t*>(Bs + umma_off(e, r, 32)) = pack2(hh[0], hh[1]);
+        *reinterpret_cast<uint32_t*>(Bs + umma_off(e + 16, r, 32)) = pack2(ll[0], ll[1]);
       }
-      if (bad) atomicOr(&mask[0], 1u << e);
-      if (range) atomicOr(&mask[MAXL - 1], 1u << e);
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      range = __reduce_or_sync(0xffffffffu, range);
+      if (lane == 0 && bad) atomicOr(&mask[0], bad);
+      if (lane == 0 && range) atomicOr(&mask[MAXL - 1], range);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    // layer 1 on tcgen05: 3 passes x W1/16 k-steps, issued by one thread
+    // layer 1 on tcgen05, issued by one thread
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t aHi = smem_u32(smem + P.off_Ahi), aLo = smem_u32(smem + P.off_Alo);
-      const uint32_t bHi = smem_u32(smem + P.off_Bhi), bLo = smem_u32(smem + P.off_Blo);
-      const uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (TC_N / 8) * 128;
+      const uint32_t aLo = smem_u32(Alo), b = smem_u32(Bs);
+      constexpr uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (32 / 8) * 128;
       for (int ks = 0; ks < W1 / 16; ++ks) {
-        const uint32_t ao = ks * 2 * a_lbo, bo = ks * 2 * b_lbo;
-        tc_mma(tmem, umma_desc(aHi + ao, a_lbo, 128), umma_desc(bHi + bo, b_lbo, 128), ks > 0);
-        tc_mma(tmem + 16, umma_desc(aHi + ao, a_lbo, 128), umma_desc(bLo + bo, b_lbo, 128), ks > 0);
-        tc_mma(tmem + 16, umma_desc(aLo + ao, a_lbo, 128), umma_desc(bHi + bo, b_lbo, 128), 1);
+        const uint64_t bd = umma_desc(b + ks * 2 * b_lbo, b_lbo, 128);
+        tc_mma_ts(tmem, tmem + TC_COL_A + ks * 8, bd, id32, ks > 0);  // D[0:32] += Ahi.[Bhi|Blo]
+        tc_mma_ss(tmem + 16, umma_desc(aLo + ks * 2 * a_lbo, a_lbo, 128), bd, id16, 1);  // D1 += Alo.Bhi
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_u32(mbar))
@@ -249,73 +300,89 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rollout_tc_kernel(const __grid_
     }
     mbar_wait_parity(mbar, (uint32_t)(it & 1));
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // epilogue: warps 0-3 own TMEM lanes 32w..32w+31 = rows of the slice
-    if (warp < 4) {
-      const int r = warp * 32 + lane;
-      float d0[16], d1[16];
-      tc_ld16(tmem + ((uint32_t)(warp * 32) << 16), d0);
-      tc_ld16(tmem + ((uint32_t)(warp * 32) << 16) + 16, d1);
+    // epilogue: row `row`, lanes 8*half .. 8*half+7; output layer fused
+    {
+      uint32_t d0[8], d1[8];
+      const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + half * 8;
+      tc_ld8(ta, d0);
+      tc_ld8(ta + 16, d1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float h[8];
       uint32_t bad = 0u;
-      const float bb = b1[r];
 #pragma unroll
-      for (int e = 0; e < TC_N; ++e) {
-        const float z = (d0[e] + d1[e] * (1.0f / TC_LO_SCALE)) + bb;
-        const float h = z > 0.0f ? z : 0.0f;
-        if (h == INFINITY) bad |= 1u << e;
-        h2[r * TC_N + e] = h;
+      for (int q = 0; q < 8; ++q) {
+        const float z = (__uint_as_float(d0[q]) + __uint_as_float(d1[q]) * (1.0f / TC_LO_SCALE)) + b1r;
+        h[q] = z > 0.0f ? z : 0.0f;
+        if (h[q] == INFINITY) bad |= 1u << (half * 8 + q);
       }
-      if (bad) atomicOr(&mask[1], bad);
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      if (lane == 0 && bad) atomicOr(&mask[1], bad);
+      // per output o: v[q] = w2[row][o] * h[q], summed over the warp's 32 rows
+      // by a reduce-scatter (lane bits 4,3,2 select the lane q it ends on)
+      const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, bb2 = (lane >> 2) & 1;
+#pragma unroll
+      for (int o = 0; o < TC_MAXO; ++o) {
+        if (o >= O) break;
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = w2r[o] * h[q];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float send = b4 ? v[i] : v[i + 4];
+          const float keep = b4 ? v[i + 4] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const float send = b3 ? v[i] : v[i + 2];
+          const float keep = b3 ? v[i + 2] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const float send = bb2 ? v[0] : v[1];
+          const float keep = bb2 ? v[1] : v[0];
+          v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        if ((lane & 3) == 0) red[(quad * O + o) * TC_N + half * 8 + b4 * 4 + b3 * 2 + bb2] = v[0];
+      }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-
-    // output layer partial over this CTA's 128 rows, reduced across the cluster
-    {
-      const int KSo = P.KSo;
-      const int kc = (TC_M + KSo - 1) / KSo;
-      for (int w = tid; w < OE * KSo; w += TC_THREADS) {
-        const int oe = w % OE, ks = w / OE;
-        const int o = oe / TC_N, e = oe % TC_N;
-        const int k0 = ks * kc, k1 = min(TC_M, k0 + kc);
-        float acc = 0.0f;
-        for (int k = k0; k < k1; ++k) acc = fmaf(W2o[k * O + o], h2[k * TC_N + e], acc);
-        part[w] = acc;
-      }
-      __syncthreads();
-      for (int oe = tid; oe < OE1; oe += TC_THREADS) {
-        float v;
-        if (oe < OE) {
-          v = part[oe];
-          for (int ks = 1; ks < KSo; ++ks) v += part[ks * OE + oe];
-        } else {
-          const int e = oe - OE;
-          int bl = (mask[MAXL - 1] >> e) & 1u ? TC_RANGE_ROW : TC_OK_ROW;
-          for (int l = 1; l >= 0; --l)
-            if ((mask[l] >> e) & 1u) bl = l;
-          v = (float)bl;
-        }
-        if constexpr (C > 1) {
-          const uint32_t la = smem_u32(pout + crank * OE1 + oe);
-#pragma unroll
-          for (int c = 0; c < C; ++c) st_cluster<float>(map_cluster(la, (uint32_t)c), v);
-        } else {
-          pout[oe] = v;
-        }
+    // this CTA's partial outputs (fixed quadrant order) -> every CTA of the cluster
+    for (int oe = tid; oe < OE1; oe += TC_THREADS) {
+      float v;
+      if (oe < OE) {
+        v = ((red[oe] + red[OE + oe]) + red[2 * OE + oe]) + red[3 * OE + oe];
+      } else {
+        const int e = oe - OE;
+        int bl = (mask[MAXL - 1] >> e) & 1u ? TC_RANGE_ROW : TC_OK_ROW;
+        for (int l = 1; l >= 0; --l)
+          if ((mask[l] >> e) & 1u) bl = l;
+        v = (float)bl;
       }
       if constexpr (C > 1) {
-        cluster_sync_all();
+        const uint32_t la = smem_u32(pout + crank * OE1 + oe);
+#pragma unroll
+        for (int c = 0; c < C; ++c) st_cluster<float>(map_cluster(la, (uint32_t)c), v);
       } else {
-        __syncthreads();
+        pout[oe] = v;
       }
+    }
+    if constexpr (C > 1) {
+      cluster_sync_all();
+    } else {
+      __syncthreads();
     }
 
     // head + env step (proj/src/rollout.cpp:57-90, :131-153)
     if (active) {
-      double z[8];
+      double z[TC_MAXO];
       bool nonfinite_out = false;
       int bad_layer = TC_OK_ROW;
       for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pout[c * OE1 + OE + tid]);
-      for (int o = 0; o < O && o < 8; ++o) {
+      for (int o = 0; o < O; ++o) {
         float v = pout[o * TC_N + tid];
         for (int c = 1; c < C; ++c) v += pout[c * OE1 + o * TC_N + tid];
         v = v + b2[o];
@@ -382,8 +449,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) rollout_tc_kernel(const __grid_
     }
     if (myfault) record_fault(A.fault, (uint64_t)((long long)agent * A.e + j), myfault, myfault_layer);
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TMEM_COLS));
+  }
   if constexpr (C > 1) cluster_sync_all();
 }
 
@@ -392,39 +463,25 @@ static int al(int x, int a) { return (x + a - 1) / a * a; }
 bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   if (net.nlayers != 3 || obs_dim > 4 || e < 5) return false;  // 16-lane teams, obs -> W1 -> W2 -> O
   const int W1 = net.dims[1], W2 = net.dims[2], O = net.dims[3];
-  if (W1 % 16 || W1 > 256 || W2 % TC_M || W2 / TC_M > 8 || O > 8) return false;
+  if (W1 % 16 || W1 > 2 * (TC_TMEM_COLS - TC_COL_A) || W2 % TC_M || W2 / TC_M > 8 || O > TC_MAXO)
+    return false;
   TcPlan p{};
   p.C = W2 / TC_M;
   p.W1 = W1;
   p.W2 = W2;
   int off = 0;
-  p.off_Ahi = off;
-  off = al(off + TC_M * W1 * 2, 1024);
   p.off_Alo = off;
   off = al(off + TC_M * W1 * 2, 1024);
-  p.off_Bhi = off;
-  off = al(off + TC_N * W1 * 2, 1024);
-  p.off_Blo = off;
-  off = al(off + TC_N * W1 * 2, 1024);
+  p.off_B = off;
+  off = al(off + 32 * W1 * 2, 1024);
   p.off_W0 = off;
   off = al(off + 4 * W1 * 4, 16);
   p.off_b0 = off;
   off = al(off + W1 * 4, 16);
-  p.off_b1 = off;
-  off = al(off + TC_M * 4, 16);
-  p.off_W2o = off;
-  off = al(off + TC_M * O * 4, 16);
-  p.off_b2 = off;
-  off = al(off + O * 4, 16);
   p.off_x0 = off;
   off = al(off + 4 * TC_N * 4, 16);
-  p.off_h2 = off;
-  off = al(off + TC_M * TC_N * 4, 16);
-  int KSo = 1;
-  while (KSo * 2 * O * TC_N <= TC_THREADS && TC_M / (KSo * 2) >= 4) KSo *= 2;
-  p.KSo = KSo;
-  p.off_part = off;
-  off = al(off + KSo * O * TC_N * 4, 16);
+  p.off_red = off;
+  off = al(off + 4 * O * TC_N * 4, 16);
   p.off_pout = off;
   off = al(off + 2 * p.C * (O + 1) * TC_N * 4, 16);
   p.off_mask = off;
