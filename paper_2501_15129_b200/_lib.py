@@ -12,7 +12,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libevorl_b200.so")
+# EVORL_B200_LIB selects another build of the same ABI (e.g. the profiling build)
+LIB_PATH = os.environ.get("EVORL_B200_LIB") or os.path.join(HERE, "libevorl_b200.so")
 
 EVORL_OK = 0
 EVORL_E_INVALID_ARGUMENT = 1

@@ -141,6 +141,20 @@ EVB_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
   const uint32_t ra = map_cluster(smem_u32(bar), rank);
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
 }
+// Arrive (release, CTA scope) on a local mbarrier.
+EVB_DEV void mbar_arrive_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Wait (acquire, CTA scope) for the phase with the given parity.
+EVB_DEV void mbar_wait_parity_cta(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
 // Wait (acquire, cluster scope) for the phase with the given parity.
 EVB_DEV void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);

@@ -43,6 +43,24 @@ constexpr float TC_LO_SCALE = 2048.0f;
 constexpr int TC_RANGE_ROW = 8;  // bad-layer row value: operand out of the split's range
 constexpr int TC_OK_ROW = 15;    // bad-layer row value: no fault
 constexpr int TC_MAXO = 8;
+constexpr int TC_L0_WARPS = 7;    // warps computing layer 0; warp 7 issues the MMAs
+constexpr int TC_MAX_ROUNDS = 4;  // layer-0 / MMA pipeline rounds (7 k-steps each): W1 <= 448
+
+#ifdef EVB_TC_PROFILE
+// Phase cycle counters (profiling build only, libevorl_b200_prof.so): thread 0
+// of every CTA accumulates clock64() deltas per phase and adds them here once.
+__device__ unsigned long long g_tc_prof[16];
+#define TC_MARK(i)                      \
+  do {                                  \
+    const long long t_ = clock64();     \
+    prof[i] += (unsigned long long)(t_ - tprev); \
+    tprev = t_;                         \
+  } while (0)
+#else
+#define TC_MARK(i) \
+  do {             \
+  } while (0)
+#endif
 
 struct TcPlan {
   int C;       // cluster size = W2 / 128
@@ -79,6 +97,26 @@ EVB_DEV void tc_mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t 
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
       "r"(atmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+// whole-warp variants: one elected lane issues (the operands are warp-uniform)
+EVB_DEV void tc_mma_ss_elect(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+EVB_DEV void tc_mma_ts_elect(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+EVB_DEV void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 EVB_DEV void tc_ld8(uint32_t taddr, uint32_t* r) {
@@ -118,9 +156,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   const int r0 = crank * TC_M;       // this CTA's rows of layer 1
   const int row = quad * 32 + lane;  // the layer-1 row this thread owns in the epilogue
 
+#ifdef EVB_TC_PROFILE
+  unsigned long long prof[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+#endif
   for (int i = tid; i < P.bytes / 4; i += TC_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
+  uint64_t* l0bar = mbar + 1;  // layer-0 rounds (up to TC_MAX_ROUNDS)
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -129,6 +172,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   }
   if (tid == 0) {
     mbar_init(mbar, 1);
+    for (int i = 0; i < TC_MAX_ROUNDS; ++i) mbar_init(&l0bar[i], TC_L0_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -236,69 +280,101 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   };
   if (valid && eps_this > 0 && A.max_iters > 0) observe_into_x0(true);
 
-  const uint32_t id32 = tc_idesc(TC_M, 32), id16 = tc_idesc(TC_M, 16);
+  constexpr uint32_t id32 = tc_idesc(TC_M, 32), id16 = tc_idesc(TC_M, 16);
+  TC_MARK(0);  // prologue
   for (int it = 0;; ++it) {
     if (tid < MAXL) mask[tid] = 0u;
     const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
     if (!__syncthreads_or(active)) break;
+    TC_MARK(1);  // loop-top barrier
     float* pout = pout_base + (it & 1) * C * OE1;
 
-    // layer 0, replicated: h1 = relu(W0 x0 + b0) -> B operand (fp16 hi/lo).
-    // A warp stores one 8-lane x 8-row core matrix per unit as 32 packed
-    // words (one per bank): lane -> (lane e&7 = lane&7, row pair = lane>>3).
+    // layer 0, replicated: h1 = relu(W0 x0 + b0) -> B operand (fp16 hi/lo),
+    // pipelined with layer 1: k-step ks (16 rows of h1) is computed by warp
+    // ks % 7 (warps 0-6); after each round of 7 k-steps those warps arrive on
+    // l0bar[round] and warp 7 issues that round's MMAs (one elected lane)
+    // while the next round is computed.  A warp stores each 8-lane x 8-row
+    // core matrix as 32 packed words (one per bank): lane -> (lane e&7 =
+    // lane&7, row pair = lane>>3).
     {
-      const int el = lane & 7, rp = lane >> 3;
-      float xr[2][4];
-#pragma unroll
-      for (int eh = 0; eh < 2; ++eh)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) xr[eh][k] = k < K0 ? x0[k * TC_N + eh * 8 + el] : 0.0f;
+      const int KS = W1 / 16, rounds = (KS + TC_L0_WARPS - 1) / TC_L0_WARPS;
       uint32_t bad = 0u, range = 0u;
-      for (int u = warp; u < W1 / 4; u += TC_THREADS / 32) {
-        const int eh = u & 1, g = u >> 1;
-        const int e = eh * 8 + el, r = g * 8 + rp * 2;
-        __half hh[2], ll[2];
+      if (warp < TC_L0_WARPS) {
+        const int el = lane & 7, rp = lane >> 3;
+        float xr[2][4];
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          float z = 0.0f;
+        for (int eh = 0; eh < 2; ++eh)
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k < K0) z = fmaf(W0[k * W1 + r + v], xr[eh][k], z);
-          z = z + b0[r + v];
-          const float h = z > 0.0f ? z : 0.0f;  // ReLU (NaN -> 0, as cwiseMax)
-          if (h == INFINITY) {
-            bad |= 1u << e;
-          } else if (h > 60000.0f) {
-            range |= 1u << e;  // finite but beyond the fp16 split's range
+          for (int k = 0; k < 4; ++k) xr[eh][k] = k < K0 ? x0[k * TC_N + eh * 8 + el] : 0.0f;
+        for (int rd = 0; rd < rounds; ++rd) {
+          const int ks = rd * TC_L0_WARPS + warp;
+          if (ks < KS) {
+            // this k-step's two row groups: weights and biases of rows r, r+1
+            float2 wv[2][4], bv[2];
+#pragma unroll
+            for (int gi = 0; gi < 2; ++gi) {
+              const int r = (ks * 2 + gi) * 8 + rp * 2;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                wv[gi][k] = k < K0 ? *reinterpret_cast<const float2*>(W0 + k * W1 + r) : make_float2(0.f, 0.f);
+              bv[gi] = *reinterpret_cast<const float2*>(b0 + r);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // (lane half eh, row group gi)
+              const int eh = u & 1, gi = u >> 1;
+              const int e = eh * 8 + el, r = (ks * 2 + gi) * 8 + rp * 2;
+              float z0 = 0.0f, z1 = 0.0f;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if (k < K0) {
+                  z0 = fmaf(wv[gi][k].x, xr[eh][k], z0);
+                  z1 = fmaf(wv[gi][k].y, xr[eh][k], z1);
+                }
+              }
+              z0 = z0 + bv[gi].x;
+              z1 = z1 + bv[gi].y;
+              const float h0 = z0 > 0.0f ? z0 : 0.0f;  // ReLU (NaN -> 0, as cwiseMax)
+              const float h1 = z1 > 0.0f ? z1 : 0.0f;
+              if (fmaxf(h0, h1) > 60000.0f) {
+                if (h0 == INFINITY || h1 == INFINITY) bad |= 1u << e;
+                else range |= 1u << e;  // finite but beyond the fp16 split's range
+              }
+              const __half2 hi = __floats2half2_rn(h0, h1);
+              const float2 hf = __half22float2(hi);
+              const __half2 lo = __floats2half2_rn((h0 - hf.x) * TC_LO_SCALE, (h1 - hf.y) * TC_LO_SCALE);
+              *reinterpret_cast<__half2*>(Bs + umma_off(e, r, 32)) = hi;
+              *reinterpret_cast<__half2*>(Bs + umma_off(e + 16, r, 32)) = lo;
+            }
           }
-          split_f16(h, hh[v], ll[v]);
+          if (tid == 0) TC_MARK(12);  // layer-0 math + stores
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(&l0bar[rd]);
         }
-        *reinterpret_cast<uint32_t*>(Bs + umma_off(e, r, 32)) = pack2(hh[0], hh[1]);
-        *reinterpret_cast<uint32_t*>(Bs + umma_off(e + 16, r, 32)) = pack2(ll[0], ll[1]);
+      } else {
+        // warp 7: layer 1 on tcgen05, round by round
+        const uint32_t aLo = smem_u32(Alo), bS = smem_u32(Bs);
+        constexpr uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (32 / 8) * 128;
+        for (int rd = 0; rd < rounds; ++rd) {
+          mbar_wait_parity_cta(&l0bar[rd], (uint32_t)(it & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const int k1 = min(KS, (rd + 1) * TC_L0_WARPS);
+          for (int k = rd * TC_L0_WARPS; k < k1; ++k) {
+            const uint64_t bd = umma_desc(bS + k * 2 * b_lbo, b_lbo, 128);
+            tc_mma_ts_elect(tmem, tmem + TC_COL_A + k * 8, bd, id32, k > 0);  // D[0:32] += Ahi.[Bhi|Blo]
+            tc_mma_ss_elect(tmem + 16, umma_desc(aLo + k * 2 * a_lbo, a_lbo, 128), bd, id16, 1);  // D1 += Alo.Bhi
+          }
+        }
+        tc_commit_elect(mbar);
       }
       bad = __reduce_or_sync(0xffffffffu, bad);
       range = __reduce_or_sync(0xffffffffu, range);
       if (lane == 0 && bad) atomicOr(&mask[0], bad);
       if (lane == 0 && range) atomicOr(&mask[MAXL - 1], range);
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    // layer 1 on tcgen05, issued by one thread
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t aLo = smem_u32(Alo), b = smem_u32(Bs);
-      constexpr uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (32 / 8) * 128;
-      for (int ks = 0; ks < W1 / 16; ++ks) {
-        const uint64_t bd = umma_desc(b + ks * 2 * b_lbo, b_lbo, 128);
-        tc_mma_ts(tmem, tmem + TC_COL_A + ks * 8, bd, id32, ks > 0);  // D[0:32] += Ahi.[Bhi|Blo]
-        tc_mma_ss(tmem + 16, umma_desc(aLo + ks * 2 * a_lbo, a_lbo, 128), bd, id16, 1);  // D1 += Alo.Bhi
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(mbar))
-                   : "memory");
-    }
+    TC_MARK(2);  // layer 0 (+ waiting for the MMA issue)
     mbar_wait_parity(mbar, (uint32_t)(it & 1));
+    TC_MARK(3);  // MMA completion wait
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // epilogue: row `row`, lanes 8*half .. 8*half+7; output layer fused
     {
@@ -350,6 +426,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    TC_MARK(4);  // epilogue
     // this CTA's partial outputs (fixed quadrant order) -> every CTA of the cluster
     for (int oe = tid; oe < OE1; oe += TC_THREADS) {
       float v;
@@ -376,6 +453,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
       __syncthreads();
     }
 
+    TC_MARK(5);  // cluster exchange
     // head + env step (proj/src/rollout.cpp:57-90, :131-153)
     if (active) {
       double z[TC_MAXO];
@@ -410,8 +488,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
         }
         double reward = 0.0;
         bool term = false, trunc = false;
+        TC_MARK(10);  // head (output sum + tanh)
         const uint32_t f =
             env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr);
+        TC_MARK(11);  // env_step
         if (f) {
           myfault = f;
         } else {
@@ -434,7 +514,19 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
       const bool next = myfault == 0 && eps_done < eps_this && it + 1 < A.max_iters;
       observe_into_x0(next);
     }
+    TC_MARK(6);  // env phase
   }
+#ifdef EVB_TC_PROFILE
+  if (tid == 0) {
+    for (int i = 0; i < 7; ++i) atomicAdd(&g_tc_prof[i], prof[i]);
+    atomicAdd(&g_tc_prof[7], prof[7]);
+    atomicAdd(&g_tc_prof[9], prof[9]);
+    atomicAdd(&g_tc_prof[10], prof[10]);
+    atomicAdd(&g_tc_prof[11], prof[11]);
+    atomicAdd(&g_tc_prof[12], prof[12]);
+    atomicAdd(&g_tc_prof[8], 1ull);
+  }
+#endif
 
   if (valid && crank == 0) {
     const long long ln = (long long)agent_local * A.e + j;
@@ -487,7 +579,7 @@ bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.off_mask = off;
   off = al(off + MAXL * 4, 16);
   p.off_bar = off;
-  off = al(off + 16, 16);
+  off = al(off + 8 * (1 + TC_MAX_ROUNDS), 16);
   p.off_tslot = off;
   off = al(off + 16, 16);
   p.bytes = off;
@@ -533,5 +625,13 @@ cudaError_t launch_rollout_tc(const RolloutArgs& a, const TcPlanOut& po, cudaStr
   }
   return cudaErrorInvalidValue;
 }
+
+#ifdef EVB_TC_PROFILE
+extern "C" int evorl_debug_tc_profile(unsigned long long* out16) {
+  if (cudaMemcpyFromSymbol(out16, g_tc_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 6;
+  static const unsigned long long zero[16] = {};
+  return cudaMemcpyToSymbol(g_tc_prof, zero, sizeof zero) == cudaSuccess ? 0 : 6;
+}
+#endif
 
 }  // namespace evorl_b200
