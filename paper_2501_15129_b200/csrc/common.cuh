@@ -131,6 +131,10 @@ template <>
 EVB_DEV void st_cluster<float>(uint32_t addr, float v) {
   st_cluster_f32(addr, v);
 }
+template <>
+EVB_DEV void st_cluster<uint32_t>(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 
 // ---------------------------------------------------------------- mbarrier
 EVB_DEV void mbar_init(uint64_t* bar, uint32_t count) {

@@ -29,9 +29,29 @@ struct LaneEnv {
 
 #define EVB_PI 3.141592653589793
 
+// fmod(x, y) for finite y > 0, bit-identical to the library fmod (which is
+// exact): for |x| < 2^40 y the truncated quotient estimate from the rounded
+// reciprocal is off by at most one, the remainder x - n*y of the right n is
+// representable so one fma yields it exactly, and a wrong n shows up as a
+// remainder outside [0, y) (rounding is monotone) and is corrected once.
+EVB_DEV double fmod_exact(double x, double y, double inv_y) {
+  const double ax = fabs(x);
+  if (!(ax < 1099511627776.0 * y)) return fmod(x, y);  // huge or non-finite: library path
+  double n = trunc(ax * inv_y);
+  double r = fma(-n, y, ax);
+  if (r < 0.0) {
+    n -= 1.0;
+    r = fma(-n, y, ax);
+  } else if (r >= y) {
+    n += 1.0;
+    r = fma(-n, y, ax);
+  }
+  return copysign(r, x);
+}
+
 // proj/src/env.cpp:28-32: fmod is exact; the adds are single rounded ops.
 EVB_DEV double wrap_angle(double th) {
-  double w = fmod(dadd(th, EVB_PI), 6.283185307179586);
+  double w = fmod_exact(dadd(th, EVB_PI), 6.283185307179586, 1.0 / 6.283185307179586);
   if (w <= 0.0) w = dadd(w, 6.283185307179586);
   return dsub(w, EVB_PI);
 }

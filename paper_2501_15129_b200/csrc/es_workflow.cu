@@ -175,6 +175,10 @@ struct evorl_es {
   bool warp_path = false;  // small policies: warp-per-lane rollout (rollout_warp.cu)
   WarpPlanOut wplan{};
   double* d_cand = nullptr;  // materialised candidates for the warp path
+  // fp32 policy paths (tc / f32 teams): the generation's candidates rounded to
+  // fp32, materialised once by a fully parallel ask instead of being
+  // regenerated in every CTA's prologue (null: regenerate, e.g. over the cap)
+  float* d_cand_f32 = nullptr;
   cudaStream_t stream = nullptr;
   // WorkflowState (proj/include/evorl/workflow.hpp:31-36)
   DKey rng{};
@@ -267,7 +271,8 @@ static void free_all(evorl_es* s) {
   void* ptrs[] = {s->d_mean, s->d_m, s->d_v, s->d_var, s->d_t, s->d_norm, s->d_normp, s->d_fitness,
                   s->d_ep_returns, s->d_lane_stats, s->d_agent_stats, s->d_lane_steps, s->d_rank,
                   s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
-                  s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand};
+                  s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand,
+                  s->d_cand_f32};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
@@ -368,6 +373,10 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   A(dalloc(&s->d_metrics, 4));
   A(dalloc(&s->d_sel, 1));
   if (s->warp_path) A(dalloc(&s->d_cand, (size_t)n * d));
+  constexpr double kCandF32Cap = 8.0 * (1ull << 30);  // bytes
+  if (!s->warp_path && cfg->precision != EVORL_PREC_F64 && cfg->algo != EVORL_ALGO_CMAES &&
+      (double)n * (double)d * sizeof(float) <= kCandF32Cap)
+    A(dalloc(&s->d_cand_f32, (size_t)n * d));
   if (cfg->algo == EVORL_ALGO_CMAES) {
     // CmaState::init (proj/src/ec.cpp:191-224)
     if (d > cfg->cmaes_max_dim) {
@@ -649,6 +658,12 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
     CK(cudaEventRecord(s->ev_r0, s->stream));
     CK(launch_rollout_warp(a, s->wplan, s->cfg.precision, s->stream));
   } else {
+    if (s->d_cand_f32) {
+      CK(run_materialize_f32(a.par, s->d, s->a0, s->a1, s->d_cand_f32, s->stream));
+      count_launch();
+      a.par.src = SRC_EXPLICIT_F32;
+      a.par.params_f32 = s->d_cand_f32;
+    }
     CK(cudaEventRecord(s->ev_r0, s->stream));
     CK(launch_rollout(a, s->cfg.precision, s->stream));
     count_launch();

@@ -23,6 +23,7 @@
 //    operation order (env.cuh).  The policy GEMM runs in T = double (parity
 //    mode) or float (throughput mode).
 #include <algorithm>
+#include <climits>
 #include <type_traits>
 #include <cstdio>
 
@@ -54,6 +55,72 @@ __global__ void k_materialize(const ParamDesc P, long long d, int a0, int a1, do
   const int al = (int)(idx / d);
   out[idx] = param_value(P, d, al, a0 + al, idx % d);
 }
+__global__ void k_materialize_f32(const ParamDesc P, long long d, int a0, int a1, float* out) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long n = (long long)(a1 - a0) * d;
+  if (idx >= n) return;
+  const int al = (int)(idx / d);
+  out[idx] = __double2float_rn(param_value(P, d, al, a0 + al, idx % d));
+}
+
+// OpenES (proj/src/ec.cpp:87-94): noise entry t = row * d + p of the sampled
+// rows [r0, r1) is normal #t of the ask stream, i.e. the cos (t even) or sin
+// (t odd) half of Box-Muller block t >> 1; thread b computes block b once and
+// writes both entries to every agent using them (row, and row + base when
+// mirrored, negated) -- the same value param_value regenerates.
+__global__ void k_materialize_openes_f32(const ParamDesc P, long long d, int a0, int a1, long long t0,
+                                         long long t1, float* out) {
+  const long long b = (t0 >> 1) + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (2 * b >= t1) return;
+  double c, sn;
+  normal_pair(P.ask_key, (uint64_t)b, c, sn);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const long long t = 2 * b + h;
+    if (t < t0 || t >= t1) continue;
+    const long long row = t / d, p = t - row * d;
+    const double eps = h ? sn : c;
+    const int ag[2] = {(int)row, P.mirrored ? (int)row + P.base : -1};
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int a = ag[m];
+      if (a < a0 || a >= a1) continue;
+      const double v = dadd(dmul(P.sigma, m ? -eps : eps), P.mean[p]);
+      out[(long long)(a - a0) * d + p] = __double2float_rn(v);
+    }
+  }
+}
+
+cudaError_t run_materialize_f32(const ParamDesc& par, long long d, int a0, int a1, float* out,
+                                cudaStream_t stream) {
+  const long long n = (long long)(a1 - a0) * d;
+  if (n <= 0) return cudaSuccess;
+  if (par.src == SRC_OPENES) {
+    // sampled rows used by agents [a0, a1)
+    long long r0 = a0, r1 = a1;
+    if (par.mirrored) {  // agent a < base uses row a, a >= base uses row a - base
+      const long long base = par.base;
+      r0 = LLONG_MAX;
+      r1 = LLONG_MIN;
+      if (a0 < base) {
+        r0 = std::min<long long>(r0, a0);
+        r1 = std::max<long long>(r1, std::min<long long>(a1, base));
+      }
+      if (a1 > base) {
+        r0 = std::min<long long>(r0, std::max<long long>(a0, base) - base);
+        r1 = std::max<long long>(r1, a1 - base);
+      }
+    }
+    const long long t0 = r0 * d, t1 = r1 * d;
+    const long long blocks = ((t1 + 1) >> 1) - (t0 >> 1);
+    k_materialize_openes_f32<<<(unsigned)((blocks + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1,
+                                                                                    out);
+    return cudaGetLastError();
+  }
+  k_materialize_f32<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, out);
+  return cudaGetLastError();
+}
+
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
                             cudaStream_t stream) {
   const long long n = (long long)(a1 - a0) * d;

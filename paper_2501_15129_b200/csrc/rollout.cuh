@@ -28,10 +28,11 @@ struct NetDesc {
 // Where candidate i's parameters come from.  Only SRC_EXPLICIT reads a stored
 // n x d matrix; the others regenerate the perturbation from the ask key
 // (proj/src/ec.cpp:71-97 OpenES/VES, :113-125 ARS, :306-313 CEM).
-enum : int { SRC_EXPLICIT = 0, SRC_OPENES = 1, SRC_ARS = 2, SRC_CEM = 3 };
+enum : int { SRC_EXPLICIT = 0, SRC_OPENES = 1, SRC_ARS = 2, SRC_CEM = 3, SRC_EXPLICIT_F32 = 4 };
 struct ParamDesc {
   int src;
   const double* params;  // SRC_EXPLICIT: n_agents x d, row-major
+  const float* params_f32;  // SRC_EXPLICIT_F32: n_agents x d, the fp32 policy paths' candidates
   const double* mean;    // d
   const double* var;     // CEM diagonal variance
   double sigma;
@@ -73,6 +74,8 @@ EVB_DEV double param_value(const ParamDesc& P, long long d, int agent_local, int
       const double z = normal_at(P.ask_key, (uint64_t)((long long)agent * d + p));
       return dadd(dmul(z, sqrt(P.var[p])), P.mean[p]);
     }
+    case SRC_EXPLICIT_F32:
+      return (double)P.params_f32[(long long)agent_local * d + p];
     default:
       return P.params[(long long)agent_local * d + p];
   }
@@ -137,6 +140,12 @@ cudaError_t launch_rollout_warp(const RolloutArgs& a, const WarpPlanOut& plan, i
 // Materialise candidates [a0, a1) (row-major, d each) from a ParamDesc.
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
                             cudaStream_t stream);
+
+// Materialise candidates [a0, a1) as fp32 (the value the fp32 policy paths
+// round each fp64 candidate parameter to).  OpenES: one Box-Muller pair per
+// thread, shared by the mirrored agents.
+cudaError_t run_materialize_f32(const ParamDesc& par, long long d, int a0, int a1, float* out,
+                                cudaStream_t stream);
 
 // Tensor-core rollout (rollout_tc.cu, precision EVORL_PREC_TC): obs -> W1 -> W2 -> O
 // policies with W2 a multiple of 128; the W2 x W1 layer runs on tcgen05.

@@ -38,13 +38,13 @@ constexpr int TC_THREADS = 256;
 constexpr int TC_M = 128;  // rows per CTA (UMMA M)
 constexpr int TC_N = 16;   // lanes per team
 constexpr int TC_TMEM_COLS = 256;
-constexpr int TC_COL_A = 32;  // A_hi starts at TMEM column 32 (D0 = 0..15, D1 = 16..31)
+constexpr int TC_COL_A = 32;   // C == 1: A_hi at TMEM column 32 (D0 = 0..15, D1 = 16..31)
+constexpr int TC_COL_A2 = 64;  // PAIR: A_hi at column 64 (D = 0..31 hi x [hi|lo], 32..63 lo x [hi|lo])
 constexpr float TC_LO_SCALE = 2048.0f;
 constexpr int TC_RANGE_ROW = 8;  // bad-layer row value: operand out of the split's range
 constexpr int TC_OK_ROW = 15;    // bad-layer row value: no fault
 constexpr int TC_MAXO = 8;
-constexpr int TC_L0_WARPS = 7;    // warps computing layer 0; warp 7 issues the MMAs
-constexpr int TC_MAX_ROUNDS = 4;  // layer-0 / MMA pipeline rounds (7 k-steps each): W1 <= 448
+constexpr int TC_MAX_ROUNDS = 4;  // layer-0 / MMA pipeline rounds of 8 k-steps: W1 <= 512
 
 #ifdef EVB_TC_PROFILE
 // Phase cycle counters (profiling build only, libevorl_b200_prof.so): thread 0
@@ -112,6 +112,27 @@ EVB_DEV void tc_mma_ts_elect(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uin
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
       "r"(atmem), "l"(bdesc), "r"(idesc), "r"(acc));
 }
+EVB_DEV void tc_mma2_ss_elect(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+EVB_DEV void tc_mma2_ts_elect(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// pair commit: arrives on the same-offset mbarrier of both CTAs of the pair
+EVB_DEV void tc_commit2_elect(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
 EVB_DEV void tc_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
@@ -154,6 +175,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   const int agent = A.agent_offset + agent_local;
   const int W1 = P.W1, W2 = P.W2, O = N.dims[3], K0 = N.dims[0];
   const int r0 = crank * TC_M;       // this CTA's rows of layer 1
+  // C >= 2: CTA pairs (2p, 2p+1) run cta_group::2 MMAs (M = 256): each CTA
+  // holds its 128 weight rows and the B columns of its 8 lanes (N-split), the
+  // even CTA issues for both and the commit arrives on both
+  constexpr bool PAIR = C >= 2;
+  const int pv = PAIR ? (crank & 1) : 0;  // 1: the pair's odd (non-issuing) CTA
   const int row = quad * 32 + lane;  // the layer-1 row this thread owns in the epilogue
 
 #ifdef EVB_TC_PROFILE
@@ -163,16 +189,24 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   for (int i = tid; i < P.bytes / 4; i += TC_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
-  uint64_t* l0bar = mbar + 1;  // layer-0 rounds (up to TC_MAX_ROUNDS)
+  uint64_t* l0bar = mbar + 1;  // [TC_MAX_ROUNDS]: layer-0 rounds stored
   __syncthreads();
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "n"(TC_TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {  // both CTAs of the pair: same columns in each TMEM
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                   "n"(TC_TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                   "n"(TC_TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (tid == 0) {
     mbar_init(mbar, 1);
-    for (int i = 0; i < TC_MAX_ROUNDS; ++i) mbar_init(&l0bar[i], TC_L0_WARPS);
+    // layer-0 round rd stored: every warp of this CTA (and, on a pair's even
+    // CTA, of its odd peer) arrives once per step
+    for (int i = 0; i < TC_MAX_ROUNDS; ++i) mbar_init(&l0bar[i], (PAIR ? 2 : 1) * (TC_THREADS / 32));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -183,7 +217,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   float* W0 = reinterpret_cast<float*>(smem + P.off_W0);  // [k][W1]
   float* b0 = reinterpret_cast<float*>(smem + P.off_b0);  // W1
   unsigned char* Alo = smem + P.off_Alo;
-  unsigned char* Bs = smem + P.off_B;  // 32 x W1: rows 0..15 = B_hi, 16..31 = B_lo
+  // B (K-major, K = W1): C == 1: 32 rows = B_hi of lanes 0..15, then B_lo;
+  // PAIR: 16 rows = B_hi of this CTA's lanes 8pv..8pv+7, then their B_lo
+  unsigned char* Bs = smem + P.off_B;
   // ---- prologue: this agent's parameters (regenerated or explicit)
   for (int i = tid; i < K0 * W1; i += TC_THREADS) {
     const int k = i / W1, r = i % W1;
@@ -208,7 +244,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
       }
       packed[q] = pack2(h[0], h[1]);
     }
-    tc_st8(tmem + ((uint32_t)(quad * 32) << 16) + TC_COL_A + c * 8, packed);
+    tc_st8(tmem + ((uint32_t)(quad * 32) << 16) + (PAIR ? TC_COL_A2 : TC_COL_A) + c * 8, packed);
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   const float b1r = (float)param_value(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row);
@@ -280,7 +316,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   };
   if (valid && eps_this > 0 && A.max_iters > 0) observe_into_x0(true);
 
-  constexpr uint32_t id32 = tc_idesc(TC_M, 32), id16 = tc_idesc(TC_M, 16);
+  constexpr uint32_t id32 = tc_idesc(TC_M, 32), id16 = tc_idesc(TC_M, 16), id2 = tc_idesc(2 * TC_M, 32);
   TC_MARK(0);  // prologue
   for (int it = 0;; ++it) {
     if (tid < MAXL) mask[tid] = 0u;
@@ -289,83 +325,107 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     TC_MARK(1);  // loop-top barrier
     float* pout = pout_base + (it & 1) * C * OE1;
 
-    // layer 0, replicated: h1 = relu(W0 x0 + b0) -> B operand (fp16 hi/lo),
-    // pipelined with layer 1: k-step ks (16 rows of h1) is computed by warp
-    // ks % 7 (warps 0-6); after each round of 7 k-steps those warps arrive on
-    // l0bar[round] and warp 7 issues that round's MMAs (one elected lane)
-    // while the next round is computed.  A warp stores each 8-lane x 8-row
-    // core matrix as 32 packed words (one per bank): lane -> (lane e&7 =
-    // lane&7, row pair = lane>>3).
+    // layer 0: h1 = relu(W0 x0 + b0) -> B operand (fp16 hi/lo).  C == 1: all
+    // 16 lanes; PAIR: the 8 lanes of this CTA's B columns.  k-step ks (16 rows
+    // of h1) goes to warp ks % 8; a warp stores each 8-lane x 8-row core
+    // matrix as 32 packed words (one per bank): lane -> (lane j = lane&7,
+    // row pair = lane>>3).  Warp 7 (of the pair's even CTA) issues layer 1
+    // once every warp (of both CTAs) has arrived.
     {
-      const int KS = W1 / 16, rounds = (KS + TC_L0_WARPS - 1) / TC_L0_WARPS;
+      constexpr int NB = PAIR ? 16 : 32;      // B rows (N) held by this CTA
+      constexpr int EH = PAIR ? 1 : 2;        // 8-lane halves computed here
+      const int KS = W1 / 16;
       uint32_t bad = 0u, range = 0u;
-      if (warp < TC_L0_WARPS) {
-        const int el = lane & 7, rp = lane >> 3;
-        float xr[2][4];
+      const int el = lane & 7, rp = lane >> 3;
+      float xr[EH][4];
 #pragma unroll
-        for (int eh = 0; eh < 2; ++eh)
+      for (int eh = 0; eh < EH; ++eh)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) xr[eh][k] = k < K0 ? x0[k * TC_N + eh * 8 + el] : 0.0f;
-        for (int rd = 0; rd < rounds; ++rd) {
-          const int ks = rd * TC_L0_WARPS + warp;
-          if (ks < KS) {
-            // this k-step's two row groups: weights and biases of rows r, r+1
-            float2 wv[2][4], bv[2];
+        for (int k = 0; k < 4; ++k) xr[eh][k] = k < K0 ? x0[k * TC_N + (eh + pv) * 8 + el] : 0.0f;
+      // one round: (pipelining layer 0 against the MMAs in rounds of 8 k-steps
+      // measured slower -- the pair's tensor pipe is shared with the SM's
+      // other team, so the MMAs do not start earlier in practice)
+      const int rounds = 1;
+      for (int rd = 0; rd < rounds; ++rd) {
+        for (int ks = warp; ks < KS; ks += TC_THREADS / 32) {
+          // this k-step's two row groups: weights and biases of rows r, r+1
+          float2 wv[2][4], bv[2];
 #pragma unroll
-            for (int gi = 0; gi < 2; ++gi) {
-              const int r = (ks * 2 + gi) * 8 + rp * 2;
+          for (int gi = 0; gi < 2; ++gi) {
+            const int r = (ks * 2 + gi) * 8 + rp * 2;
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                wv[gi][k] = k < K0 ? *reinterpret_cast<const float2*>(W0 + k * W1 + r) : make_float2(0.f, 0.f);
-              bv[gi] = *reinterpret_cast<const float2*>(b0 + r);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {  // (lane half eh, row group gi)
-              const int eh = u & 1, gi = u >> 1;
-              const int e = eh * 8 + el, r = (ks * 2 + gi) * 8 + rp * 2;
-              float z0 = 0.0f, z1 = 0.0f;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                if (k < K0) {
-                  z0 = fmaf(wv[gi][k].x, xr[eh][k], z0);
-                  z1 = fmaf(wv[gi][k].y, xr[eh][k], z1);
-                }
-              }
-              z0 = z0 + bv[gi].x;
-              z1 = z1 + bv[gi].y;
-              const float h0 = z0 > 0.0f ? z0 : 0.0f;  // ReLU (NaN -> 0, as cwiseMax)
-              const float h1 = z1 > 0.0f ? z1 : 0.0f;
-              if (fmaxf(h0, h1) > 60000.0f) {
-                if (h0 == INFINITY || h1 == INFINITY) bad |= 1u << e;
-                else range |= 1u << e;  // finite but beyond the fp16 split's range
-              }
-              const __half2 hi = __floats2half2_rn(h0, h1);
-              const float2 hf = __half22float2(hi);
-              const __half2 lo = __floats2half2_rn((h0 - hf.x) * TC_LO_SCALE, (h1 - hf.y) * TC_LO_SCALE);
-              *reinterpret_cast<__half2*>(Bs + umma_off(e, r, 32)) = hi;
-              *reinterpret_cast<__half2*>(Bs + umma_off(e + 16, r, 32)) = lo;
-            }
+            for (int k = 0; k < 4; ++k)
+              wv[gi][k] = k < K0 ? *reinterpret_cast<const float2*>(W0 + k * W1 + r) : make_float2(0.f, 0.f);
+            bv[gi] = *reinterpret_cast<const float2*>(b0 + r);
           }
-          if (tid == 0) TC_MARK(12);  // layer-0 math + stores
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive_local(&l0bar[rd]);
+#pragma unroll
+          for (int u = 0; u < 2 * EH; ++u) {  // (lane half eh, row group gi)
+            const int eh = u % EH, gi = u / EH;
+            const int e = (eh + pv) * 8 + el, r = (ks * 2 + gi) * 8 + rp * 2;
+            float z0 = 0.0f, z1 = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (k < K0) {
+                z0 = fmaf(wv[gi][k].x, xr[eh][k], z0);
+                z1 = fmaf(wv[gi][k].y, xr[eh][k], z1);
+              }
+            }
+            z0 = z0 + bv[gi].x;
+            z1 = z1 + bv[gi].y;
+            const float h0 = z0 > 0.0f ? z0 : 0.0f;  // ReLU (NaN -> 0, as cwiseMax)
+            const float h1 = z1 > 0.0f ? z1 : 0.0f;
+            if (fmaxf(h0, h1) > 60000.0f) {
+              if (h0 == INFINITY || h1 == INFINITY) bad |= 1u << e;
+              else range |= 1u << e;  // finite but beyond the fp16 split's range
+            }
+            const __half2 hi = __floats2half2_rn(h0, h1);
+            const float2 hf = __half22float2(hi);
+            const __half2 lo = __floats2half2_rn((h0 - hf.x) * TC_LO_SCALE, (h1 - hf.y) * TC_LO_SCALE);
+            const int nh = PAIR ? el : eh * 8 + el;  // B row of (lane e, hi); lo rows follow NB/2 later
+            *reinterpret_cast<__half2*>(Bs + umma_off(nh, r, NB)) = hi;
+            *reinterpret_cast<__half2*>(Bs + umma_off(nh + NB / 2, r, NB)) = lo;
+          }
         }
-      } else {
-        // warp 7: layer 1 on tcgen05, round by round
-        const uint32_t aLo = smem_u32(Alo), bS = smem_u32(Bs);
-        constexpr uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (32 / 8) * 128;
-        for (int rd = 0; rd < rounds; ++rd) {
-          mbar_wait_parity_cta(&l0bar[rd], (uint32_t)(it & 1));
+        if (tid == 0) TC_MARK(12);  // layer-0 math + stores
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR && pv) {
+            mbar_arrive_remote(&l0bar[rd], (uint32_t)(crank - 1));
+          } else {
+            mbar_arrive_local(&l0bar[rd]);
+          }
+        }
+        if (warp == TC_THREADS / 32 - 1 && !(PAIR && pv)) {  // layer 1 on tcgen05 for this round
+          if constexpr (PAIR) {
+            mbar_wait_parity(&l0bar[rd], (uint32_t)(it & 1));
+          } else {
+            mbar_wait_parity_cta(&l0bar[rd], (uint32_t)(it & 1));
+          }
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const int k1 = min(KS, (rd + 1) * TC_L0_WARPS);
-          for (int k = rd * TC_L0_WARPS; k < k1; ++k) {
+          const uint32_t aLo = smem_u32(Alo), bS = smem_u32(Bs);
+          constexpr uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (NB / 8) * 128;
+          for (int k = 0; k < KS; ++k) {
             const uint64_t bd = umma_desc(bS + k * 2 * b_lbo, b_lbo, 128);
-            tc_mma_ts_elect(tmem, tmem + TC_COL_A + k * 8, bd, id32, k > 0);  // D[0:32] += Ahi.[Bhi|Blo]
-            tc_mma_ss_elect(tmem + 16, umma_desc(aLo + k * 2 * a_lbo, a_lbo, 128), bd, id16, 1);  // D1 += Alo.Bhi
+            const uint64_t ad = umma_desc(aLo + k * 2 * a_lbo, a_lbo, 128);
+            if constexpr (PAIR) {
+              // D[0:32] += Ahi.[Bhi|Blo] (per CTA v: cols 16v..16v+7 hi.hi, +8 hi.lo);
+              // D[32:64] += Alo.[Bhi|Blo] (cols 32+16v.. lo.hi; the lo.lo half is unused)
+              tc_mma2_ts_elect(tmem, tmem + TC_COL_A2 + k * 8, bd, id2, k > 0);
+              tc_mma2_ss_elect(tmem + 32, ad, bd, id2, k > 0);
+            } else {
+              tc_mma_ts_elect(tmem, tmem + TC_COL_A + k * 8, bd, id32, k > 0);  // D[0:32] += Ahi.[Bhi|Blo]
+              tc_mma_ss_elect(tmem + 16, ad, bd, id16, 1);                      // D1 += Alo.Bhi
+            }
+          }
+          if (rd == rounds - 1) {
+            if constexpr (PAIR) {
+              tc_commit2_elect(mbar, (uint16_t)(3u << crank));  // crank is the pair's even rank
+            } else {
+              tc_commit_elect(mbar);
+            }
           }
         }
-        tc_commit_elect(mbar);
       }
       bad = __reduce_or_sync(0xffffffffu, bad);
       range = __reduce_or_sync(0xffffffffu, range);
@@ -378,16 +438,23 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // epilogue: row `row`, lanes 8*half .. 8*half+7; output layer fused
     {
-      uint32_t d0[8], d1[8];
-      const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + half * 8;
-      tc_ld8(ta, d0);
-      tc_ld8(ta + 16, d1);
+      uint32_t d0[8], d1[8], d2[8];
+      const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16);
+      if constexpr (PAIR) {  // lane e = 8*half + q: hi.hi col 16h+q, hi.lo 16h+8+q, lo.hi 32+16h+q
+        tc_ld8(tl + half * 16, d0);
+        tc_ld8(tl + half * 16 + 8, d1);
+        tc_ld8(tl + 32 + half * 16, d2);
+      } else {
+        tc_ld8(tl + half * 8, d0);
+        tc_ld8(tl + 16 + half * 8, d1);
+      }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       float h[8];
       uint32_t bad = 0u;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float z = (__uint_as_float(d0[q]) + __uint_as_float(d1[q]) * (1.0f / TC_LO_SCALE)) + b1r;
+        const float cross = PAIR ? __uint_as_float(d1[q]) + __uint_as_float(d2[q]) : __uint_as_float(d1[q]);
+        const float z = (__uint_as_float(d0[q]) + cross * (1.0f / TC_LO_SCALE)) + b1r;
         h[q] = z > 0.0f ? z : 0.0f;
         if (h[q] == INFINITY) bad |= 1u << (half * 8 + q);
       }
@@ -545,7 +612,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TMEM_COLS));
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TMEM_COLS));
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TMEM_COLS));
+    }
   }
   if constexpr (C > 1) cluster_sync_all();
 }
@@ -555,7 +626,7 @@ static int al(int x, int a) { return (x + a - 1) / a * a; }
 bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   if (net.nlayers != 3 || obs_dim > 4 || e < 5) return false;  // 16-lane teams, obs -> W1 -> W2 -> O
   const int W1 = net.dims[1], W2 = net.dims[2], O = net.dims[3];
-  if (W1 % 16 || W1 > 2 * (TC_TMEM_COLS - TC_COL_A) || W2 % TC_M || W2 / TC_M > 8 || O > TC_MAXO)
+  if (W1 % 16 || W1 > 2 * (TC_TMEM_COLS - (W2 >= 2 * TC_M ? TC_COL_A2 : TC_COL_A)) || W2 % TC_M || W2 / TC_M > 8 || O > TC_MAXO)
     return false;
   TcPlan p{};
   p.C = W2 / TC_M;
@@ -565,7 +636,7 @@ bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.off_Alo = off;
   off = al(off + TC_M * W1 * 2, 1024);
   p.off_B = off;
-  off = al(off + 32 * W1 * 2, 1024);
+  off = al(off + (p.C >= 2 ? 16 : 32) * W1 * 2, 1024);
   p.off_W0 = off;
   off = al(off + 4 * W1 * 4, 16);
   p.off_b0 = off;

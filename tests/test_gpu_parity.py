@@ -144,6 +144,30 @@ def test_env_step_kats_and_random(oracle, evb):
                 assert abs(phys[i, q] - nx.phys[q]) <= 1e-14 * max(1, abs(nx.phys[q]))
 
 
+def test_pendulum_wrap_angle_bitexact(evb):
+    """wrap_angle (proj/src/env.cpp:28-32) uses a fast exact fmod on the
+    device; with thdot = u = 0 the reward is -(w*w), so comparing it with C
+    fmod (numpy) pins w bit for bit, over wide angles and near-multiples of
+    2*pi where the quotient estimate is off by one."""
+    two_pi = 6.283185307179586
+    rng = np.random.default_rng(3)
+    th = list(rng.uniform(-200, 200, 3000)) + list(rng.uniform(-1e7, 1e7, 200))
+    for k in range(-60, 61):
+        x = k * two_pi - np.pi
+        th += [x, np.nextafter(x, np.inf), np.nextafter(x, -np.inf), -x, k * two_pi]
+    th += [0.0, -0.0, np.pi, -np.pi, 1e13, -1e13, 5e-324, 1e300]
+    th = np.array(th, dtype=np.float64)
+    n = len(th)
+    ph = np.zeros((n, 4))
+    ph[:, 0] = th
+    _, _, r, _, _, f = evb.env_step_batch("pendulum", ph, np.zeros(n, np.int32), np.zeros(n))
+    assert not np.any(f)
+    w = np.fmod(th + np.pi, two_pi)
+    w = np.where(w <= 0.0, w + two_pi, w) - np.pi
+    want = -((w * w + 0.0) + 0.0)
+    assert np.array_equal(r, want), np.flatnonzero(r != want)[:10]
+
+
 # -------------------------------------------------------- P2/P3 ask + tell
 def test_openes_ask_matches(oracle, evb):
     # proj/tests/test_ec.cpp:46-67 layout: block mirror, sigma*eps + mean

@@ -143,3 +143,27 @@ def test_tc_operand_range_is_reported(oracle, evb):
 def ospec_bias0(ospec):
     # flat layout (proj/src/net.cpp:26-48): W0 (obs x W1, column-major) then b0
     return ospec.input_dim * 128
+
+
+@pytest.mark.parametrize("precision", ["tc", "f32"])
+@pytest.mark.parametrize("algo", ["openes", "ars"])
+def test_sharded_materialised_ask_matches_unsharded(evb, precision, algo):
+    """The fp32 paths materialise the shard's candidates [a0, a1) once per
+    generation (run_materialize_f32; for mirrored OpenES one Box-Muller pair
+    feeds both mirrored agents).  Three shard handles (shard 1 straddles the
+    mirror boundary pop/2) must reproduce the unsharded fitness bit for bit."""
+    kw = dict(algo=algo, env="pendulum", fixed_horizon=True, pop=64, fitness_episodes=16,
+              hidden=(128, 128), max_episode_steps=50, precision=precision)
+    key = (7, 8)
+    full = evb.EsWorkflow(evb.EsConfig(**kw)).init(key)
+    full.step()
+    want = full.fitness()
+    got = np.full(64, np.nan)
+    for r in range(3):
+        h = evb.EsWorkflow(evb.EsConfig(**kw))
+        h.set_shard(r, 3)
+        h.init(key)
+        h.phase_rollout()
+        a0, a1, _, _ = h.shard_ranges()
+        got[a0:a1] = h.fitness()[a0:a1]
+    assert np.array_equal(got, want)
