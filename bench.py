@@ -193,6 +193,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", dest="variants", action="store_false",
+                    help="skip the tensor-core (precision tc) measurement beside the headline")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     if args.impl == "reference":
@@ -216,16 +218,6 @@ def main():
     L = _lib.load()
 
     kw = {k: v for k, v in cfgd.items() if k != "desc"}
-    cfg = evb.EsConfig(**kw, precision=args.precision, device=local)
-    if world > 1:
-        runner = CudaShardedEs(cfg, rank, world)
-        runner.init((0x9E3779B97F4A7C15, 0))
-        step = runner.step
-        es = runner.es
-    else:
-        es = evb.EsWorkflow(cfg).init((0x9E3779B97F4A7C15, 0))
-        step = es.step
-
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
@@ -233,13 +225,24 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step()
-    barrier()
-
-    launches0 = L.evorl_kernel_launches()
-    times, roll = [], []
-    with ClockSampler(local) as clk:
+    def timed_generations(precision, clk=None):
+        """W warm-up + K timed generations at `precision`; returns the handle,
+        max-over-ranks total ms, per-step rollout ms and kernel launches."""
+        cfg = evb.EsConfig(**kw, precision=precision, device=local)
+        if world > 1:
+            runner = CudaShardedEs(cfg, rank, world)
+            runner.init((0x9E3779B97F4A7C15, 0))
+            step, es = runner.step, runner.es
+        else:
+            es = evb.EsWorkflow(cfg).init((0x9E3779B97F4A7C15, 0))
+            step = es.step
+        for _ in range(args.warmup):
+            step()
+        barrier()
+        launches0 = L.evorl_kernel_launches()
+        times, roll = [], []
+        if clk is not None:
+            clk.__enter__()
         for _ in range(args.steps):
             flush.zero_()                      # L2 flush outside the timed events
             barrier()
@@ -251,12 +254,16 @@ def main():
             barrier()
             times.append(e0.elapsed_time(e1))
             roll.append(es.last_timings()[0])   # rollout kernel, events on the library stream
-    launches = L.evorl_kernel_launches() - launches0
-    local_ms = sum(times)
-    tot = torch.tensor([local_ms], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    max_ms = float(tot.item())
+        if clk is not None:
+            clk.__exit__(None, None, None)
+        launches = L.evorl_kernel_launches() - launches0
+        tot = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        return cfg, es, float(tot.item()), roll, launches
+
+    clk = ClockSampler(local)
+    cfg, es, max_ms, roll, launches = timed_generations(args.precision, clk)
 
     pop, e, H = cfg.pop, cfg.fitness_episodes, cfg.max_episode_steps
     env_steps_per_gen = pop * e * H
@@ -329,6 +336,31 @@ def main():
                 "rollout_ms_per_launch": roll_ms, "rollout_share_of_step":
                     (roll_ms / ms_per_step) if roll_ms else None}
 
+    # ---- the tensor-core policy path (tcgen05, precision "tc") on the same
+    # workload, reported beside the fp64 parity headline: returns within the
+    # fp32 tolerance of the reference, ranks not bit-exact
+    tc_variant = None
+    params_dim = es.dim
+    if args.variants and args.precision != "tc" and int(kw.get("fitness_episodes", 1)) >= 5 \
+            and len(kw.get("hidden", ())) == 2:
+        del es
+        _, es_tc, tc_ms, tc_roll, tc_launches = timed_generations("tc")
+        tc_roll_ms = statistics.mean(tc_roll) if tc_roll else None
+        tc_peak = load_peaks().get("bf16_tflops")
+        tc_ach = flops_launch / (tc_roll_ms * 1e-3) / 1e12 if tc_roll_ms else None
+        tc_variant = {
+            "precision": "tc", "value": env_steps_per_gen * args.steps / (tc_ms / 1e3),
+            "unit": "env-steps/s", "ms_per_step": tc_ms / args.steps,
+            "generations_per_sec": args.steps / (tc_ms / 1e3), "gpu_launches": int(tc_launches),
+            "roofline": {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak, "unit": "TFLOP/s",
+                         "frac": (tc_ach / tc_peak) if (tc_ach and tc_peak) else None,
+                         "kernel": "rollout_tc_kernel (cta_group::2 tcgen05 hidden layer, fused env)",
+                         "rollout_ms_per_launch": tc_roll_ms,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops; achieved counts algorithmic flops"},
+            "parity": "returns within fp32 tolerance of the reference; fitness ranks not bit-exact "
+                      "(tools/tc_rank_agreement.py: 10-81 of 4096 ranks shift by <= 9 positions)"}
+        del es_tc
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfgd, args.config)
@@ -341,7 +373,7 @@ def main():
             "dtype": args.precision, "data": "synthetic",
             "config": {"workload": cfgd["desc"], "config": args.config, "pop": pop,
                        "envs_per_individual": e, "horizon": H, "hidden": list(cfg.hidden),
-                       "params": es.dim, "parallelism": f"population-sharded dp{world}",
+                       "params": params_dim, "parallelism": f"population-sharded dp{world}",
                        "l2": "flushed (256 MiB write) between timed generations",
                        "policy_precision": args.precision,
                        "env_dynamics": "f64"},
@@ -351,6 +383,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
+            "tc_variant": tc_variant,
         }
         print(json.dumps(line))
     if dist is not None:

@@ -372,10 +372,15 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   A(dalloc(&s->d_elite_diff, n));
   A(dalloc(&s->d_metrics, 4));
   A(dalloc(&s->d_sel, 1));
-  if (s->warp_path) A(dalloc(&s->d_cand, (size_t)n * d));
-  constexpr double kCandF32Cap = 8.0 * (1ull << 30);  // bytes
-  if (!s->warp_path && cfg->precision != EVORL_PREC_F64 && cfg->algo != EVORL_ALGO_CMAES &&
-      (double)n * (double)d * sizeof(float) <= kCandF32Cap)
+  // materialised ask: the warp path always; the CTA teams when the candidate
+  // matrix fits the cap (fp32 for the fp32 policy paths, fp64 for parity) --
+  // one fully parallel pass instead of every CTA regenerating its slice
+  constexpr double kCandCap = 8.0 * (1ull << 30);  // bytes
+  const bool team_mat = !s->warp_path && cfg->algo != EVORL_ALGO_CMAES;
+  if (s->warp_path ||
+      (team_mat && cfg->precision == EVORL_PREC_F64 && (double)n * (double)d * sizeof(double) <= kCandCap))
+    A(dalloc(&s->d_cand, (size_t)n * d));
+  if (team_mat && cfg->precision != EVORL_PREC_F64 && (double)n * (double)d * sizeof(float) <= kCandCap)
     A(dalloc(&s->d_cand_f32, (size_t)n * d));
   if (cfg->algo == EVORL_ALGO_CMAES) {
     // CmaState::init (proj/src/ec.cpp:191-224)
@@ -663,6 +668,11 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
       count_launch();
       a.par.src = SRC_EXPLICIT_F32;
       a.par.params_f32 = s->d_cand_f32;
+    } else if (s->d_cand) {
+      CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream));
+      count_launch();
+      a.par.src = SRC_EXPLICIT;
+      a.par.params = s->d_cand;
     }
     CK(cudaEventRecord(s->ev_r0, s->stream));
     CK(launch_rollout(a, s->cfg.precision, s->stream));

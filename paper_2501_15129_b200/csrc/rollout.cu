@@ -68,8 +68,9 @@ __global__ void k_materialize_f32(const ParamDesc P, long long d, int a0, int a1
 // (t odd) half of Box-Muller block t >> 1; thread b computes block b once and
 // writes both entries to every agent using them (row, and row + base when
 // mirrored, negated) -- the same value param_value regenerates.
-__global__ void k_materialize_openes_f32(const ParamDesc P, long long d, int a0, int a1, long long t0,
-                                         long long t1, float* out) {
+template <typename T>
+__global__ void k_materialize_openes(const ParamDesc P, long long d, int a0, int a1, long long t0, long long t1,
+                                     T* out) {
   const long long b = (t0 >> 1) + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (2 * b >= t1) return;
   double c, sn;
@@ -86,47 +87,61 @@ __global__ void k_materialize_openes_f32(const ParamDesc P, long long d, int a0,
       const int a = ag[m];
       if (a < a0 || a >= a1) continue;
       const double v = dadd(dmul(P.sigma, m ? -eps : eps), P.mean[p]);
-      out[(long long)(a - a0) * d + p] = __double2float_rn(v);
+      if constexpr (sizeof(T) == 4) {
+        out[(long long)(a - a0) * d + p] = __double2float_rn(v);
+      } else {
+        out[(long long)(a - a0) * d + p] = v;
+      }
     }
   }
+}
+
+// sampled noise rows [r0, r1) used by agents [a0, a1) (OpenES: agent a < base
+// uses row a, a >= base row a - base when mirrored)
+static void openes_rows(const ParamDesc& par, int a0, int a1, long long& r0, long long& r1) {
+  r0 = a0;
+  r1 = a1;
+  if (!par.mirrored) return;
+  const long long base = par.base;
+  r0 = LLONG_MAX;
+  r1 = LLONG_MIN;
+  if (a0 < base) {
+    r0 = std::min<long long>(r0, a0);
+    r1 = std::max<long long>(r1, std::min<long long>(a1, base));
+  }
+  if (a1 > base) {
+    r0 = std::min<long long>(r0, std::max<long long>(a0, base) - base);
+    r1 = std::max<long long>(r1, a1 - base);
+  }
+}
+
+template <typename T>
+static cudaError_t materialize(const ParamDesc& par, long long d, int a0, int a1, T* out, cudaStream_t stream) {
+  const long long n = (long long)(a1 - a0) * d;
+  if (n <= 0) return cudaSuccess;
+  if (par.src == SRC_OPENES) {
+    long long r0, r1;
+    openes_rows(par, a0, a1, r0, r1);
+    const long long t0 = r0 * d, t1 = r1 * d;
+    const long long blocks = ((t1 + 1) >> 1) - (t0 >> 1);
+    k_materialize_openes<T><<<(unsigned)((blocks + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1, out);
+    return cudaGetLastError();
+  }
+  if constexpr (sizeof(T) == 4) {
+    k_materialize_f32<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, out);
+  } else {
+    k_materialize<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, out);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t run_materialize_f32(const ParamDesc& par, long long d, int a0, int a1, float* out,
                                 cudaStream_t stream) {
-  const long long n = (long long)(a1 - a0) * d;
-  if (n <= 0) return cudaSuccess;
-  if (par.src == SRC_OPENES) {
-    // sampled rows used by agents [a0, a1)
-    long long r0 = a0, r1 = a1;
-    if (par.mirrored) {  // agent a < base uses row a, a >= base uses row a - base
-      const long long base = par.base;
-      r0 = LLONG_MAX;
-      r1 = LLONG_MIN;
-      if (a0 < base) {
-        r0 = std::min<long long>(r0, a0);
-        r1 = std::max<long long>(r1, std::min<long long>(a1, base));
-      }
-      if (a1 > base) {
-        r0 = std::min<long long>(r0, std::max<long long>(a0, base) - base);
-        r1 = std::max<long long>(r1, a1 - base);
-      }
-    }
-    const long long t0 = r0 * d, t1 = r1 * d;
-    const long long blocks = ((t1 + 1) >> 1) - (t0 >> 1);
-    k_materialize_openes_f32<<<(unsigned)((blocks + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1,
-                                                                                    out);
-    return cudaGetLastError();
-  }
-  k_materialize_f32<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, out);
-  return cudaGetLastError();
+  return materialize(par, d, a0, a1, out, stream);
 }
-
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
                             cudaStream_t stream) {
-  const long long n = (long long)(a1 - a0) * d;
-  if (n <= 0) return cudaSuccess;
-  k_materialize<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, out);
-  return cudaGetLastError();
+  return materialize(par, d, a0, a1, out, stream);
 }
 
 template <typename T, int N>
