@@ -20,6 +20,7 @@ generations outside the events; max over ranks.
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import statistics
@@ -44,14 +45,26 @@ CONFIGS = {
               desc="OpenES pop 4096 x 16 envs/individual, 2x256 MLP, Pendulum H=200"),
     "4": dict(algo="cmaes", env="pendulum", fixed_horizon=True, pop=512, hidden=(97, 97),
               max_episode_steps=200, fitness_episodes=1, cmaes_elites=64, cmaes_sigma0=0.1,
-              cmaes_max_dim=10240,
-              desc="CMA-ES pop 512, mu 64, 3x97x97x1 MLP (d=9992), Pendulum H=200, eig every gen"),
+              cmaes_max_dim=10240, cmaes_eig_every=0,
+              desc="CMA-ES pop 512, mu 64, 3x97x97x1 MLP (d=9992), Pendulum H=200, Jacobi eig every "
+                   "k gens (k = floor(1/(10 d (c1+cmu))) = 9)"),
 }
 
 
 def mlp_flops_per_step(obs_dim, hidden, out_dim):
     dims = [obs_dim] + list(hidden) + [out_dim]
     return 2 * sum(a * b for a, b in zip(dims[:-1], dims[1:]))
+
+
+def cma_lazy_gap(d, mu, pop):
+    """max(1, floor(1 / (10 d (c1 + cmu)))) with the reference's CMA constants
+    (proj/src/ec.cpp:191-224; weights log((pop+1)/2) - log(i+1), clamped at 0)."""
+    w = [max(0.0, math.log((pop + 1) / 2.0) - math.log(i + 1)) for i in range(mu)]
+    sw = sum(w)
+    mueff = 1.0 / sum((x / sw) ** 2 for x in w)
+    c1 = 2.0 / ((d + 1.3) ** 2 + mueff)
+    cmu = min(1.0 - c1, 2.0 * (mueff - 2.0 + 1.0 / mueff) / ((d + 2.0) ** 2 + mueff))
+    return max(1, int(math.floor(1.0 / (10.0 * d * (c1 + cmu)))))
 
 
 def load_peaks():
@@ -239,6 +252,12 @@ def main():
         for _ in range(args.warmup):
             step()
         barrier()
+        if kw.get("algo") == "cmaes" and kw.get("cmaes_eig_every", 1) == 0:
+            # lazy CMA-ES: time whole periods so the amortised eigendecomposition
+            # is inside the window (generation counter g -> eig when g % gap == 0)
+            gap = cma_lazy_gap(es.dim, kw["cmaes_elites"], kw["pop"])
+            args.steps = -(-max(args.steps, gap) // gap) * gap
+            args.cma_gap = gap
         launches0 = L.evorl_kernel_launches()
         times, roll = [], []
         if clk is not None:
@@ -376,6 +395,9 @@ def main():
                        "params": params_dim, "parallelism": f"population-sharded dp{world}",
                        "l2": "flushed (256 MiB write) between timed generations",
                        "policy_precision": args.precision,
+                       **({"eig_every": getattr(args, "cma_gap", None),
+                           "timed_window": "whole lazy periods (one eigendecomposition per period)"}
+                          if kw.get("algo") == "cmaes" else {}),
                        "env_dynamics": "f64"},
             "generations_per_sec": args.steps / (max_ms / 1e3),
             "gpu_launches": int(launches),

@@ -187,7 +187,8 @@ typedef struct {
   int32_t device;    /* CUDA ordinal (not a reference key) */
   /* EXTENSION (BASELINE config 4): re-factorise C every k-th generation
    * (lazy CMA-ES).  k = 1 (default) is the reference behaviour
-   * (proj/src/ec.cpp:276-287); B and D stay fixed in between. */
+   * (proj/src/ec.cpp:276-287); B and D stay fixed in between; k = 0 picks
+   * the standard lazy gap max(1, floor(1 / (10 d (c1 + cmu)))). */
   int32_t cmaes_eig_every;
 } evorl_es_config;
 

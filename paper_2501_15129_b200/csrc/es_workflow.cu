@@ -800,7 +800,11 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       c.generation += 1;
       // re-factorise; re-condition when eigenvalues fall to <= 0
       // (EXTENSION: only every cmaes_eig_every-th generation; 1 = reference)
-      const int k_eig = std::max(1, s->cfg.cmaes_eig_every);
+      // k = 0: Hansen's lazy gap max(1, floor(1 / (10 d (c1 + cmu)))), which
+      // keeps the amortised eigendecomposition at O(d^2) per generation
+      const int k_eig = s->cfg.cmaes_eig_every > 0
+                            ? s->cfg.cmaes_eig_every
+                            : std::max(1, (int)std::floor(1.0 / (10.0 * d * (c.c1 + c.cmu))));
       if (c.generation % k_eig != 0) {
         sigma = c.sigma;
         break;

@@ -77,7 +77,7 @@ class EsConfig:
     cem_decay_iters: int = 2000
     precision: str = "f64"               # "f64" (parity) | "f32" | "tc" (tcgen05 hidden layer)
     device: int = 0
-    cmaes_eig_every: int = 1             # EXTENSION: lazy CMA-ES eigendecomposition period
+    cmaes_eig_every: int = 1             # EXTENSION: lazy CMA-ES eigendecomposition period (0 = auto gap)
 
     def to_c(self) -> _lib.EsConfigC:
         c = _lib.EsConfigC()

@@ -129,3 +129,33 @@ def test_cma_capacity_cap(evb):
     with pytest.raises(evb.LengthError, match="capacity cap"):
         evb.EsWorkflow(evb.EsConfig(algo="cmaes", env="pendulum", hidden=(64, 64), cmaes_max_dim=4096,
                                     pop=16, cmaes_elites=8))
+
+
+def test_cma_lazy_eig_auto_gap(evb):
+    """EXTENSION (BASELINE config 4): cmaes_eig_every = 0 re-factorises C every
+    k = max(1, floor(1/(10 d (c1+cmu)))) generations; B and D stay fixed in
+    between while C keeps updating, and at each refresh B D^2 B^T = C."""
+    import math
+    cfg = evb.EsConfig(algo="cmaes", env="pendulum", fixed_horizon=True, pop=32, hidden=(64,),
+                       max_episode_steps=40, cmaes_elites=8, cmaes_sigma0=0.2, cmaes_eig_every=0)
+    g = evb.EsWorkflow(cfg).init((3, 4))
+    d, mu, pop = g.dim, 8, 32
+    w = [max(0.0, math.log((pop + 1) / 2) - math.log(i + 1)) for i in range(mu)]  # proj/src/ec.cpp:205-212
+    mueff = sum(w) ** 2 / sum(x * x for x in w)
+    c1 = 2.0 / ((d + 1.3) ** 2 + mueff)
+    cmu = min(1 - c1, 2 * (mueff - 2 + 1 / mueff) / ((d + 2) ** 2 + mueff))
+    gap = max(1, math.floor(1 / (10 * d * (c1 + cmu))))
+    assert gap >= 2
+    prev = g.cma_state()
+    for gen in range(1, 2 * gap + 1):
+        g.step()
+        s = g.cma_state()
+        assert s["generation"] == gen
+        assert not np.array_equal(s["C"], prev["C"])
+        if gen % gap:
+            assert np.array_equal(s["B"], prev["B"]) and np.array_equal(s["D"], prev["D"]), gen
+        else:
+            assert not np.array_equal(s["B"], prev["B"]), gen
+            Bm, Dv, Cm = s["B"], s["D"], s["C"]
+            assert np.abs(Bm @ np.diag(Dv ** 2) @ Bm.T - Cm).max() < 1e-11 * np.abs(Cm).max()
+        prev = s
