@@ -179,6 +179,8 @@ struct evorl_es {
   // fp32, materialised once by a fully parallel ask instead of being
   // regenerated in every CTA's prologue (null: regenerate, e.g. over the cap)
   float* d_cand_f32 = nullptr;
+  double* d_tell_part = nullptr;  // OpenES tell: per-row-chunk partial contractions
+  long long tell_part_cap = 0;
   cudaStream_t stream = nullptr;
   // WorkflowState (proj/include/evorl/workflow.hpp:31-36)
   DKey rng{};
@@ -272,7 +274,7 @@ static void free_all(evorl_es* s) {
                   s->d_ep_returns, s->d_lane_stats, s->d_agent_stats, s->d_lane_steps, s->d_rank,
                   s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
                   s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand,
-                  s->d_cand_f32};
+                  s->d_cand_f32, s->d_tell_part};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
@@ -732,6 +734,17 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       t.shaped = s->d_shaped;
       t.adam_bc = s->d_adam_bc;
       t.adam_bc_len = s->adam_bc_len;
+      {
+        const long long need = (long long)openes_tell_chunks(t.base, s->p1 - s->p0) * (s->p1 - s->p0);
+        if (need > s->tell_part_cap) {
+          if (s->d_tell_part) cudaFree(s->d_tell_part);
+          s->d_tell_part = nullptr;
+          s->tell_part_cap = 0;
+          CK(cudaMalloc((void**)&s->d_tell_part, sizeof(double) * need));
+          s->tell_part_cap = need;
+        }
+      }
+      t.partial = s->d_tell_part;
       CK(run_openes_tell(t, st));
       CK(run_inc_counter(s->d_t, st));
       s->adam_t_host += 1;
@@ -1306,7 +1319,7 @@ extern "C" int evorl_openes_tell(double* mean, double* m, double* v, int64_t* t,
   if (n < 1) return set_err(EVORL_E_INVALID_ARGUMENT, "openes_tell: eps/fitness size mismatch");
   if (mirrored && n % 2)
     return set_err(EVORL_E_INVALID_ARGUMENT, "openes_ask: mirrored sampling needs an even population");
-  Scratch a, b, c, f, r, sh, tt, bc;
+  Scratch a, b, c, f, r, sh, tt, bc, pt;
   double *dmean, *dm, *dv, *df, *dsh, *dbc;
   int* dr;
   long long* dt;
@@ -1347,6 +1360,10 @@ extern "C" int evorl_openes_tell(double* mean, double* m, double* v, int64_t* t,
   // single-entry table holding exactly this step's corrections
   ta.adam_bc = dbc - 2 * th;  // index 2*(t-1) with t = th+1 -> dbc[0]
   ta.adam_bc_len = th + 1;
+  double* dpart = nullptr;
+  const long long part_n = (long long)openes_tell_chunks(ta.base, d) * d;
+  if (int rc = up(pt, (const double*)nullptr, (size_t)part_n, &dpart)) return rc;
+  ta.partial = dpart;
   CK(run_openes_tell(ta, 0));
   CK(cudaMemcpy(mean, dmean, sizeof(double) * d, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(m, dm, sizeof(double) * d, cudaMemcpyDeviceToHost));

@@ -313,15 +313,19 @@ cudaError_t run_metrics(const double* f, int n, double* out, cudaStream_t s) {
 // Each thread owns V consecutive coordinates so one Box-Muller block feeds
 // two of them (normal #2b -> cos, #2b+1 -> sin).
 constexpr int TELL_V = 8;
-__global__ void __launch_bounds__(128) k_openes_tell(const OpenEsTellArgs a) {
+constexpr int TELL_T = 128;
+// Partial contraction of one row chunk: partial[chunk][p - p0] =
+// sum_{i in chunk} eps_i[p] w_i (sequential fma over the chunk's rows).
+__global__ void __launch_bounds__(TELL_T) k_openes_tell_partial(const OpenEsTellArgs a, int chunk_rows) {
   __shared__ double wsh[1024];
   const long long pbase = a.p0 + (blockIdx.x * (long long)blockDim.x + threadIdx.x) * TELL_V;
   const int rows = a.mirrored ? a.base : a.n;
+  const int r0 = blockIdx.y * chunk_rows, r1 = min(rows, r0 + chunk_rows);
   double acc[TELL_V];
 #pragma unroll
   for (int v = 0; v < TELL_V; ++v) acc[v] = 0.0;
-  for (int i0 = 0; i0 < rows; i0 += 1024) {
-    const int lim = min(1024, rows - i0);
+  for (int i0 = r0; i0 < r1; i0 += 1024) {
+    const int lim = min(1024, r1 - i0);
     __syncthreads();
     for (int q = threadIdx.x; q < lim; q += blockDim.x) {
       const int i = i0 + q;
@@ -356,6 +360,20 @@ __global__ void __launch_bounds__(128) k_openes_tell(const OpenEsTellArgs a) {
     }
   }
   if (pbase >= a.p1) return;
+  const long long span = a.p1 - a.p0;
+  double* out = a.partial + (long long)blockIdx.y * span + (pbase - a.p0);
+#pragma unroll
+  for (int v = 0; v < TELL_V; ++v)
+    if (pbase + v < a.p1) out[v] = acc[v];
+}
+
+// g_p = sum over chunks (fixed order) / (n sigma), then adam_step.
+__global__ void k_openes_adam(const OpenEsTellArgs a, int chunks) {
+  const long long p = a.p0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= a.p1 || p >= a.d) return;
+  const long long span = a.p1 - a.p0;
+  double acc = 0.0;
+  for (int c = 0; c < chunks; ++c) acc = dadd(acc, a.partial[(long long)c * span + (p - a.p0)]);
   const long long t = *a.t_dev + 1;
   double bc1, bc2;
   if (t <= a.adam_bc_len) {
@@ -366,26 +384,36 @@ __global__ void __launch_bounds__(128) k_openes_tell(const OpenEsTellArgs a) {
     bc2 = 1.0 - pow(a.beta2, (double)t);
   }
   const double denom = dmul((double)a.n, a.sigma);
-#pragma unroll
-  for (int v = 0; v < TELL_V; ++v) {
-    const long long p = pbase + v;
-    if (p >= a.p1 || p >= a.d) break;
-    const double grad = -ddiv(acc[v], denom);  // Adam descends along -g
-    const double m = dadd(dmul(a.beta1, a.m[p]), dmul(a.omb1, grad));
-    const double vv = dadd(dmul(a.beta2, a.v[p]), dmul(a.omb2, dmul(grad, grad)));
-    double prm = a.mean[p];
-    prm = dsub(prm, ddiv(dmul(a.lr, ddiv(m, bc1)), dadd(sqrt(ddiv(vv, bc2)), a.eps)));
-    if (a.weight_decay != 0.0) prm = dsub(prm, dmul(a.lrwd, prm));
-    a.m[p] = m;
-    a.v[p] = vv;
-    a.mean[p] = prm;
-  }
+  const double grad = -ddiv(acc, denom);  // Adam descends along -g
+  const double m = dadd(dmul(a.beta1, a.m[p]), dmul(a.omb1, grad));
+  const double vv = dadd(dmul(a.beta2, a.v[p]), dmul(a.omb2, dmul(grad, grad)));
+  double prm = a.mean[p];
+  prm = dsub(prm, ddiv(dmul(a.lr, ddiv(m, bc1)), dadd(sqrt(ddiv(vv, bc2)), a.eps)));
+  if (a.weight_decay != 0.0) prm = dsub(prm, dmul(a.lrwd, prm));
+  a.m[p] = m;
+  a.v[p] = vv;
+  a.mean[p] = prm;
 }
+
+int openes_tell_chunks(int rows, long long span) {
+  // fill ~8 resident CTAs of TELL_T threads per SM over 148 SMs, keeping
+  // >= 32 rows per chunk so the Box-Muller work dominates the partial traffic
+  const long long coord_threads = (span + TELL_V - 1) / TELL_V;
+  const long long want = (148LL * 8 * TELL_T + coord_threads - 1) / std::max(1LL, coord_threads);
+  const long long by_rows = std::max(1, rows / 32);
+  return (int)std::max(1LL, std::min({want, by_rows, 256LL}));
+}
+
 cudaError_t run_openes_tell(const OpenEsTellArgs& a, cudaStream_t s) {
   const long long span = a.p1 - a.p0;
   if (span <= 0) return cudaSuccess;
+  const int rows = a.mirrored ? a.base : a.n;
+  const int chunks = openes_tell_chunks(rows, span);
+  const int chunk_rows = (rows + chunks - 1) / chunks;
   const long long threads = (span + TELL_V - 1) / TELL_V;
-  k_openes_tell<<<blocks_for(threads, 128), 128, 0, s>>>(a);
+  dim3 grid((unsigned)((threads + TELL_T - 1) / TELL_T), (unsigned)chunks);
+  k_openes_tell_partial<<<grid, TELL_T, 0, s>>>(a, chunk_rows);
+  k_openes_adam<<<blocks_for(span, 256), 256, 0, s>>>(a, chunks);
   EVB_CHECK_LAUNCH();
 }
 

@@ -50,7 +50,11 @@ struct OpenEsTellArgs {
   const double* shaped;     // n
   const double* adam_bc;    // [2 * T_max]
   long long adam_bc_len;
+  double* partial;          // scratch: openes_tell_chunks(...) x (p1 - p0) doubles
 };
+// Row chunks of the tell's noise contraction for a coordinate span (so the
+// grid fills the GPU; the chunk partials are summed in a fixed order).
+int openes_tell_chunks(int rows, long long span);
 cudaError_t run_openes_tell(const OpenEsTellArgs& a, cudaStream_t s);
 cudaError_t run_inc_counter(long long* t, cudaStream_t s);
 cudaError_t run_openes_ask(const double* mean, long long d, double sigma, int mirrored, DKey key, int n,
