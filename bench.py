@@ -67,6 +67,14 @@ def cma_lazy_gap(d, mu, pop):
     return max(1, int(math.floor(1.0 / (10.0 * d * (c1 + cmu)))))
 
 
+# DRAM bytes (read + write) per launch of the dominant kernel from one
+# `ncu --set full` capture of the same command (profiles/README.md)
+NCU_TRAFFIC = {
+    ("3", "f64"): (2230139136 + 68040960, "ncu r01_f64_v6: rollout_kernel<double,1,16,4,1>"),
+    ("3", "tc"): (1104589568 + 10959616, "ncu r01_tc_v3: rollout_tc_kernel<2>"),
+}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -348,7 +356,9 @@ def main():
     achieved = flops_launch / (roll_ms * 1e-3) / 1e12 if roll_ms else None
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                 "frac": (achieved / peak) if (achieved and peak) else None,
-                "traffic": None, "kernel": ("rollout_tc_kernel (tcgen05 hidden layer, fused obs-norm/MLP/env/return)"
+"traffic": NCU_TRAFFIC.get((args.config, args.precision), (None,))[0],
+                "traffic_source": NCU_TRAFFIC.get((args.config, args.precision), (None, None))[1],
+                "kernel": ("rollout_tc_kernel (tcgen05 hidden layer, fused obs-norm/MLP/env/return)"
                           if args.precision == "tc" else "rollout_kernel (fused obs-norm/MLP/env/return)"),
                 "algorithmic_flops_per_launch": flops_launch,
                 "flops_per_env_step": F, "peak_source": peak_src,
@@ -373,6 +383,7 @@ def main():
             "generations_per_sec": args.steps / (tc_ms / 1e3), "gpu_launches": int(tc_launches),
             "roofline": {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak, "unit": "TFLOP/s",
                          "frac": (tc_ach / tc_peak) if (tc_ach and tc_peak) else None,
+                         "traffic": NCU_TRAFFIC.get((args.config, "tc"), (None,))[0],
                          "kernel": "rollout_tc_kernel (cta_group::2 tcgen05 hidden layer, fused env)",
                          "rollout_ms_per_launch": tc_roll_ms,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops; achieved counts algorithmic flops"},
