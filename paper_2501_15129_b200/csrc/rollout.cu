@@ -31,6 +31,21 @@
 
 namespace evorl_b200 {
 
+#ifdef EVB_TC_PROFILE
+// Phase cycle counters of the cluster team (profiling build only)
+__device__ unsigned long long g_rk_prof[16];
+#define RK_MARK(i)                                \
+  do {                                            \
+    const long long t_ = clock64();               \
+    rk_prof[i] += (unsigned long long)(t_ - rk_prev); \
+    rk_prev = t_;                                 \
+  } while (0)
+#else
+#define RK_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 template <typename T>
 EVB_DEV T to_T(double v);
 template <>
@@ -420,6 +435,17 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
       bo[o] = to_T<T>(param_value(A.par, N.d, agent_local, agent, N.b_off[L - 1] + o));
   }
 
+  // output-exchange mbarriers (double-buffered by step parity): every CTA of
+  // the cluster st.async's its partial outputs into every CTA's pout, and the
+  // env threads wait for the bytes (no cluster barrier per step)
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(smem + S.off_bar);
+  if (C > 1 && tid == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (C > 1) cluster_sync_all();  // peers' prologues (SMEM zeroing, barriers) done
+
   // ------------------------------------------------------------ lane state
   const int j = group * ET + tid;  // lane index within the agent
   const bool is_env = tid < ET;
@@ -481,12 +507,18 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
     }
   };
   if (valid && eps_this > 0 && A.max_iters > 0) observe_into_x0(true);
+#ifdef EVB_TC_PROFILE
+  unsigned long long rk_prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long rk_prev = clock64();
+#endif
 
   for (int it = 0;; ++it) {
     if (tid < MAXL) mask[(it & 1) * MAXL + tid] = 0u;  // last used two steps ago
     const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
     if (!__syncthreads_or(active)) break;  // also orders the x0 writes before layer 0
+    RK_MARK(0);  // loop-top barrier
     uint32_t* cur_mask = mask + (it & 1) * MAXL;
+    if (C > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[it & 1], (uint32_t)(C * OE1 * sizeof(T)));
     // output partials are double-buffered by step parity: with a single
     // cluster barrier per step, a fast CTA may write step t+1's partials
     // while a slow one still reads step t's
@@ -565,6 +597,7 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
       } else {
         __syncthreads();
       }
+      RK_MARK(1 + (l > 0 ? 1 : 0));  // layer 0 / layers >= 1 (incl. their barrier)
     }
 
     // output layer partial over this CTA's rows, reduced across the cluster
@@ -596,22 +629,24 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
           v = T(bl);
         }
         if constexpr (C > 1) {
-          const uint32_t la = smem_u32(pout + crank * OE1 + oe);
+          const uint32_t la = smem_u32(pout + crank * OE1 + oe), lb = smem_u32(&xbar[it & 1]);
 #pragma unroll
-          for (int c = 0; c < C; ++c) st_cluster<T>(map_cluster(la, (uint32_t)c), v);
+          for (int c = 0; c < C; ++c)
+            st_async(map_cluster(la, (uint32_t)c), v, map_cluster(lb, (uint32_t)c));
         } else {
           pout[oe] = v;
         }
       }
-      // one cluster barrier per step (measured faster on B200 than mbarrier
-      // point-to-point signalling: 165 vs 175 ms/generation on config 3)
       if constexpr (C > 1) {
-        cluster_sync_all();
+        // only the env threads consume the exchanged outputs: wait for all
+        // C * OE1 values of this step (the other warps run on to the loop top)
+        if (tid < ET) mbar_wait_parity(&xbar[it & 1], (uint32_t)((it >> 1) & 1));
       } else {
         __syncthreads();
       }
     }
 
+    RK_MARK(3);  // output partial + cluster exchange
     // head + env step (proj/src/rollout.cpp:57-90, :131-153), then the next
     // observation (same threads: no extra barrier)
     if (active) {
@@ -668,7 +703,14 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
       const bool next = myfault == 0 && eps_done < eps_this && it + 1 < A.max_iters;
       observe_into_x0(next);
     }
+    RK_MARK(4);  // head + env + observe
   }
+#ifdef EVB_TC_PROFILE
+  if (tid == 0) {
+    for (int i = 0; i < 5; ++i) atomicAdd(&g_rk_prof[i], rk_prof[i]);
+    atomicAdd(&g_rk_prof[8], 1ull);
+  }
+#endif
 
   if (valid && crank == 0) {
     const long long lane = (long long)agent_local * A.e + j;
@@ -685,6 +727,14 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   }
   if constexpr (C > 1) cluster_sync_all();  // no CTA may exit while peers still address its SMEM
 }
+
+#ifdef EVB_TC_PROFILE
+extern "C" int evorl_debug_rk_profile(unsigned long long* out16) {
+  if (cudaMemcpyFromSymbol(out16, g_rk_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 6;
+  static const unsigned long long zero[16] = {};
+  return cudaMemcpyToSymbol(g_rk_prof, zero, sizeof zero) == cudaSuccess ? 0 : 6;
+}
+#endif
 
 // ------------------------------------------------------------------ host side
 static int align16(int x) { return (x + 15) & ~15; }

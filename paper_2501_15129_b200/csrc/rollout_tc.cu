@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
   uint64_t* l0bar = mbar + 1;  // [TC_MAX_ROUNDS]: layer-0 rounds stored
+  uint64_t* xbar = l0bar + TC_MAX_ROUNDS;  // [2]: partial outputs of every cluster CTA landed
   __syncthreads();
   if (warp == 0) {
     if constexpr (PAIR) {  // both CTAs of the pair: same columns in each TMEM
@@ -207,6 +208,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     // layer-0 round rd stored: every warp of this CTA (and, on a pair's even
     // CTA, of its odd peer) arrives once per step
     for (int i = 0; i < TC_MAX_ROUNDS; ++i) mbar_init(&l0bar[i], (PAIR ? 2 : 1) * (TC_THREADS / 32));
+    mbar_init(&xbar[0], 1);  // output exchange, double-buffered by step parity
+    mbar_init(&xbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -324,6 +327,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     if (!__syncthreads_or(active)) break;
     TC_MARK(1);  // loop-top barrier
     float* pout = pout_base + (it & 1) * C * OE1;
+    if (C > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[it & 1], (uint32_t)(C * OE1 * sizeof(float)));
 
     // layer 0: h1 = relu(W0 x0 + b0) -> B operand (fp16 hi/lo).  C == 1: all
     // 16 lanes; PAIR: the 8 lanes of this CTA's B columns.  k-step ks (16 rows
@@ -507,15 +511,19 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
         v = (float)bl;
       }
       if constexpr (C > 1) {
-        const uint32_t la = smem_u32(pout + crank * OE1 + oe);
+        const uint32_t la = smem_u32(pout + crank * OE1 + oe), lb = smem_u32(&xbar[it & 1]);
 #pragma unroll
-        for (int c = 0; c < C; ++c) st_cluster<float>(map_cluster(la, (uint32_t)c), v);
+        for (int c = 0; c < C; ++c) st_async(map_cluster(la, (uint32_t)c), v, map_cluster(lb, (uint32_t)c));
       } else {
         pout[oe] = v;
       }
     }
     if constexpr (C > 1) {
-      cluster_sync_all();
+      // st.async + mbarrier: only the env threads wait for the cluster's
+      // partial outputs.  This also orders the pair's B reuse: a CTA reaches
+      // the next step's layer 0 only after its env threads saw the leader's
+      // outputs, which the leader sends after its MMA completed.
+      if (tid < TC_N) mbar_wait_parity(&xbar[it & 1], (uint32_t)((it >> 1) & 1));
     } else {
       __syncthreads();
     }
@@ -650,7 +658,7 @@ bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.off_mask = off;
   off = al(off + MAXL * 4, 16);
   p.off_bar = off;
-  off = al(off + 8 * (1 + TC_MAX_ROUNDS), 16);
+  off = al(off + 8 * (3 + TC_MAX_ROUNDS), 16);
   p.off_tslot = off;
   off = al(off + 16, 16);
   p.bytes = off;
