@@ -179,6 +179,7 @@ struct evorl_es {
   // fp32, materialised once by a fully parallel ask instead of being
   // regenerated in every CTA's prologue (null: regenerate, e.g. over the cap)
   float* d_cand_f32 = nullptr;
+  int cand_cap = 0;               // agents per materialised chunk (team path)
   double* d_tell_part = nullptr;  // OpenES tell: per-row-chunk partial contractions
   long long tell_part_cap = 0;
   cudaStream_t stream = nullptr;
@@ -377,13 +378,22 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   // materialised ask: the warp path always; the CTA teams when the candidate
   // matrix fits the cap (fp32 for the fp32 policy paths, fp64 for parity) --
   // one fully parallel pass instead of every CTA regenerating its slice
-  constexpr double kCandCap = 8.0 * (1ull << 30);  // bytes
+  // (chunks of cand_cap agents when the whole population exceeds the cap;
+  // the global-weights plan reads its weights from this buffer)
+  // (EVORL_CAND_CAP_BYTES overrides the 8 GiB cap -- used by the chunking test)
+  static const double kCandCap =
+      getenv("EVORL_CAND_CAP_BYTES") ? atof(getenv("EVORL_CAND_CAP_BYTES")) : 8.0 * (1ull << 30);
   const bool team_mat = !s->warp_path && cfg->algo != EVORL_ALGO_CMAES;
-  if (s->warp_path ||
-      (team_mat && cfg->precision == EVORL_PREC_F64 && (double)n * (double)d * sizeof(double) <= kCandCap))
-    A(dalloc(&s->d_cand, (size_t)n * d));
-  if (team_mat && cfg->precision != EVORL_PREC_F64 && (double)n * (double)d * sizeof(float) <= kCandCap)
-    A(dalloc(&s->d_cand_f32, (size_t)n * d));
+  if (s->warp_path) A(dalloc(&s->d_cand, (size_t)n * d));
+  if (team_mat) {
+    const size_t tsz = cfg->precision == EVORL_PREC_F64 ? sizeof(double) : sizeof(float);
+    s->cand_cap = (int)std::max(1.0, std::min((double)n, std::floor(kCandCap / ((double)d * tsz))));
+    if (cfg->precision == EVORL_PREC_F64) {
+      A(dalloc(&s->d_cand, (size_t)s->cand_cap * d));
+    } else {
+      A(dalloc(&s->d_cand_f32, (size_t)s->cand_cap * d));
+    }
+  }
   if (cfg->algo == EVORL_ALGO_CMAES) {
     // CmaState::init (proj/src/ec.cpp:191-224)
     if (d > cfg->cmaes_max_dim) {
@@ -665,20 +675,30 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
     CK(cudaEventRecord(s->ev_r0, s->stream));
     CK(launch_rollout_warp(a, s->wplan, s->cfg.precision, s->stream));
   } else {
-    if (s->d_cand_f32) {
-      CK(run_materialize_f32(a.par, s->d, s->a0, s->a1, s->d_cand_f32, s->stream));
+    // team path: materialise the shard's candidates (chunks of cand_cap
+    // agents), then roll each chunk out
+    for (int c0 = s->a0; c0 < s->a1; c0 += s->cand_cap) {
+      const int c1 = std::min(s->a1, c0 + s->cand_cap);
+      RolloutArgs ac = a;
+      ac.n_agents = c1 - c0;
+      ac.agent_offset = c0;
+      ac.ep_returns = s->d_ep_returns + (long long)c0 * s->count;
+      ac.lane_steps = s->d_lane_steps + (long long)c0 * s->e;
+      ac.lane_stats = s->d_lane_stats + (long long)c0 * s->e * 9;
+      if (s->d_cand_f32) {
+        CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream));
+        ac.par.src = SRC_EXPLICIT_F32;
+        ac.par.params_f32 = s->d_cand_f32;
+      } else {
+        CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream));
+        ac.par.src = SRC_EXPLICIT;
+        ac.par.params = s->d_cand;
+      }
       count_launch();
-      a.par.src = SRC_EXPLICIT_F32;
-      a.par.params_f32 = s->d_cand_f32;
-    } else if (s->d_cand) {
-      CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream));
+      if (c0 == s->a0) CK(cudaEventRecord(s->ev_r0, s->stream));
+      CK(launch_rollout(ac, s->cfg.precision, s->stream));
       count_launch();
-      a.par.src = SRC_EXPLICIT;
-      a.par.params = s->d_cand;
     }
-    CK(cudaEventRecord(s->ev_r0, s->stream));
-    CK(launch_rollout(a, s->cfg.precision, s->stream));
-    count_launch();
   }
   CK(cudaEventRecord(s->ev_r1, s->stream));
   CK(run_fitness(a.ep_returns, s->count, a.n_agents, s->a0, s->d_fitness, a.lane_steps, s->e, s->d_steps,
@@ -1075,7 +1095,15 @@ extern "C" int evorl_es_evaluate(evorl_es* s, int32_t episodes, uint64_t key_hi,
   a.ep_returns = rets;
   a.lane_steps = steps;
   a.fault = s->d_fault;
+  float* mean_f32 = nullptr;
+  if (plan.gw && s->cfg.precision != EVORL_PREC_F64) {  // global-weights fp32 team reads an fp32 row
+    CK(cudaMallocAsync((void**)&mean_f32, sizeof(float) * s->d, s->stream));
+    CK(run_materialize_f32(a.par, s->d, 0, 1, mean_f32, s->stream));
+    a.par.src = SRC_EXPLICIT_F32;
+    a.par.params_f32 = mean_f32;
+  }
   CK(launch_rollout(a, s->cfg.precision, s->stream));
+  if (mean_f32) CK(cudaFreeAsync(mean_f32, s->stream));
   count_launch();
   CK(run_eval_reduce(rets, episodes, out2, s->stream));
   CK(cudaMemcpyAsync(s->h->eval, out2, sizeof(double) * 2, cudaMemcpyDeviceToHost, s->stream));
@@ -1270,6 +1298,14 @@ extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp
   a.lane_steps = dsteps;
   a.lane_stats = dstats;
   a.fault = dfault;
+  Scratch sf32;
+  if (!use_warp && plan.gw && precision != EVORL_PREC_F64) {  // global-weights fp32 team reads fp32 rows
+    float* pf = nullptr;
+    if (int rc = up(sf32, (const float*)nullptr, (size_t)m * d, &pf)) return rc;
+    CK(run_materialize_f32(a.par, d, 0, m, pf, 0));
+    a.par.src = SRC_EXPLICIT_F32;
+    a.par.params_f32 = pf;
+  }
   if (use_warp) {
     CK(launch_rollout_warp(a, wplan, precision, 0));
   } else {

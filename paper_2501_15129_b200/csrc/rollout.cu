@@ -57,6 +57,18 @@ EVB_DEV float to_T<float>(double v) {
   return __double2float_rn(v);
 }
 
+// candidate row base for the global-weights plan (materialised ask)
+template <typename T>
+EVB_DEV const T* gparams(const ParamDesc& P);
+template <>
+EVB_DEV const double* gparams<double>(const ParamDesc& P) {
+  return P.params;
+}
+template <>
+EVB_DEV const float* gparams<float>(const ParamDesc& P) {
+  return P.params_f32;
+}
+
 EVB_DEV uint32_t ld_cluster_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
@@ -402,7 +414,9 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   // every CTA avoids one DSMEM scatter + cluster barrier per step).
   for (int i = tid; i < S.bytes / 4; i += ROLLOUT_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
   __syncthreads();
-  for (int l = 0; l < nh; ++l) {
+  // global-weights plan: this agent's materialised candidate row (HBM / L2)
+  const T* gp = S.gw ? gparams<T>(A.par) + (long long)agent_local * N.d : nullptr;
+  for (int l = 0; l < nh && !S.gw; ++l) {
     const int K = N.dims[l], W = N.dims[l + 1];
     const int RS = S.RS[l], r0 = S.REP[l] ? 0 : crank * RS;
     const int RSv = max(0, min(RS, W - r0));
@@ -423,7 +437,7 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   const int KRP = nh > 0 ? S.RSP[nh - 1] : Kout;
   const int k0out = nh > 0 ? crank * KRS : 0;
   const int KRv = max(0, min(KRS, Kout - k0out));
-  {
+  if (!S.gw) {
     T* Wo = reinterpret_cast<T*>(smem + S.off_wout);
     T* bo = reinterpret_cast<T*>(smem + S.off_bout);
     for (int i = tid; i < KRv * O; i += ROLLOUT_THREADS) {
@@ -472,8 +486,10 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   T* part = reinterpret_cast<T*>(smem + S.off_part);
   T* pout_base = reinterpret_cast<T*>(smem + S.off_pout);
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem + S.off_mask);
-  const T* Wo = reinterpret_cast<const T*>(smem + S.off_wout);
-  const T* bo = reinterpret_cast<const T*>(smem + S.off_bout);
+  // output layer: flat p = w_off + k * O + o (column-major O x K), the same
+  // k-major indexing as the SMEM copy
+  const T* Wo = S.gw ? gp + N.w_off[L - 1] + (long long)k0out * O : reinterpret_cast<const T*>(smem + S.off_wout);
+  const T* bo = S.gw ? gp + N.b_off[L - 1] : reinterpret_cast<const T*>(smem + S.off_bout);
   const int OE = O * ET;
   const int OE1 = (O + 1) * ET;  // + one row carrying each lane's first non-finite layer
 
@@ -532,8 +548,10 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
       const int RS = S.RS[l], RSP = S.RSP[l], r0 = rep ? 0 : crank * RS;
       const int RSv = max(0, min(RS, W - r0));
       const T* xin = l == 0 ? x0 : reinterpret_cast<const T*>(smem + S.off_h[l - 1]);
-      const T* Ws = reinterpret_cast<const T*>(smem + S.off_w[l]);
-      const T* bs = reinterpret_cast<const T*>(smem + S.off_b[l]);
+      // weights k-major with row stride WS: the SMEM slice, or (gw) the
+      // candidate row itself -- flat p = w_off + k * W + r is k-major, stride W
+      const T* Ws = S.gw ? gp + N.w_off[l] + r0 : reinterpret_cast<const T*>(smem + S.off_w[l]);
+      const T* bs = S.gw ? gp + N.b_off[l] + r0 : reinterpret_cast<const T*>(smem + S.off_b[l]);
       T* hb = reinterpret_cast<T*>(smem + S.off_h[l]);
       const bool last_hidden = l == nh - 1;
       const bool scatter = C > 1 && !rep && !last_hidden;
@@ -745,7 +763,7 @@ static int pow2floor(int x) {
 }
 
 static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int tsize, SmemPlan* P,
-                     bool mma = false) {
+                     bool mma = false, bool gw = false) {
   const int L = net.nlayers, nh = L - 1, O = net.dims[L];
   if (nh == 0 && C > 1) return false;
   if (O > 8 || obs_dim > 4) return false;
@@ -773,23 +791,24 @@ static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int
       KS = 1;
       WS = RSP + 4;
     }
+    if (gw) WS = W;  // the candidate row's own layout
     p.RS[l] = RS;
     p.RSP[l] = RSP;
     p.KS[l] = KS;
     p.WS[l] = WS;
     p.off_w[l] = off;
-    off = align16(off + K * WS * tsize);
+    if (!gw) off = align16(off + K * WS * tsize);
     p.off_b[l] = off;
-    off = align16(off + RSP * tsize);
+    if (!gw) off = align16(off + RSP * tsize);
     if (!mma) part = std::max(part, (size_t)KS * RSP * ET * tsize);
   }
   const int XS = mma ? ET + 4 : ET;
   p.XS = XS;
   const int KRP = nh > 0 ? p.RSP[nh - 1] : net.dims[0];
   p.off_wout = off;
-  off = align16(off + KRP * O * tsize);
+  if (!gw) off = align16(off + KRP * O * tsize);
   p.off_bout = off;
-  off = align16(off + O * tsize);
+  if (!gw) off = align16(off + O * tsize);
   p.off_x0 = off;
   off = align16(off + 4 * XS * tsize);
   for (int l = 0; l < nh; ++l) {
@@ -811,6 +830,7 @@ static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int
   off = align16(off + 16);
   p.bytes = off;
   p.mma = mma ? 1 : 0;
+  p.gw = gw ? 1 : 0;
   if (off > 227 * 1024) return false;
   *P = p;
   return true;
@@ -841,6 +861,10 @@ bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPla
     }
     if (try_plan(net, obs_dim, ET, 1, C, tsize, plan)) return true;
   }
+  // too large for SMEM residency: weights streamed from the materialised
+  // candidates (HBM / L2), rows split over the largest cluster that fits
+  for (int C : {8, 4, 2, 1})
+    if (try_plan(net, obs_dim, ET, 1, C, tsize, plan, false, true)) return true;
   return false;
 }
 

@@ -100,6 +100,8 @@ struct SmemPlan {
   int off_w[MAXL], off_b[MAXL];
   int off_wout, off_bout, off_x0, off_h[MAXL], off_part, off_pout, off_mask, off_bar;
   int bytes;
+  int gw;         // 1: weights read from the materialised candidates in HBM/L2
+                 //    (policies too large for SMEM residency; SIMT slice GEMMs)
   int tc;         // 1: EVORL_PREC_TC tcgen05 team (rollout_tc.cu), plan in tcp
   TcPlanOut tcp;
 };

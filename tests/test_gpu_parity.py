@@ -11,6 +11,7 @@ Bars (SURVEY.md §8(c) parity protocol):
 """
 import ctypes as C
 import math
+import os
 
 import numpy as np
 import pytest
@@ -428,3 +429,52 @@ def test_config3_shape_runs_and_is_deterministic(evb):
     g.set_counters(0, 0, 0)
     g.step()
     assert np.array_equal(g.fitness(), f1)
+
+
+# ------------------------------------------- policies too large for SMEM residency
+@pytest.mark.parametrize("hidden,m,e,H,prec", [
+    ([512, 512], 2, 16, 50, "f64"),
+    ([1024, 1024], 1, 4, 20, "f64"),
+    ([384, 512, 256], 2, 5, 30, "f64"),
+    ([768, 768], 2, 16, 50, "f32"),
+])
+def test_global_weights_team_matches_oracle(oracle, evb, hidden, m, e, H, prec):
+    """Widths beyond the SMEM-resident plans (BASELINE config 5 sweeps to
+    1024) run on the global-weights team: weights read from the candidate rows
+    in HBM/L2 instead of being resident."""
+    ospec, desc = _policy(oracle, evb, "pendulum", hidden)
+    params = np.array([oracle.init_params(ospec, oracle.key_from_seed(600 + a)) for a in range(m)])
+    params += 0.02 * np.random.default_rng(6).standard_normal(params.shape)
+    key = oracle.key_from_seed(601)
+    envspec = oracle.env_spec("pendulum", True, H)
+    want, wsteps, _ = oracle.batched_rollout(envspec, ospec, None, params, e, key, workers=0)
+    got, steps, _ = evb.batched_rollout("pendulum", desc, params, e, key, fixed_horizon=True,
+                                        max_episode_steps=H, precision=prec)
+    assert list(steps) == list(wsteps)
+    w = np.array(want)
+    rel = np.abs(got - w) / np.abs(w)
+    assert rel.max() < (RTOL_CLOSED if prec == "f64" else RTOL_F32), rel.max()
+
+
+def test_chunked_materialised_ask_is_identical(evb):
+    """Populations whose candidate matrix exceeds the cap are materialised and
+    rolled out in chunks (EVORL_CAND_CAP_BYTES shrinks the cap in a child
+    process): fitness identical to the single-chunk run."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, paper_2501_15129_b200 as evb\n"
+            "kw = dict(algo='openes', env='pendulum', fixed_horizon=True, pop=24, hidden=(32, 32),\n"
+            "          max_episode_steps=40, fitness_episodes=16)\n"
+            "g = evb.EsWorkflow(evb.EsConfig(**kw)).init((5, 6)); g.step(); g.step()\n"
+            "print('FIT', g.fitness().tobytes().hex())\n")
+    outs = []
+    for cap in (None, str(7 * 1217 * 8)):  # d = 1217: 7 agents per chunk
+        env = dict(os.environ)
+        if cap:
+            env["EVORL_CAND_CAP_BYTES"] = cap
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        line = [x for x in r.stdout.decode().splitlines() if x.startswith("FIT ")][-1]
+        outs.append(np.frombuffer(bytes.fromhex(line.split()[1]), dtype=np.float64))
+    assert len(outs[0]) == 24
+    assert np.array_equal(outs[0], outs[1])
