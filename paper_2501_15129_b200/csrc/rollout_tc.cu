@@ -6,7 +6,8 @@
 //   * Shape: obs -> [W1] -> [W2] -> O (two hidden layers, BASELINE config 3).
 //     Layer 0 (K = obs_dim <= 4) runs replicated on the CUDA cores in fp32;
 //     layer 1 (W2 x W1, the dense contraction) runs on tcgen05, M = 128 rows
-//     per CTA (a cluster of W2/128 CTAs per agent), N = 16 lanes, K = W1.
+//     per CTA (a cluster of C = pow2(ceil(W2/128)) CTAs per agent, zero-padded
+//     rows past W2), N = 16 lanes, K = W1 rounded up to 16 (zero-padded).
 //   * Precision: bf16 single pass flips ~27% of ranks on this workload
 //     (measured), so each fp32 operand x is split into fp16 hi = fp16(x) and
 //     lo = fp16((x - hi) * 2^11); D0 = Ahi.Bhi and D1 = Ahi.Blo + Alo.Bhi are
@@ -63,8 +64,9 @@ __device__ unsigned long long g_tc_prof[16];
 #endif
 
 struct TcPlan {
-  int C;       // cluster size = W2 / 128
+  int C;       // cluster size: the power of two >= W2 / 128 (rows past W2 are zero)
   int W1, W2;  // hidden widths
+  int W1p;     // W1 rounded up to the MMA K step (16); h1 rows past W1 are zero
   int off_Alo, off_B, off_W0, off_b0, off_x0, off_red, off_pout, off_mask, off_bar, off_tslot;
   int bytes;
 };
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   const int agent_local = team / A.groups;
   const int group = team % A.groups;
   const int agent = A.agent_offset + agent_local;
-  const int W1 = P.W1, W2 = P.W2, O = N.dims[3], K0 = N.dims[0];
+  const int W1 = P.W1, W1p = P.W1p, W2 = P.W2, O = N.dims[3], K0 = N.dims[0];
   const int r0 = crank * TC_M;       // this CTA's rows of layer 1
   // C >= 2: CTA pairs (2p, 2p+1) run cta_group::2 MMAs (M = 256): each CTA
   // holds its 128 weight rows and the B columns of its 8 lanes (N-split), the
@@ -217,8 +219,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
 
-  float* W0 = reinterpret_cast<float*>(smem + P.off_W0);  // [k][W1]
-  float* b0 = reinterpret_cast<float*>(smem + P.off_b0);  // W1
+  float* W0 = reinterpret_cast<float*>(smem + P.off_W0);  // [k][W1p], zero past W1
+  float* b0 = reinterpret_cast<float*>(smem + P.off_b0);  // W1p, zero past W1
   unsigned char* Alo = smem + P.off_Alo;
   // B (K-major, K = W1): C == 1: 32 rows = B_hi of lanes 0..15, then B_lo;
   // PAIR: 16 rows = B_hi of this CTA's lanes 8pv..8pv+7, then their B_lo
@@ -226,13 +228,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   // ---- prologue: this agent's parameters (regenerated or explicit)
   for (int i = tid; i < K0 * W1; i += TC_THREADS) {
     const int k = i / W1, r = i % W1;
-    W0[k * W1 + r] = (float)param_value(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W1 + r);
+    W0[k * W1p + r] = (float)param_value(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W1 + r);
   }
+  const bool row_ok = r0 + row < W2;  // zero-padded rows of the last CTA
   for (int r = tid; r < W1; r += TC_THREADS)
     b0[r] = (float)param_value(A.par, N.d, agent_local, agent, N.b_off[0] + r);
   // layer-1 weights of row `row`: A_hi -> TMEM (lanes = rows, 2 halves per
   // column), A_lo -> SMEM.  Warp halves take alternate 16-wide k chunks.
-  for (int c = half; c < W1 / 16; c += 2) {
+  for (int c = half; c < W1p / 16; c += 2) {
     uint32_t packed[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -240,8 +243,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int k = c * 16 + 2 * q + u;
-        const float w =
-            (float)param_value(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + row);
+        const float w = (row_ok && k < W1) ? (float)param_value(A.par, N.d, agent_local, agent,
+                                                                 N.w_off[1] + (long long)k * W2 + r0 + row)
+                                           : 0.0f;
         split_f16(w, h[u], l[u]);
         *reinterpret_cast<__half*>(Alo + umma_off(row, k, TC_M)) = l[u];
       }
@@ -250,13 +254,13 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     tc_st8(tmem + ((uint32_t)(quad * 32) << 16) + (PAIR ? TC_COL_A2 : TC_COL_A) + c * 8, packed);
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  const float b1r = (float)param_value(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row);
+  const float b1r = row_ok ? (float)param_value(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row) : 0.0f;
   float w2r[TC_MAXO];
 #pragma unroll
   for (int o = 0; o < TC_MAXO; ++o)
-    w2r[o] = o < O ? (float)param_value(A.par, N.d, agent_local, agent,
-                                        N.w_off[2] + (long long)(r0 + row) * O + o)
-                   : 0.0f;
+    w2r[o] = (o < O && row_ok) ? (float)param_value(A.par, N.d, agent_local, agent,
+                                                    N.w_off[2] + (long long)(r0 + row) * O + o)
+                               : 0.0f;
   float b2[TC_MAXO];
 #pragma unroll
   for (int o = 0; o < TC_MAXO; ++o)
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     {
       constexpr int NB = PAIR ? 16 : 32;      // B rows (N) held by this CTA
       constexpr int EH = PAIR ? 1 : 2;        // 8-lane halves computed here
-      const int KS = W1 / 16;
+      const int KS = W1p / 16;
       uint32_t bad = 0u, range = 0u;
       const int el = lane & 7, rp = lane >> 3;
       float xr[EH][4];
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
             const int r = (ks * 2 + gi) * 8 + rp * 2;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              wv[gi][k] = k < K0 ? *reinterpret_cast<const float2*>(W0 + k * W1 + r) : make_float2(0.f, 0.f);
+              wv[gi][k] = k < K0 ? *reinterpret_cast<const float2*>(W0 + k * W1p + r) : make_float2(0.f, 0.f);
             bv[gi] = *reinterpret_cast<const float2*>(b0 + r);
           }
 #pragma unroll
@@ -634,21 +638,24 @@ static int al(int x, int a) { return (x + a - 1) / a * a; }
 bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   if (net.nlayers != 3 || obs_dim > 4 || e < 5) return false;  // 16-lane teams, obs -> W1 -> W2 -> O
   const int W1 = net.dims[1], W2 = net.dims[2], O = net.dims[3];
-  if (W1 % 16 || W1 > 2 * (TC_TMEM_COLS - (W2 >= 2 * TC_M ? TC_COL_A2 : TC_COL_A)) || W2 % TC_M || W2 / TC_M > 8 || O > TC_MAXO)
-    return false;
+  const int W1p = (W1 + 15) / 16 * 16;
+  int C = 1;
+  while (C * TC_M < W2) C *= 2;
+  if (C > 8 || O > TC_MAXO || W1p > 2 * (TC_TMEM_COLS - (C >= 2 ? TC_COL_A2 : TC_COL_A))) return false;
   TcPlan p{};
-  p.C = W2 / TC_M;
+  p.C = C;
   p.W1 = W1;
+  p.W1p = W1p;
   p.W2 = W2;
   int off = 0;
   p.off_Alo = off;
-  off = al(off + TC_M * W1 * 2, 1024);
+  off = al(off + TC_M * W1p * 2, 1024);
   p.off_B = off;
-  off = al(off + (p.C >= 2 ? 16 : 32) * W1 * 2, 1024);
+  off = al(off + (p.C >= 2 ? 16 : 32) * W1p * 2, 1024);
   p.off_W0 = off;
-  off = al(off + 4 * W1 * 4, 16);
+  off = al(off + 4 * W1p * 4, 16);
   p.off_b0 = off;
-  off = al(off + W1 * 4, 16);
+  off = al(off + W1p * 4, 16);
   p.off_x0 = off;
   off = al(off + 4 * TC_N * 4, 16);
   p.off_red = off;

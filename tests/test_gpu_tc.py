@@ -36,6 +36,9 @@ SHAPES = [
     ([16, 128], 2, 16, 16),
     ([256, 256], 3, 5, 7),     # padded 16-lane team, uneven episode split 2,2,1,1,1
     ([128, 256], 2, 40, 40),   # three teams per agent, last one ragged
+    ([97, 97], 2, 16, 16),     # zero-padded K (112) and rows (128)
+    ([64, 64], 2, 16, 16),
+    ([100, 300], 2, 16, 16),   # cluster of 4: the last CTA holds only padding rows
 ]
 
 
@@ -79,9 +82,9 @@ def test_tc_matches_fp32_simt_path(oracle, evb):
 
 
 def test_tc_unsupported_shape_runs_as_fp32(oracle, evb):
-    """Shapes outside the tcgen05 tile (W2 not a multiple of 128, 1 or 3
-    hidden layers) run on the fp32 team -- same answer as precision='f32'."""
-    for hidden in ([96, 96], [64], [32, 16, 8]):
+    """Shapes outside the tcgen05 team (1 or 3 hidden layers, W1 beyond the
+    TMEM-resident A_hi) run on the fp32 team -- same answer as precision='f32'."""
+    for hidden in ([512, 128], [64], [32, 16, 8]):
         ospec, desc = _policy(oracle, evb, "pendulum", hidden)
         params = np.array([oracle.init_params(ospec, oracle.key_from_seed(900))])
         key = oracle.key_from_seed(901)
