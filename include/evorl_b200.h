@@ -48,7 +48,8 @@ enum {
   EVORL_E_NET_FAULT = 4,        /* evorl::NetFault (proj/include/evorl/net.hpp:19-21) */
   EVORL_E_CONFIG = 5,           /* evorl::ConfigError (proj/include/evorl/config.hpp:11-13) */
   EVORL_E_CUDA = 6,             /* device / driver failure */
-  EVORL_E_UNSUPPORTED = 7       /* valid reference input the device path refuses */
+  EVORL_E_UNSUPPORTED = 7,      /* valid reference input the device path refuses */
+  EVORL_E_CHECKPOINT = 8        /* evorl::CheckpointError (proj/include/evorl/checkpoint.hpp:14-16) */
 };
 
 enum { EVORL_PREC_F64 = 0, EVORL_PREC_F32 = 1, EVORL_PREC_TC = 2 };
@@ -210,6 +211,15 @@ int evorl_es_step(evorl_es* es, evorl_step_metrics* out);
 /* Workflow::evaluate (centre evaluation, proj/src/workflow.cpp:103-129) */
 int evorl_es_evaluate(evorl_es* es, int32_t episodes, uint64_t key_hi, uint64_t key_lo,
                       double* mean_return, double* return_std);
+/* Workflow::save / load + checkpoint_save / checkpoint_load
+ * (proj/src/workflow.cpp:70-80, proj/src/checkpoint.cpp:180-212,
+ * proj/src/workflow_es.cpp:181-249): EVORL1 files, workflow id "es", the
+ * reference's segment names, order and encoding -- interchangeable with the
+ * reference's checkpoints.  load() needs a handle created with the same config
+ * and leaves it initialised; errors are EVORL_E_CHECKPOINT with the reference's
+ * messages. */
+int evorl_es_save(evorl_es* es, const char* path);
+int evorl_es_load(evorl_es* es, const char* path);
 /* WorkflowState counters (proj/include/evorl/workflow.hpp:31-36) */
 int evorl_es_counters(const evorl_es* es, int64_t* iteration, int64_t* env_steps,
                       int64_t* episodes);

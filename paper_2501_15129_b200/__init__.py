@@ -4,8 +4,8 @@ The product is ``libevorl_b200.so`` (hand-written sm_100a CUDA behind the C ABI
 in ``include/evorl_b200.h``); this package is the thin host-side mirror of the
 reference's Workflow / ask-tell / rollout interfaces over that ABI.
 """
-from ._lib import (ConfigError, DeviceError, EnvFault, EvorlError, InvalidArgument,
-                   LengthError, MissingExtension, NetFault, Unsupported)
+from ._lib import (CheckpointError, ConfigError, DeviceError, EnvFault, EvorlError,
+                   InvalidArgument, LengthError, MissingExtension, NetFault, Unsupported)
 from .es import (EsConfig, EsWorkflow, StepMetrics, ars_ask, ars_tell, batched_rollout,
                  centered_ranks, env_step_batch, gaussian_matrix, measure_fp64_peak, mlp_desc,
                  openes_ask, openes_tell, param_count, rank_desc, stream_words, sym_eig,
@@ -13,7 +13,7 @@ from .es import (EsConfig, EsWorkflow, StepMetrics, ars_ask, ars_tell, batched_r
 
 __all__ = [
     "ConfigError", "DeviceError", "EnvFault", "EvorlError", "InvalidArgument", "LengthError",
-    "MissingExtension", "NetFault", "Unsupported", "EsConfig", "EsWorkflow", "StepMetrics",
+    "MissingExtension", "NetFault", "Unsupported", "CheckpointError", "EsConfig", "EsWorkflow", "StepMetrics",
     "ars_ask", "ars_tell", "batched_rollout", "centered_ranks", "env_step_batch",
     "gaussian_matrix", "measure_fp64_peak", "mlp_desc", "openes_ask", "openes_tell",
     "param_count", "rank_desc", "stream_words", "sym_eig", "threefry2x64",

@@ -23,6 +23,7 @@ EVORL_E_NET_FAULT = 4
 EVORL_E_CONFIG = 5
 EVORL_E_CUDA = 6
 EVORL_E_UNSUPPORTED = 7
+EVORL_E_CHECKPOINT = 8
 
 PREC_F64, PREC_F32, PREC_TC = 0, 1, 2
 PRECISIONS = {"f64": PREC_F64, "f32": PREC_F32, "tc": PREC_TC}
@@ -70,8 +71,12 @@ class Unsupported(EvorlError):
     code = EVORL_E_UNSUPPORTED
 
 
+class CheckpointError(EvorlError):  # evorl::CheckpointError
+    code = EVORL_E_CHECKPOINT
+
+
 _EXC = {c.code: c for c in (InvalidArgument, LengthError, EnvFault, NetFault, ConfigError,
-                            DeviceError, Unsupported)}
+                            DeviceError, Unsupported, CheckpointError)}
 
 
 class MlpDesc(C.Structure):
@@ -129,7 +134,7 @@ EXPORTS = [
     "evorl_es_shard_ranges", "evorl_es_phase_rollout", "evorl_es_phase_tell",
     "evorl_es_device_buffers", "evorl_es_stream", "evorl_es_last_timings",
     "evorl_measure_fp64_peak", "evorl_measure_dmma_peak", "evorl_es_cma_get", "evorl_es_cma_set",
-    "evorl_sym_eig",
+    "evorl_sym_eig", "evorl_es_save", "evorl_es_load",
 ]
 
 _lib = None
@@ -170,6 +175,8 @@ def load() -> C.CDLL:
     L.evorl_es_init.argtypes = [vp, u64, u64]
     L.evorl_es_step.argtypes = [vp, C.POINTER(StepMetricsC)]
     L.evorl_es_evaluate.argtypes = [vp, i32, u64, u64, C.POINTER(dbl), C.POINTER(dbl)]
+    L.evorl_es_save.argtypes = [vp, C.c_char_p]
+    L.evorl_es_load.argtypes = [vp, C.c_char_p]
     L.evorl_es_counters.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
     L.evorl_es_set_counters.argtypes = [vp, i64, i64, i64]
     L.evorl_es_get_mean.argtypes = [vp, vp]

@@ -1499,3 +1499,352 @@ extern "C" int evorl_sym_eig(const double* A, int32_t n, double* evals, double* 
   return EVORL_OK;
 }
 
+
+// ====================================================== checkpoint interop
+// EVORL1 files (proj/src/checkpoint.cpp:6-212): magic "EVORL1", u32 version 1,
+// length-prefixed workflow id, u32 segment count, then segments {u32 name
+// length, name, u8 type (0 f64, 1 i64), u64 count, little-endian 64-bit words}.
+// EsWorkflow::save/load (proj/src/workflow_es.cpp:181-249) with the base
+// segments of proj/src/workflow.cpp:11-25 and the obs_norm / adam helpers of
+// proj/src/workflow.cpp:146-174, in the same order, so files are
+// interchangeable with the reference's.
+namespace {
+
+struct SegWriter {
+  std::string buf;
+  uint32_t count = 0;
+  static void u32(std::string& b, uint32_t v) {
+    for (int i = 0; i < 4; ++i) b.push_back((char)((v >> (8 * i)) & 0xff));
+  }
+  static void u64(std::string& b, uint64_t v) {
+    for (int i = 0; i < 8; ++i) b.push_back((char)((v >> (8 * i)) & 0xff));
+  }
+  void head(const std::string& name, uint8_t type, uint64_t n) {
+    u32(buf, (uint32_t)name.size());
+    buf += name;
+    buf.push_back((char)type);
+    u64(buf, n);
+    ++count;
+  }
+  void f64(const std::string& name, const double* p, size_t n) {
+    head(name, 0, n);
+    for (size_t i = 0; i < n; ++i) {
+      uint64_t w;
+      std::memcpy(&w, p + i, 8);
+      u64(buf, w);
+    }
+  }
+  void f64(const std::string& name, double v) { f64(name, &v, 1); }
+  void i64(const std::string& name, const int64_t* p, size_t n) {
+    head(name, 1, n);
+    for (size_t i = 0; i < n; ++i) u64(buf, (uint64_t)p[i]);
+  }
+  void i64(const std::string& name, int64_t v) { i64(name, &v, 1); }
+};
+
+struct SegReader {
+  std::vector<std::pair<std::string, std::vector<double>>> f;
+  std::vector<std::pair<std::string, std::vector<int64_t>>> i;
+  const std::vector<double>* fv(const std::string& n) const {
+    for (auto& x : f)
+      if (x.first == n) return &x.second;
+    return nullptr;
+  }
+  const std::vector<int64_t>* iv(const std::string& n) const {
+    for (auto& x : i)
+      if (x.first == n) return &x.second;
+    return nullptr;
+  }
+};
+
+int ckpt_err(const char* fmt, const std::string& a = "", const std::string& b = "") {
+  return set_err(EVORL_E_CHECKPOINT, fmt, a.c_str(), b.c_str());
+}
+
+// parse (proj/src/checkpoint.cpp:72-118): later segments of the same name
+// replace earlier ones, as std::map::operator[] does
+int ckpt_parse(const std::string& bytes, std::string* id, SegReader* r) {
+  size_t pos = 0;
+  bool ok = true;
+  auto need = [&](size_t n) {
+    if (pos + n > bytes.size()) ok = false;
+    return ok;
+  };
+  auto u32 = [&]() -> uint32_t {
+    if (!need(4)) return 0;
+    uint32_t v = 0;
+    for (int k = 0; k < 4; ++k) v |= (uint32_t)(unsigned char)bytes[pos + k] << (8 * k);
+    pos += 4;
+    return v;
+  };
+  auto u64 = [&]() -> uint64_t {
+    if (!need(8)) return 0;
+    uint64_t v = 0;
+    for (int k = 0; k < 8; ++k) v |= (uint64_t)(unsigned char)bytes[pos + k] << (8 * k);
+    pos += 8;
+    return v;
+  };
+  auto str = [&](size_t n) -> std::string {
+    if (!need(n)) return std::string();
+    std::string s = bytes.substr(pos, n);
+    pos += n;
+    return s;
+  };
+  const std::string magic = str(6);
+  if (!ok) return ckpt_err("incompatible checkpoint: truncated file");
+  if (magic != "EVORL1") return ckpt_err("incompatible checkpoint: bad magic");
+  const uint32_t version = u32();
+  if (!ok) return ckpt_err("incompatible checkpoint: truncated file");
+  if (version != 1)
+    return set_err(EVORL_E_CHECKPOINT, "incompatible checkpoint: format version %u", (unsigned)version);
+  *id = str(u32());
+  const uint32_t nseg = u32();
+  if (!ok) return ckpt_err("incompatible checkpoint: truncated file");
+  for (uint32_t sgi = 0; sgi < nseg; ++sgi) {
+    const std::string name = str(u32());
+    if (!need(1)) return ckpt_err("incompatible checkpoint: truncated file");
+    const uint8_t type = (uint8_t)bytes[pos++];
+    const uint64_t n = u64();
+    if (!ok) return ckpt_err("incompatible checkpoint: truncated file");
+    if (type > 1) return ckpt_err("incompatible checkpoint: unknown segment type");
+    if (n > (bytes.size() - pos) / 8) return ckpt_err("incompatible checkpoint: truncated file");
+    if (type == 0) {
+      std::vector<double> v(n);
+      for (uint64_t k = 0; k < n; ++k) {
+        const uint64_t w = u64();
+        std::memcpy(&v[k], &w, 8);
+      }
+      bool replaced = false;
+      for (auto& x : r->f)
+        if (x.first == name) {
+          x.second = std::move(v);
+          replaced = true;
+          break;
+        }
+      if (!replaced) r->f.emplace_back(name, std::move(v));
+    } else {
+      std::vector<int64_t> v(n);
+      for (uint64_t k = 0; k < n; ++k) v[k] = (int64_t)u64();
+      bool replaced = false;
+      for (auto& x : r->i)
+        if (x.first == name) {
+          x.second = std::move(v);
+          replaced = true;
+          break;
+        }
+      if (!replaced) r->i.emplace_back(name, std::move(v));
+    }
+  }
+  if (pos != bytes.size()) return ckpt_err("incompatible checkpoint: trailing bytes after last segment");
+  return EVORL_OK;
+}
+
+}  // namespace
+
+extern "C" int evorl_es_save(evorl_es* s, const char* path) {
+  if (!s->initialised) return set_err(EVORL_E_INVALID_ARGUMENT, "evorl_es_save before evorl_es_init");
+  const long long d = s->d;
+  SegWriter w;
+  // WorkflowState::save_base (proj/src/workflow.cpp:11-17)
+  w.i64("iteration", (int64_t)s->iteration);
+  const int64_t key[2] = {(int64_t)s->rng.hi, (int64_t)s->rng.lo};
+  w.i64("rng", key, 2);
+  w.i64("env_steps", (int64_t)s->env_steps);
+  w.i64("episodes", (int64_t)s->episodes);
+  w.i64("rl_updates", (int64_t)0);
+  // save_obs_norm (proj/src/workflow.cpp:160-165); ObsNormState::none() has
+  // empty mean/var (proj/include/evorl/obs_norm.hpp:27)
+  evorl_obs_norm on{};
+  if (int rc = evorl_es_get_obs_norm(s, &on)) return rc;
+  const int nd = on.mode == EVORL_NORM_NONE ? 0 : on.dim;
+  w.i64("obs_norm/mode", (int64_t)on.mode);
+  w.f64("obs_norm/mean", on.mean, nd);
+  w.f64("obs_norm/var", on.var, nd);
+  w.f64("obs_norm/count", on.count);
+  std::vector<double> mean(d);
+  if (int rc = evorl_es_get_mean(s, mean.data())) return rc;
+  switch (s->cfg.algo) {
+    case EVORL_ALGO_OPENES: {
+      std::vector<double> m(d), v(d);
+      int64_t t = 0;
+      if (int rc = evorl_es_get_adam(s, m.data(), v.data(), &t)) return rc;
+      w.f64("ec/mean", mean.data(), d);
+      w.f64("ec/sigma", s->cfg.openes_sigma);
+      w.f64("ec/adam/m", m.data(), d);
+      w.f64("ec/adam/v", v.data(), d);
+      w.i64("ec/adam/t", t);
+      w.i64("ec/table_seed", (int64_t)0);  // noise-table mode is not on the device path
+      break;
+    }
+    case EVORL_ALGO_ARS:
+    case EVORL_ALGO_VES:
+      w.f64("ec/mean", mean.data(), d);
+      break;
+    case EVORL_ALGO_CMAES: {
+      std::vector<double> C(d * d), B(d * d), Bc(d * d), D(d), ps(d), pc(d);
+      double sigma = 0;
+      int64_t gen = 0, rec = 0;
+      if (int rc = evorl_es_cma_get(s, C.data(), B.data(), D.data(), ps.data(), pc.data(), &sigma, &gen, &rec))
+        return rc;
+      for (long long p = 0; p < d; ++p)  // row-major B[p][j] -> Eigen column-major flat[j*d + p]
+        for (long long j = 0; j < d; ++j) Bc[j * d + p] = B[p * d + j];
+      w.f64("ec/mean", mean.data(), d);
+      w.f64("ec/sigma", sigma);
+      w.f64("ec/C", C.data(), d * d);  // symmetric: row- and column-major coincide
+      w.f64("ec/B", Bc.data(), d * d);
+      w.f64("ec/D", D.data(), d);
+      w.f64("ec/ps", ps.data(), d);
+      w.f64("ec/pc", pc.data(), d);
+      w.i64("ec/generation", gen);
+      w.i64("ec/recondition_count", rec);
+      break;
+    }
+    default: {  // CEM
+      std::vector<double> var(d);
+      CK(cudaMemcpy(var.data(), s->d_var, sizeof(double) * d, cudaMemcpyDeviceToHost));
+      w.f64("ec/mean", mean.data(), d);
+      w.f64("ec/var", var.data(), d);
+      w.i64("ec/iter", (int64_t)s->cem_iter);
+      break;
+    }
+  }
+  // checkpoint_save (proj/src/checkpoint.cpp:180-198): header, then tmp + rename
+  std::string out = "EVORL1";
+  SegWriter::u32(out, 1);
+  const std::string id = "es";
+  SegWriter::u32(out, (uint32_t)id.size());
+  out += id;
+  SegWriter::u32(out, w.count);
+  out += w.buf;
+  const std::string fpath(path), tmp = fpath + ".tmp";
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return ckpt_err("cannot write checkpoint: %s", tmp);
+  const size_t wr = std::fwrite(out.data(), 1, out.size(), f);
+  const int cl = std::fclose(f);
+  if (wr != out.size() || cl != 0) return ckpt_err("short write to checkpoint: %s", tmp);
+  std::remove(fpath.c_str());
+  if (std::rename(tmp.c_str(), fpath.c_str()) != 0) return ckpt_err("cannot finalize checkpoint: %s", fpath);
+  return EVORL_OK;
+}
+
+extern "C" int evorl_es_load(evorl_es* s, const char* path) {
+  CK(cudaSetDevice(s->cfg.device));
+  std::string bytes;
+  {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return ckpt_err("cannot open checkpoint: %s", path);
+    char buf[1 << 16];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) bytes.append(buf, n);
+    std::fclose(f);
+  }
+  std::string id;
+  SegReader r;
+  if (int rc = ckpt_parse(bytes, &id, &r)) return rc;
+  if (id != "es") return ckpt_err("incompatible checkpoint: workflow '%s', expected '%s'", id, "es");
+  const long long d = s->d;
+  auto scal_i = [&](const char* n, int64_t* out) -> int {
+    const auto* v = r.iv(n);
+    if (!v || v->size() != 1) return ckpt_err("checkpoint: missing integer segment '%s'", n);
+    *out = (*v)[0];
+    return EVORL_OK;
+  };
+  auto scal_f = [&](const char* n, double* out) -> int {
+    const auto* v = r.fv(n);
+    if (!v || v->size() != 1) return ckpt_err("checkpoint: missing scalar segment '%s'", n);
+    *out = (*v)[0];
+    return EVORL_OK;
+  };
+  auto vec = [&](const char* n, long long len, const std::vector<double>** out) -> int {
+    const auto* v = r.fv(n);
+    if (!v) return ckpt_err("checkpoint: missing segment '%s'", n);
+    if (len >= 0 && (long long)v->size() != len) return ckpt_err("checkpoint: segment '%s' has wrong size", n);
+    *out = v;
+    return EVORL_OK;
+  };
+  // load_base (proj/src/workflow.cpp:19-25)
+  int64_t it = 0, steps = 0, eps = 0, rl = 0;
+  if (int rc = scal_i("iteration", &it)) return rc;
+  const auto* key = r.iv("rng");
+  if (!key || key->size() != 2) return ckpt_err("checkpoint: missing key segment '%s'", "rng");
+  if (int rc = scal_i("env_steps", &steps)) return rc;
+  if (int rc = scal_i("episodes", &eps)) return rc;
+  if (int rc = scal_i("rl_updates", &rl)) return rc;
+  // load_obs_norm (proj/src/workflow.cpp:167-174)
+  int64_t mode = 0;
+  double count = 0;
+  const std::vector<double>*nmean, *nvar;
+  if (int rc = scal_i("obs_norm/mode", &mode)) return rc;
+  if (int rc = vec("obs_norm/mean", -1, &nmean)) return rc;
+  if (int rc = vec("obs_norm/var", (long long)nmean->size(), &nvar)) return rc;
+  if (int rc = scal_f("obs_norm/count", &count)) return rc;
+  if (mode < 0 || mode > 2 || nmean->size() > 4 || (mode != 0 && (int)nmean->size() != s->env.obs_dim))
+    return ckpt_err("checkpoint: segment '%s' has wrong size", "obs_norm/mean");
+  const std::vector<double>* mean;
+  if (int rc = vec("ec/mean", d, &mean)) return rc;
+  // stage everything before touching the handle (no partial state on error)
+  switch (s->cfg.algo) {
+    case EVORL_ALGO_OPENES: {
+      double sigma = 0;
+      int64_t t = 0, seed = 0;
+      const std::vector<double>*m, *v;
+      if (int rc = scal_f("ec/sigma", &sigma)) return rc;
+      if (int rc = vec("ec/adam/m", d, &m)) return rc;
+      if (int rc = vec("ec/adam/v", d, &v)) return rc;
+      if (int rc = scal_i("ec/adam/t", &t)) return rc;
+      if (int rc = scal_i("ec/table_seed", &seed)) return rc;
+      if (seed != 0 || s->cfg.openes_noise_table)
+        return set_err(EVORL_E_UNSUPPORTED, "openes noise_table mode: device path not built in this revision");
+      s->cfg.openes_sigma = sigma;
+      if (int rc = evorl_es_set_adam(s, m->data(), v->data(), t)) return rc;
+      break;
+    }
+    case EVORL_ALGO_ARS:
+    case EVORL_ALGO_VES:
+      break;
+    case EVORL_ALGO_CMAES: {
+      double sigma = 0;
+      int64_t gen = 0, rec = 0;
+      const std::vector<double>*C, *B, *D, *ps, *pc;
+      if (int rc = scal_f("ec/sigma", &sigma)) return rc;
+      if (int rc = vec("ec/C", d * d, &C)) return rc;
+      if (int rc = vec("ec/B", d * d, &B)) return rc;
+      if (int rc = vec("ec/D", d, &D)) return rc;
+      if (int rc = vec("ec/ps", d, &ps)) return rc;
+      if (int rc = vec("ec/pc", d, &pc)) return rc;
+      if (int rc = scal_i("ec/generation", &gen)) return rc;
+      if (int rc = scal_i("ec/recondition_count", &rec)) return rc;
+      std::vector<double> Br(d * d);
+      for (long long p = 0; p < d; ++p)
+        for (long long j = 0; j < d; ++j) Br[p * d + j] = (*B)[j * d + p];
+      if (int rc = evorl_es_cma_set(s, C->data(), Br.data(), D->data(), ps->data(), pc->data(), sigma, gen, rec))
+        return rc;
+      break;
+    }
+    default: {  // CEM
+      const std::vector<double>* var;
+      int64_t iter = 0;
+      if (int rc = vec("ec/var", d, &var)) return rc;
+      if (int rc = scal_i("ec/iter", &iter)) return rc;
+      CK(cudaMemcpy(s->d_var, var->data(), sizeof(double) * d, cudaMemcpyHostToDevice));
+      s->cem_iter = iter;
+      break;
+    }
+  }
+  if (int rc = evorl_es_set_mean(s, mean->data())) return rc;
+  evorl_obs_norm on{};
+  on.mode = (int32_t)mode;
+  on.dim = mode == 0 ? s->env.obs_dim : (int32_t)nmean->size();
+  for (int k = 0; k < 4; ++k) {
+    on.mean[k] = k < (int)nmean->size() ? (*nmean)[k] : 0.0;
+    on.var[k] = k < (int)nvar->size() ? (*nvar)[k] : 1.0;
+  }
+  on.count = count;
+  if (int rc = evorl_es_set_obs_norm(s, &on)) return rc;
+  s->rng = DKey{(uint64_t)(*key)[0], (uint64_t)(*key)[1]};
+  s->iteration = it;
+  s->env_steps = steps;
+  s->episodes = eps;
+  s->initialised = true;
+  return EVORL_OK;
+}

@@ -15,6 +15,7 @@ All compute runs on the GPU through libevorl_b200.so.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -162,6 +163,16 @@ class EsWorkflow:
         mr, sd = C.c_double(), C.c_double()
         check(self.L.evorl_es_evaluate(self.h, int(episodes), hi, lo, C.byref(mr), C.byref(sd)))
         return mr.value, sd.value
+
+    # checkpoints (Workflow::save / load, EVORL1 format) --------------------
+    def save(self, path) -> None:
+        """Write an EVORL1 checkpoint the reference can load (and vice versa)."""
+        check(self.L.evorl_es_save(self.h, os.fsencode(path)))
+
+    def load(self, path) -> "EsWorkflow":
+        """Restore state from an EVORL1 checkpoint (same config as the writer)."""
+        check(self.L.evorl_es_load(self.h, os.fsencode(path)))
+        return self
 
     @staticmethod
     def _metrics(m) -> StepMetrics:
