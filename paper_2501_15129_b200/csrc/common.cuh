@@ -61,7 +61,7 @@ EVB_HD DKey fold_in(DKey k, uint64_t i) {
 }
 
 // Word #w of RandomStream(k) (proj/src/rng.cpp:54-63).
-EVB_DEV uint64_t stream_word(DKey k, uint64_t w) {
+EVB_HD uint64_t stream_word(DKey k, uint64_t w) {
   uint64_t o0, o1;
   threefry2x64(k.hi, k.lo, 1, w >> 1, o0, o1);
   return (w & 1) ? o1 : o0;

@@ -180,6 +180,12 @@ struct evorl_es {
   // regenerated in every CTA's prologue (null: regenerate, e.g. over the cap)
   float* d_cand_f32 = nullptr;
   int cand_cap = 0;               // agents per materialised chunk (team path)
+  // OpenES noise-table mode (proj/src/ec.cpp:50-86): the shared table and
+  // this generation's window offsets
+  double* d_table = nullptr;
+  long long* d_offsets = nullptr;
+  uint64_t table_seed = 0;
+  std::vector<long long> h_offsets;
   double* d_tell_part = nullptr;  // OpenES tell: per-row-chunk partial contractions
   long long tell_part_cap = 0;
   cudaStream_t stream = nullptr;
@@ -275,7 +281,7 @@ static void free_all(evorl_es* s) {
                   s->d_ep_returns, s->d_lane_stats, s->d_agent_stats, s->d_lane_steps, s->d_rank,
                   s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
                   s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand,
-                  s->d_cand_f32, s->d_tell_part};
+                  s->d_cand_f32, s->d_tell_part, s->d_table, s->d_offsets};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
@@ -301,8 +307,6 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
   if (cfg->algo < 0 || cfg->algo > EVORL_ALGO_CEM) return set_err(EVORL_E_CONFIG, "ec.algo: unknown algorithm");
   if (cfg->env_id != EVORL_ENV_CARTPOLE && cfg->env_id != EVORL_ENV_PENDULUM)
     return set_err(EVORL_E_INVALID_ARGUMENT, "unknown env id");
-  if (cfg->algo == EVORL_ALGO_OPENES && cfg->openes_noise_table)
-    return set_err(EVORL_E_UNSUPPORTED, "openes noise_table mode: device path not built in this revision");
   if (cfg->precision != EVORL_PREC_F64 && cfg->precision != EVORL_PREC_F32 && cfg->precision != EVORL_PREC_TC)
     return set_err(EVORL_E_INVALID_ARGUMENT, "precision must be EVORL_PREC_F64, EVORL_PREC_F32 or EVORL_PREC_TC");
   if (cfg->pop < 1 || cfg->fitness_episodes < 1)
@@ -326,6 +330,12 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
     return rc;
   }
   s->d = s->net.d;
+  const bool table = cfg->algo == EVORL_ALGO_OPENES && cfg->openes_noise_table;
+  if (table && cfg->openes_noise_table_size < s->d) {  // the reference's span = size - d would wrap (UB)
+    delete s;
+    return set_err(EVORL_E_INVALID_ARGUMENT, "openes noise table (%lld entries) smaller than the parameter count (%lld)",
+                   (long long)cfg->openes_noise_table_size, (long long)s->net.d);
+  }
   s->norm_mode = resolve_norm(*cfg);
   s->e = cfg->fitness_episodes;
   s->count = cfg->fitness_episodes;  // RolloutMode::episodes(fitness_episodes)
@@ -385,6 +395,10 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
       getenv("EVORL_CAND_CAP_BYTES") ? atof(getenv("EVORL_CAND_CAP_BYTES")) : 8.0 * (1ull << 30);
   const bool team_mat = !s->warp_path && cfg->algo != EVORL_ALGO_CMAES;
   if (s->warp_path) A(dalloc(&s->d_cand, (size_t)n * d));
+  if (cfg->algo == EVORL_ALGO_OPENES && cfg->openes_noise_table) {
+    A(dalloc(&s->d_table, (size_t)cfg->openes_noise_table_size));
+    A(dalloc(&s->d_offsets, (size_t)n));
+  }
   if (team_mat) {
     const size_t tsz = cfg->precision == EVORL_PREC_F64 ? sizeof(double) : sizeof(float);
     s->cand_cap = (int)std::max(1.0, std::min((double)n, std::floor(kCandCap / ((double)d * tsz))));
@@ -505,6 +519,39 @@ extern "C" int64_t evorl_es_dim(const evorl_es* s) { return s->d; }
 
 static DKey init_key(DKey run, uint64_t i) { return fold_in(fold_in(run, 2), i); }
 
+// key_from_seed (proj/src/rng.cpp:36-41)
+static DKey key_from_seed(uint64_t seed) {
+  DKey k;
+  threefry2x64(0x9E3779B97F4A7C15ull, 0xBB67AE8584CAA73Bull, 0, seed, k.hi, k.lo);
+  return k;
+}
+// openes_rebuild_table (proj/src/ec.cpp:63-69): normals #0.. of
+// RandomStream(key_from_seed(table_seed)), counter-addressed on the device
+static cudaError_t rebuild_table(evorl_es* s) {
+  return run_gaussian_matrix(key_from_seed(s->table_seed), 1, s->cfg.openes_noise_table_size, s->d_table,
+                             s->stream);
+}
+// this generation's window offsets (proj/src/ec.cpp:79-84): RandomStream(ask
+// key).randint(span + 1) per sampled row, with the rejection of
+// proj/src/rng.cpp:89-96 -- sequential, so drawn on the host (base words)
+static cudaError_t table_offsets(evorl_es* s, int base) {
+  const uint64_t nn = (uint64_t)(s->cfg.openes_noise_table_size - s->d) + 1;
+  const uint64_t m = (~0ull % nn + 1) % nn;
+  s->h_offsets.resize(base);
+  uint64_t w = 0;
+  for (int i = 0; i < base; ++i) {
+    for (;;) {
+      const uint64_t x = stream_word(s->ask_key, w++);
+      if (m == 0 || x < 0ull - m) {
+        s->h_offsets[i] = (long long)(x % nn);
+        break;
+      }
+    }
+  }
+  return cudaMemcpyAsync(s->d_offsets, s->h_offsets.data(), sizeof(long long) * base, cudaMemcpyHostToDevice,
+                         s->stream);
+}
+
 // EsWorkflow::init (proj/src/workflow_es.cpp:68-85)
 extern "C" int evorl_es_init(evorl_es* s, uint64_t key_hi, uint64_t key_lo) {
   CK(cudaSetDevice(s->cfg.device));
@@ -514,6 +561,10 @@ extern "C" int evorl_es_init(evorl_es* s, uint64_t key_hi, uint64_t key_lo) {
   s->adam_t_host = 0;
   s->cem_iter = 0;
   CK(run_init_params(s->net, init_key(key, 1), s->d_mean, s->stream));
+  if (s->d_table) {  // OpenEsState::init (proj/src/ec.cpp:50-61) with init_key(key, 2)
+    s->table_seed = fold_in(init_key(key, 2), 0x7ab1e).lo;
+    CK(rebuild_table(s));
+  }
   CK(cudaMemsetAsync(s->d_m, 0, sizeof(double) * s->d, s->stream));
   CK(cudaMemsetAsync(s->d_v, 0, sizeof(double) * s->d, s->stream));
   CK(cudaMemsetAsync(s->d_t, 0, sizeof(long long), s->stream));
@@ -562,10 +613,12 @@ static ParamDesc param_desc(const evorl_es* s) {
   p.ask_key = s->ask_key;
   switch (s->cfg.algo) {
     case EVORL_ALGO_OPENES:
-      p.src = SRC_OPENES;
+      p.src = s->d_table ? SRC_OPENES_TABLE : SRC_OPENES;
       p.sigma = s->cfg.openes_sigma;
       p.mirrored = s->cfg.openes_mirrored;
       p.base = p.mirrored ? s->cfg.pop / 2 : s->cfg.pop;
+      p.table = s->d_table;
+      p.offsets = s->d_offsets;
       break;
     case EVORL_ALGO_VES:
       p.src = SRC_OPENES;
@@ -639,6 +692,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
   s->step_key = fold_in(fold_in(s->rng, 0), (uint64_t)s->iteration);
   s->ask_key = fold_in(s->step_key, 0);      // proj/src/workflow_es.cpp:94
   s->rollout_key = fold_in(s->step_key, 1);  // proj/src/workflow_es.cpp:125
+  if (s->d_table) CK(table_offsets(s, s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop));
   CK(cudaEventRecord(s->ev_s0, s->stream));
   CK(cudaMemsetAsync(s->d_steps, 0, sizeof(unsigned long long), s->stream));
   CK(cudaMemsetAsync(s->d_fault, 0xFF, sizeof(unsigned long long), s->stream));
@@ -754,6 +808,8 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       t.shaped = s->d_shaped;
       t.adam_bc = s->d_adam_bc;
       t.adam_bc_len = s->adam_bc_len;
+      t.table = s->d_table;
+      t.offsets = s->d_offsets;
       {
         const long long need = (long long)openes_tell_chunks(t.base, s->p1 - s->p0) * (s->p1 - s->p0);
         if (need > s->tell_part_cap) {
@@ -1673,7 +1729,7 @@ extern "C" int evorl_es_save(evorl_es* s, const char* path) {
       w.f64("ec/adam/m", m.data(), d);
       w.f64("ec/adam/v", v.data(), d);
       w.i64("ec/adam/t", t);
-      w.i64("ec/table_seed", (int64_t)0);  // noise-table mode is not on the device path
+      w.i64("ec/table_seed", s->d_table ? (int64_t)s->table_seed : (int64_t)0);
       break;
     }
     case EVORL_ALGO_ARS:
@@ -1793,9 +1849,11 @@ extern "C" int evorl_es_load(evorl_es* s, const char* path) {
       if (int rc = vec("ec/adam/v", d, &v)) return rc;
       if (int rc = scal_i("ec/adam/t", &t)) return rc;
       if (int rc = scal_i("ec/table_seed", &seed)) return rc;
-      if (seed != 0 || s->cfg.openes_noise_table)
-        return set_err(EVORL_E_UNSUPPORTED, "openes noise_table mode: device path not built in this revision");
       s->cfg.openes_sigma = sigma;
+      if (s->d_table) {  // openes_rebuild_table (proj/src/workflow_es.cpp:223-224)
+        s->table_seed = (uint64_t)seed;
+        CK(rebuild_table(s));
+      }
       if (int rc = evorl_es_set_adam(s, m->data(), v->data(), t)) return rc;
       break;
     }

@@ -332,7 +332,15 @@ __global__ void __launch_bounds__(TELL_T) k_openes_tell_partial(const OpenEsTell
       wsh[q] = a.mirrored ? dsub(a.shaped[i], a.shaped[i + a.base]) : a.shaped[i];
     }
     __syncthreads();
-    if (pbase < a.p1) {
+    if (pbase < a.p1 && a.table != nullptr) {  // noise-table rows (proj/src/ec.cpp:79-86)
+      for (int q = 0; q < lim; ++q) {
+        const double w = wsh[q];
+        const double* row = a.table + a.offsets[i0 + q] + pbase;
+#pragma unroll
+        for (int v = 0; v < TELL_V; ++v)
+          if (pbase + v < a.p1) acc[v] = fma(row[v], w, acc[v]);
+      }
+    } else if (pbase < a.p1) {
       for (int q = 0; q < lim; ++q) {
         const double w = wsh[q];
         const uint64_t k0 = (uint64_t)((long long)(i0 + q) * a.d + pbase);

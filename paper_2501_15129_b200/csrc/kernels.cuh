@@ -51,6 +51,8 @@ struct OpenEsTellArgs {
   const double* adam_bc;    // [2 * T_max]
   long long adam_bc_len;
   double* partial;          // scratch: openes_tell_chunks(...) x (p1 - p0) doubles
+  const double* table;      // noise-table mode: eps_i[p] = table[offsets[i] + p] (else regenerated)
+  const long long* offsets;
 };
 // Row chunks of the tell's noise contraction for a coordinate span (so the
 // grid fills the GPU; the chunk partials are summed in a fixed order).

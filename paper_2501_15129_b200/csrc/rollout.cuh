@@ -28,7 +28,8 @@ struct NetDesc {
 // Where candidate i's parameters come from.  Only SRC_EXPLICIT reads a stored
 // n x d matrix; the others regenerate the perturbation from the ask key
 // (proj/src/ec.cpp:71-97 OpenES/VES, :113-125 ARS, :306-313 CEM).
-enum : int { SRC_EXPLICIT = 0, SRC_OPENES = 1, SRC_ARS = 2, SRC_CEM = 3, SRC_EXPLICIT_F32 = 4 };
+enum : int { SRC_EXPLICIT = 0, SRC_OPENES = 1, SRC_ARS = 2, SRC_CEM = 3, SRC_EXPLICIT_F32 = 4,
+             SRC_OPENES_TABLE = 5 };
 struct ParamDesc {
   int src;
   const double* params;  // SRC_EXPLICIT: n_agents x d, row-major
@@ -38,6 +39,8 @@ struct ParamDesc {
   double sigma;
   DKey ask_key;
   int base;  // OpenES/VES: number of sampled rows (n/2 when mirrored)
+  const double* table;         // SRC_OPENES_TABLE: the shared noise table
+  const long long* offsets;    // SRC_OPENES_TABLE: window start of each sampled row
   int mirrored;
 };
 
@@ -62,6 +65,17 @@ EVB_DEV double param_value(const ParamDesc& P, long long d, int agent_local, int
         neg = true;
       }
       double eps = normal_at(P.ask_key, (uint64_t)(row * d + p));
+      if (neg) eps = -eps;
+      return dadd(dmul(P.sigma, eps), P.mean[p]);
+    }
+    case SRC_OPENES_TABLE: {  // proj/src/ec.cpp:79-86: row i = table[off_i : off_i + d]
+      long long row = agent;
+      bool neg = false;
+      if (P.mirrored && agent >= P.base) {
+        row = agent - P.base;
+        neg = true;
+      }
+      double eps = P.table[P.offsets[row] + p];
       if (neg) eps = -eps;
       return dadd(dmul(P.sigma, eps), P.mean[p]);
     }

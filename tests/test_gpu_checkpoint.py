@@ -155,3 +155,20 @@ def test_checkpoint_errors(evb, tmp_path):
     ck.write(str(tmp_path / "n.ckpt"), "es", miss)
     with pytest.raises(evb.CheckpointError, match="missing integer segment 'ec/adam/t'"):
         h.load(str(tmp_path / "n.ckpt"))
+
+
+def test_noise_table_checkpoint_resume(evb, tmp_path):
+    """ec/table_seed carries the table across save/load (openes_rebuild_table,
+    proj/src/workflow_es.cpp:223-224): resumed generations are bit-identical."""
+    cfg = dict(CFGS["openes"], openes_noise_table=True, openes_noise_table_size=1 << 16)
+    g = evb.EsWorkflow(evb.EsConfig(**cfg)).init((51, 52))
+    g.step()
+    path = str(tmp_path / "t.ckpt")
+    g.save(path)
+    _, segs = ck.read(path)
+    assert dict((n, a) for n, _, a in segs)["ec/table_seed"][0] != 0
+    g.step()
+    h = evb.EsWorkflow(evb.EsConfig(**cfg)).load(path)
+    h.step()
+    assert np.array_equal(h.fitness(), g.fitness())
+    assert np.array_equal(h.mean(), g.mean())

@@ -478,3 +478,30 @@ def test_chunked_materialised_ask_is_identical(evb):
         outs.append(np.frombuffer(bytes.fromhex(line.split()[1]), dtype=np.float64))
     assert len(outs[0]) == 24
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("mirrored", [True, False])
+def test_openes_noise_table_generations_match_oracle(oracle, evb, mirrored):
+    """OpenES noise-table mode (proj/src/ec.cpp:50-86): the table (normals of
+    key_from_seed(fold_in(init_key(key, 2), 0x7ab1e).lo)) and the per-row
+    randint windows match the oracle; generations track it at the fp64 bar."""
+    common = dict(algo="openes", env="pendulum", fixed_horizon=True, pop=64, hidden=[16, 16],
+                  max_episode_steps=80, vbn_samples=300)
+    o = oracle.OracleEs(oracle.es_config(workers=0, **common, **{
+        "openes.noise_table": 1, "openes.noise_table_size": 65536, "openes.mirrored": int(mirrored)}))
+    g = evb.EsWorkflow(evb.EsConfig(**{k: (tuple(v) if k == "hidden" else v) for k, v in common.items()},
+                                    openes_noise_table=True, openes_noise_table_size=65536,
+                                    openes_mirrored=mirrored))
+    key = oracle.key_from_seed(17)
+    o.init(key)
+    g.init(key)
+    for gen in range(3):
+        o.step()
+        g.step()
+        fo, fg = o.fitness(), g.fitness()
+        assert np.allclose(fg, fo, rtol=RTOL_CLOSED, atol=1e-12), gen
+        assert np.array_equal(np.argsort(fg, kind="stable"), np.argsort(fo, kind="stable"))
+        assert np.allclose(g.mean(), o.mean(), rtol=RTOL_CLOSED, atol=1e-12), gen
+    with pytest.raises(evb.InvalidArgument, match="smaller than the parameter count"):
+        evb.EsWorkflow(evb.EsConfig(algo="openes", hidden=(16, 16), openes_noise_table=True,
+                                    openes_noise_table_size=100))
