@@ -132,6 +132,25 @@ int evorl_batched_rollout(const evorl_env_desc* env, const evorl_mlp_desc* net,
                           int32_t precision, double* returns, int64_t* steps,
                           double* obs_stats);
 
+/* batched_rollout with RolloutOptions::collect_transitions -- the ERL / CEM-RL
+ * population evaluation (proj/src/workflow_erl.cpp:104-110,
+ * proj/src/workflow_cemrl.cpp:176-182; SampleBatch rows of
+ * proj/src/rollout.cpp:132-170).  As evorl_batched_rollout, plus every lane's
+ * transitions in padded per-lane buffers: lane l = a * e + j owns rows
+ * [l * row_cap, l * row_cap + lane_rows[l]) (lane-major concatenation per agent
+ * gives the reference's AgentRollout::batch, lane_bounds = prefix sums of
+ * lane_rows).  row_cap >= ceil(count / e) * max_episode_steps.  t_obs / t_next:
+ * rows x obs_dim (t_next = the successor observation before any auto-reset),
+ * t_act: rows x 1, t_term / t_trunc: 0/1 bytes.  Evaluated by the cluster
+ * team (precision tc evaluates as f32). */
+int evorl_batched_rollout_transitions(const evorl_env_desc* env, const evorl_mlp_desc* net,
+                                      const evorl_obs_norm* norm, const double* params, int32_t m,
+                                      int32_t e, int32_t count, uint64_t key_hi, uint64_t key_lo,
+                                      int32_t precision, double* returns, int64_t* steps,
+                                      int64_t row_cap, double* t_obs, double* t_act,
+                                      double* t_rew, uint8_t* t_term, uint8_t* t_trunc,
+                                      double* t_next, int64_t* lane_rows);
+
 /* -------------------------------------------------------- EC updates
  * replaces openes_tell (proj/src/ec.cpp:99-109) + adam_step
  * (proj/src/optim.cpp:7-17).  The perturbations are NOT passed: they are

@@ -17,6 +17,13 @@ int eo_set_error(int code, const char* fmt, ...);
 void eo_agent_rollout_free(eo_agent_rollout* r) {
   free(r->episode_returns);
   free(r->episode_lengths);
+  free(r->t_obs);
+  free(r->t_act);
+  free(r->t_rew);
+  free(r->t_term);
+  free(r->t_trunc);
+  free(r->t_next);
+  free(r->lane_bounds);
   memset(r, 0, sizeof *r);
 }
 
@@ -68,9 +75,31 @@ static int draw_action(const eo_env_spec* env, const eo_policy* pol, const doubl
 }
 
 /* proj/src/rollout.cpp:94-174 */
+/* append one transition row (growing the lane's SampleBatch arrays) */
+static void push_row(eo_agent_rollout* o, int64_t* cap, const eo_env_spec* env, const double* raw,
+                     const double* a, double r, int term, int trunc, const double* next) {
+  if (o->n_rows == *cap) {
+    *cap = *cap ? *cap * 2 : 64;
+    o->t_obs = (double*)realloc(o->t_obs, sizeof(double) * (size_t)(*cap * env->obs_dim));
+    o->t_act = (double*)realloc(o->t_act, sizeof(double) * (size_t)(*cap * env->act_dim));
+    o->t_rew = (double*)realloc(o->t_rew, sizeof(double) * (size_t)*cap);
+    o->t_term = (uint8_t*)realloc(o->t_term, (size_t)*cap);
+    o->t_trunc = (uint8_t*)realloc(o->t_trunc, (size_t)*cap);
+    o->t_next = (double*)realloc(o->t_next, sizeof(double) * (size_t)(*cap * env->obs_dim));
+  }
+  const int64_t i = o->n_rows++;
+  memcpy(o->t_obs + i * env->obs_dim, raw, sizeof(double) * (size_t)env->obs_dim);
+  memcpy(o->t_act + i * env->act_dim, a, sizeof(double) * (size_t)env->act_dim);
+  o->t_rew[i] = r;
+  o->t_term[i] = (uint8_t)(term ? 1 : 0);
+  o->t_trunc[i] = (uint8_t)(trunc ? 1 : 0);
+  memcpy(o->t_next + i * env->obs_dim, next, sizeof(double) * (size_t)env->obs_dim);
+}
+
 int eo_rollout_lane(const eo_env_spec* env, const eo_policy* pol, const double* params, int mode,
                     int count, int episodes_this_lane, eo_key lane_key, int track_obs_stats,
-                    eo_agent_rollout* out) {
+                    int collect_transitions, eo_agent_rollout* out) {
+  int64_t rcap = 0;
   memset(out, 0, sizeof *out);
   const int by_episodes = mode == EO_MODE_EPISODES;
   if (by_episodes && episodes_this_lane <= 0) return EO_OK;
@@ -90,8 +119,10 @@ int eo_rollout_lane(const eo_env_spec* env, const eo_policy* pol, const double* 
     if (rc != EO_OK) return rc;
     double reward;
     int term, trunc;
-    rc = eo_env_step_autoreset(env, &state, a, &reward, &term, &trunc, obs, NULL);
+    double final_obs[4];
+    rc = eo_env_step_autoreset(env, &state, a, &reward, &term, &trunc, obs, final_obs);
     if (rc != EO_OK) return rc;
+    if (collect_transitions) push_row(out, &rcap, env, raw, a, reward, term, trunc, final_obs);
     ep_return += reward;
     ep_len += 1;
     out->steps += 1;
@@ -112,7 +143,7 @@ typedef struct {
   const eo_env_spec* env;
   const eo_policy* pol;
   const double* const* agents;
-  int e, mode, count, track;
+  int e, mode, count, track, collect;
   eo_key key;
   eo_agent_rollout* lanes;
   int* rcs;
@@ -128,7 +159,7 @@ static void run_lane(lane_job* J, size_t li) {
   if (J->mode == EO_MODE_EPISODES)
     eps_this = J->count / J->e + ((int)j < J->count % J->e ? 1 : 0);
   J->rcs[li] = eo_rollout_lane(J->env, J->pol, J->agents[a], J->mode, J->count, eps_this, lane_key,
-                               J->track, &J->lanes[li]);
+                               J->track, J->collect, &J->lanes[li]);
   if (J->rcs[li] != EO_OK) strncpy(J->msgs[li], eo_last_error(), 511);
 }
 
@@ -154,6 +185,12 @@ static int resolve_workers(int workers) {
 int eo_batched_rollout(int workers, const eo_env_spec* env, const eo_policy* pol,
                        const double* const* agents, int m, int e, int mode, int count, eo_key key,
                        int track_obs_stats, eo_agent_rollout* out) {
+  return eo_batched_rollout_ex(workers, env, pol, agents, m, e, mode, count, key, track_obs_stats, 0, out);
+}
+
+int eo_batched_rollout_ex(int workers, const eo_env_spec* env, const eo_policy* pol,
+                          const double* const* agents, int m, int e, int mode, int count, eo_key key,
+                          int track_obs_stats, int collect_transitions, eo_agent_rollout* out) {
   const size_t n = (size_t)m * (size_t)e;
   lane_job J;
   memset(&J, 0, sizeof J);
@@ -164,6 +201,7 @@ int eo_batched_rollout(int workers, const eo_env_spec* env, const eo_policy* pol
   J.mode = mode;
   J.count = count;
   J.track = track_obs_stats;
+  J.collect = collect_transitions;
   J.key = key;
   J.n = n;
   J.lanes = (eo_agent_rollout*)calloc(n ? n : 1, sizeof(eo_agent_rollout));
@@ -198,6 +236,22 @@ int eo_batched_rollout(int workers, const eo_env_spec* env, const eo_policy* pol
         agg->steps += lane->steps;
         eo_welford_merge(&agg->obs_stats, &lane->obs_stats);
       }
+      if (collect_transitions) {  /* lane-major concatenation + lane bounds */
+        int64_t rows = 0;
+        agg->lane_bounds = (int64_t*)calloc((size_t)e + 1, sizeof(int64_t));
+        for (int j = 0; j < e; ++j) {
+          agg->lane_bounds[j] = rows;
+          rows += J.lanes[(size_t)a * e + j].n_rows;
+        }
+        agg->lane_bounds[e] = rows;
+        int64_t cap = 0;
+        for (int j = 0; j < e; ++j) {
+          const eo_agent_rollout* L = &J.lanes[(size_t)a * e + j];
+          for (int64_t i = 0; i < L->n_rows; ++i)
+            push_row(agg, &cap, env, L->t_obs + i * env->obs_dim, L->t_act + i * env->act_dim, L->t_rew[i],
+                     L->t_term[i], L->t_trunc[i], L->t_next + i * env->obs_dim);
+        }
+      }
     }
   }
   for (size_t i = 0; i < n; ++i) eo_agent_rollout_free(&J.lanes[i]);
@@ -213,7 +267,7 @@ eo_obs_norm eo_vbn_fit(const eo_env_spec* env, eo_key key, int n) {
   memset(&pol, 0, sizeof pol);
   pol.mode = EO_ACT_UNIFORM;
   eo_agent_rollout r;
-  eo_rollout_lane(env, &pol, NULL, EO_MODE_STEPS, n, 0, key, 1, &r);
+  eo_rollout_lane(env, &pol, NULL, EO_MODE_STEPS, n, 0, key, 1, 0, &r);
   eo_obs_norm s = eo_obs_norm_from_stats(EO_NORM_VBN, &r.obs_stats);
   eo_agent_rollout_free(&r);
   return s;

@@ -283,6 +283,17 @@ typedef struct {
   double* episode_returns; /* malloc'd, n_episodes */
   int* episode_lengths;
   eo_welford obs_stats;
+  /* SampleBatch when collecting transitions (proj/include/evorl/sample_batch.hpp,
+   * proj/src/rollout.cpp:118-170): rows lane-major; next_obs is the true
+   * successor (final_obs) even across auto-resets; lane_bounds[e + 1] */
+  int64_t n_rows;
+  double* t_obs;      /* n_rows x obs_dim */
+  double* t_act;      /* n_rows x act_dim */
+  double* t_rew;      /* n_rows */
+  uint8_t* t_term;    /* n_rows */
+  uint8_t* t_trunc;   /* n_rows */
+  double* t_next;     /* n_rows x obs_dim */
+  int64_t* lane_bounds; /* e + 1 (batched results only) */
 } eo_agent_rollout;
 void eo_agent_rollout_free(eo_agent_rollout* r);
 
@@ -290,11 +301,16 @@ void eo_agent_rollout_free(eo_agent_rollout* r);
 enum { EO_MODE_EPISODES = 0, EO_MODE_STEPS = 1 };
 int eo_rollout_lane(const eo_env_spec* env, const eo_policy* pol, const double* params,
                     int mode, int count, int episodes_this_lane, eo_key lane_key,
-                    int track_obs_stats, eo_agent_rollout* out);
+                    int track_obs_stats, int collect_transitions, eo_agent_rollout* out);
 /* agents: m pointers to d-vectors; out: m results.  workers: 0 = all cores. */
 int eo_batched_rollout(int workers, const eo_env_spec* env, const eo_policy* pol,
                        const double* const* agents, int m, int envs_per_agent, int mode,
                        int count, eo_key key, int track_obs_stats, eo_agent_rollout* out);
+/* RolloutOptions::collect_transitions = 1 */
+int eo_batched_rollout_ex(int workers, const eo_env_spec* env, const eo_policy* pol,
+                          const double* const* agents, int m, int envs_per_agent, int mode,
+                          int count, eo_key key, int track_obs_stats, int collect_transitions,
+                          eo_agent_rollout* out);
 eo_obs_norm eo_vbn_fit(const eo_env_spec* env, eo_key key, int n);
 
 /* ------------------------------------------------------- ES workflow

@@ -125,7 +125,11 @@ class Policy(C.Structure):
 class AgentRollout(C.Structure):
     _fields_ = [("steps", C.c_int64), ("n_episodes", C.c_int),
                 ("episode_returns", C.POINTER(C.c_double)),
-                ("episode_lengths", C.POINTER(C.c_int)), ("obs_stats", Welford)]
+                ("episode_lengths", C.POINTER(C.c_int)), ("obs_stats", Welford),
+                ("n_rows", C.c_int64), ("t_obs", C.POINTER(C.c_double)),
+                ("t_act", C.POINTER(C.c_double)), ("t_rew", C.POINTER(C.c_double)),
+                ("t_term", C.POINTER(C.c_uint8)), ("t_trunc", C.POINTER(C.c_uint8)),
+                ("t_next", C.POINTER(C.c_double)), ("lane_bounds", C.POINTER(C.c_int64))]
 
 
 class EsConfig(C.Structure):
@@ -207,7 +211,10 @@ def lib() -> C.CDLL:
         L.eo_cma_init.argtypes = [C.POINTER(CmaState), C.POINTER(CmaCfg), C.c_void_p, C.c_int64]
         L.eo_cma_ask.argtypes = [C.POINTER(CmaState), Key, C.c_int, C.c_void_p]
         L.eo_rollout_lane.argtypes = [C.POINTER(EnvSpec), C.POINTER(Policy), C.c_void_p, C.c_int,
-                                      C.c_int, C.c_int, Key, C.c_int, C.POINTER(AgentRollout)]
+                                      C.c_int, C.c_int, Key, C.c_int, C.c_int, C.POINTER(AgentRollout)]
+        L.eo_batched_rollout_ex.argtypes = [C.c_int, C.POINTER(EnvSpec), C.POINTER(Policy), C.c_void_p,
+                                            C.c_int, C.c_int, C.c_int, C.c_int, Key, C.c_int, C.c_int,
+                                            C.POINTER(AgentRollout)]
         L.eo_batched_rollout.argtypes = [C.c_int, C.POINTER(EnvSpec), C.POINTER(Policy),
                                          C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, Key,
                                          C.c_int, C.POINTER(AgentRollout)]
@@ -463,8 +470,10 @@ class OracleEs:
 
 
 def batched_rollout(env: EnvSpec, spec: MlpSpec, obs_norm, params: np.ndarray, e: int,
-                    key: Key, count=None, track=False, workers=1):
-    """Returns (returns list per agent, steps per agent, obs_stats per agent)."""
+                    key: Key, count=None, track=False, workers=1, collect=False):
+    """Returns (returns list per agent, steps per agent, obs_stats per agent) and,
+    with collect=True, a 4th item: per agent a dict SampleBatch (obs, actions,
+    rewards, terminated, truncated, next_obs, lane_bounds)."""
     m = params.shape[0]
     params = np.ascontiguousarray(params, np.float64)
     ptrs = (C.c_void_p * m)(*[params.ctypes.data + i * params.strides[0] for i in range(m)])
@@ -474,13 +483,25 @@ def batched_rollout(env: EnvSpec, spec: MlpSpec, obs_norm, params: np.ndarray, e
     pol.mode = EO_ACT_DETERMINISTIC
     out = (AgentRollout * m)()
     count = e if count is None else count
-    check(lib().eo_batched_rollout(workers, C.byref(env), C.byref(pol), ptrs, m, e,
-                                   EO_MODE_EPISODES, count, key, int(track), out))
-    rets, steps, stats = [], [], []
+    check(lib().eo_batched_rollout_ex(workers, C.byref(env), C.byref(pol), ptrs, m, e,
+                                      EO_MODE_EPISODES, count, key, int(track), int(collect), out))
+    rets, steps, stats, batches = [], [], [], []
+    od, ad = env.obs_dim, env.act_dim
     for a in range(m):
         r = out[a]
         rets.append(np.array([r.episode_returns[i] for i in range(r.n_episodes)]))
         steps.append(r.steps)
         stats.append((r.obs_stats.count, list(r.obs_stats.mean), list(r.obs_stats.m2)))
+        if collect:
+            n = r.n_rows
+
+            def arr(ptr, k, dt=np.float64):
+                return np.ctypeslib.as_array(ptr, shape=(max(k, 1),))[:k].astype(dt) if k else np.zeros(0, dt)
+            batches.append(dict(obs=arr(r.t_obs, n * od).reshape(n, od), actions=arr(r.t_act, n * ad).reshape(n, ad),
+                                rewards=arr(r.t_rew, n), terminated=arr(r.t_term, n, np.uint8),
+                                truncated=arr(r.t_trunc, n, np.uint8), next_obs=arr(r.t_next, n * od).reshape(n, od),
+                                lane_bounds=arr(r.lane_bounds, e + 1, np.int64)))
         lib().eo_agent_rollout_free(C.byref(r))
+    if collect:
+        return rets, steps, stats, batches
     return rets, steps, stats

@@ -134,7 +134,7 @@ EXPORTS = [
     "evorl_es_shard_ranges", "evorl_es_phase_rollout", "evorl_es_phase_tell",
     "evorl_es_device_buffers", "evorl_es_stream", "evorl_es_last_timings",
     "evorl_measure_fp64_peak", "evorl_measure_dmma_peak", "evorl_es_cma_get", "evorl_es_cma_set",
-    "evorl_sym_eig", "evorl_es_save", "evorl_es_load",
+    "evorl_sym_eig", "evorl_es_save", "evorl_es_load", "evorl_batched_rollout_transitions",
 ]
 
 _lib = None
@@ -162,6 +162,9 @@ def load() -> C.CDLL:
     L.evorl_batched_rollout.argtypes = [C.POINTER(EnvDescC), C.POINTER(MlpDesc),
                                         C.POINTER(ObsNormC), vp, i32, i32, i32, u64, u64, i32,
                                         vp, vp, vp]
+    L.evorl_batched_rollout_transitions.argtypes = [C.POINTER(EnvDescC), C.POINTER(MlpDesc),
+                                                    C.POINTER(ObsNormC), vp, i32, i32, i32, u64, u64,
+                                                    i32, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]
     L.evorl_openes_tell.argtypes = [vp, vp, vp, C.POINTER(i64), i64, dbl, dbl, dbl, i32, u64,
                                     u64, vp, i32]
     L.evorl_openes_ask.argtypes = [vp, i64, dbl, i32, u64, u64, i32, vp, vp]

@@ -1292,10 +1292,18 @@ extern "C" int evorl_env_step_batch(int env_id, int fixed_horizon, int max_episo
   return EVORL_OK;
 }
 
-extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp_desc* netd,
-                                     const evorl_obs_norm* norm, const double* params, int32_t m, int32_t e,
-                                     int32_t count, uint64_t key_hi, uint64_t key_lo, int32_t precision,
-                                     double* returns, int64_t* steps, double* obs_stats) {
+// transition outputs of evorl_batched_rollout_transitions (host pointers)
+struct TransHost {
+  long long row_cap;
+  double *obs, *act, *rew, *next;
+  uint8_t *term, *trunc;
+  int64_t* lane_rows;
+};
+
+static int batched_rollout_impl(const evorl_env_desc* envd, const evorl_mlp_desc* netd,
+                                const evorl_obs_norm* norm, const double* params, int32_t m, int32_t e,
+                                int32_t count, uint64_t key_hi, uint64_t key_lo, int32_t precision,
+                                double* returns, int64_t* steps, double* obs_stats, const TransHost* tr) {
   DEV_OR_RETURN();
   if (m <= 0) return EVORL_OK;
   if (e < 1 || count < 0) return set_err(EVORL_E_INVALID_ARGUMENT, "envs_per_agent must be positive");
@@ -1307,11 +1315,18 @@ extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp
   WarpPlanOut wplan{};
   if (precision < EVORL_PREC_F64 || precision > EVORL_PREC_TC)
     return set_err(EVORL_E_INVALID_ARGUMENT, "unknown precision");
-  const bool cta_ok = plan_rollout(net, env.obs_dim, e, precision, &plan);
-  const bool use_warp = !(cta_ok && plan.tc) && plan_rollout_warp(net, env.obs_dim, e, precision, &wplan);
+  // transitions are written by the cluster team (the tc team evaluates as f32)
+  const bool cta_ok = plan_rollout(net, env.obs_dim, e, tr && precision == EVORL_PREC_TC ? EVORL_PREC_F32 : precision,
+                                   &plan);
+  const bool use_warp =
+      !tr && !(cta_ok && plan.tc) && plan_rollout_warp(net, env.obs_dim, e, precision, &wplan);
   if (!cta_ok && !use_warp)
     return set_err(EVORL_E_UNSUPPORTED, "policy too large for a shared-memory resident team");
   const long long d = net.d;
+  const long long max_iters = (long long)((count + e - 1) / e) * env.max_episode_steps;
+  if (tr && tr->row_cap < max_iters)
+    return set_err(EVORL_E_INVALID_ARGUMENT, "row_cap (%lld) below episodes per lane x max_episode_steps (%lld)",
+                   tr->row_cap, max_iters);
   Scratch sp, sr, ss, sst, sag, sn, sf;
   double *dparams, *drets, *dstats, *dagent;
   long long* dsteps;
@@ -1354,6 +1369,17 @@ extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp
   a.lane_steps = dsteps;
   a.lane_stats = dstats;
   a.fault = dfault;
+  Scratch st_o, st_a, st_r, st_n, st_t, st_u;
+  if (tr) {
+    const size_t rows = (size_t)m * e * tr->row_cap;
+    if (int rc = up(st_o, (const double*)nullptr, rows * env.obs_dim, &a.t_obs)) return rc;
+    if (int rc = up(st_n, (const double*)nullptr, rows * env.obs_dim, &a.t_next)) return rc;
+    if (int rc = up(st_a, (const double*)nullptr, rows, &a.t_act)) return rc;
+    if (int rc = up(st_r, (const double*)nullptr, rows, &a.t_rew)) return rc;
+    if (int rc = up(st_t, (const unsigned char*)nullptr, rows, &a.t_term)) return rc;
+    if (int rc = up(st_u, (const unsigned char*)nullptr, rows, &a.t_trunc)) return rc;
+    a.t_cap = tr->row_cap;
+  }
   Scratch sf32;
   if (!use_warp && plan.gw && precision != EVORL_PREC_F64) {  // global-weights fp32 team reads fp32 rows
     float* pf = nullptr;
@@ -1384,7 +1410,37 @@ extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp
     }
   }
   if (obs_stats) CK(cudaMemcpy(obs_stats, dagent, sizeof(double) * m * 9, cudaMemcpyDeviceToHost));
+  if (tr) {
+    const size_t rows = (size_t)m * e * tr->row_cap;
+    CK(cudaMemcpy(tr->obs, a.t_obs, sizeof(double) * rows * env.obs_dim, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tr->next, a.t_next, sizeof(double) * rows * env.obs_dim, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tr->act, a.t_act, sizeof(double) * rows, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tr->rew, a.t_rew, sizeof(double) * rows, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tr->term, a.t_term, rows, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tr->trunc, a.t_trunc, rows, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tr->lane_rows, dsteps, sizeof(long long) * m * e, cudaMemcpyDeviceToHost));
+  }
   return EVORL_OK;
+}
+
+extern "C" int evorl_batched_rollout(const evorl_env_desc* envd, const evorl_mlp_desc* netd,
+                                     const evorl_obs_norm* norm, const double* params, int32_t m, int32_t e,
+                                     int32_t count, uint64_t key_hi, uint64_t key_lo, int32_t precision,
+                                     double* returns, int64_t* steps, double* obs_stats) {
+  return batched_rollout_impl(envd, netd, norm, params, m, e, count, key_hi, key_lo, precision, returns, steps,
+                              obs_stats, nullptr);
+}
+
+extern "C" int evorl_batched_rollout_transitions(const evorl_env_desc* envd, const evorl_mlp_desc* netd,
+                                                 const evorl_obs_norm* norm, const double* params, int32_t m,
+                                                 int32_t e, int32_t count, uint64_t key_hi, uint64_t key_lo,
+                                                 int32_t precision, double* returns, int64_t* steps,
+                                                 int64_t row_cap, double* t_obs, double* t_act, double* t_rew,
+                                                 uint8_t* t_term, uint8_t* t_trunc, double* t_next,
+                                                 int64_t* lane_rows) {
+  const TransHost tr{row_cap, t_obs, t_act, t_rew, t_next, t_term, t_trunc, lane_rows};
+  return batched_rollout_impl(envd, netd, norm, params, m, e, count, key_hi, key_lo, precision, returns, steps,
+                              nullptr, &tr);
 }
 
 extern "C" int evorl_openes_ask(const double* mean, int64_t d, double sigma, int32_t mirrored, uint64_t hi,

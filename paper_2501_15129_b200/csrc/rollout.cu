@@ -496,10 +496,12 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   // observation -> (RunningStats) -> normalisation, written into x0 for the
   // next forward pass (proj/src/rollout.cpp:124-126)
   double sin_th = 0.0;  // sin of the current pendulum angle (reused by env_step)
+  double cur_raw[4] = {0, 0, 0, 0};  // raw observation of the current state (transitions)
   auto observe_into_x0 = [&](bool act) {
     double raw[4];
     observe(E, s, raw);
     sin_th = raw[1];
+    for (int i = 0; i < 4; ++i) cur_raw[i] = raw[i];
     if (act && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
       if (wc == 0.0) {
         for (int i = 0; i < E.obs_dim; ++i) {
@@ -699,6 +701,19 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
         bool term = false, trunc = false;
         const uint32_t f =
             env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr);
+        if (!f && A.t_obs != nullptr && crank == 0) {  // one SampleBatch row (rollout.cpp:132-139)
+          double nxt[4];
+          observe(E, s, nxt);  // final_obs: the successor before any auto-reset
+          const long long row = ((long long)agent_local * A.e + j) * A.t_cap + steps;
+          for (int i = 0; i < E.obs_dim; ++i) {
+            A.t_obs[row * E.obs_dim + i] = cur_raw[i];
+            A.t_next[row * E.obs_dim + i] = nxt[i];
+          }
+          A.t_act[row] = action;
+          A.t_rew[row] = reward;
+          A.t_term[row] = term ? 1 : 0;
+          A.t_trunc[row] = trunc ? 1 : 0;
+        }
         if (f) {
           myfault = f;
         } else {

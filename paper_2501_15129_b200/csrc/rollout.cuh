@@ -139,6 +139,16 @@ struct RolloutArgs {
   long long* lane_steps;   // [n_agents * e]
   double* lane_stats;      // [n_agents * e][9] = count, mean[4], m2[4]
   unsigned long long* fault;
+  // RolloutOptions::collect_transitions (proj/src/rollout.cpp:118-170), cluster
+  // team only: lane l's rows at [l * t_cap, l * t_cap + lane_steps[l]) with
+  // l = agent_local * e + j; null = not collected
+  double* t_obs;      // rows x obs_dim (raw observation)
+  double* t_act;      // rows x 1 (act_dim of both envs)
+  double* t_rew;
+  unsigned char* t_term;
+  unsigned char* t_trunc;
+  double* t_next;     // rows x obs_dim (final_obs: successor before auto-reset)
+  long long t_cap;
 };
 
 // Host-side: launch the rollout with the plan's template instance.

@@ -407,9 +407,16 @@ def env_step_batch(env: str, phys, step_count, action, fixed_horizon=False,
 
 def batched_rollout(env: str, net: _lib.MlpDesc, params, envs_per_agent: int, key,
                     count: Optional[int] = None, obs_norm=None, fixed_horizon=False,
-                    max_episode_steps=0, precision="f64", track_obs_stats=False):
+                    max_episode_steps=0, precision="f64", track_obs_stats=False,
+                    collect_transitions=False):
     """proj/src/rollout.cpp:176-214 (Episodes mode, deterministic policy).
-    Returns (returns m x count, steps m, obs_stats m x 9 or None)."""
+    Returns (returns m x count, steps m, obs_stats m x 9 or None); with
+    collect_transitions=True instead (returns, steps, batches): per agent the
+    reference's AgentRollout::batch as a dict (obs, actions, rewards,
+    terminated, truncated, next_obs, lane_bounds), lanes concatenated in order."""
+    if collect_transitions:
+        return _batched_rollout_transitions(env, net, params, envs_per_agent, key, count, obs_norm,
+                                            fixed_horizon, max_episode_steps, precision)
     params = np.ascontiguousarray(params, np.float64)
     m = params.shape[0]
     e = int(envs_per_agent)
@@ -433,6 +440,50 @@ def batched_rollout(env: str, net: _lib.MlpDesc, params, envs_per_agent: int, ke
         count, hi, lo, _lib.PRECISIONS[precision], _p(rets),
         _p(steps), _p(stats) if stats is not None else None))
     return rets, steps, stats
+
+
+def _norm_c(obs_norm):
+    if obs_norm is None:
+        return None
+    nc = _lib.ObsNormC()
+    for k in ("mode", "dim", "count"):
+        setattr(nc, k, getattr(obs_norm, k))
+    for i in range(4):
+        nc.mean[i] = obs_norm.mean[i]
+        nc.var[i] = obs_norm.var[i]
+    return nc
+
+
+def _batched_rollout_transitions(env, net, params, envs_per_agent, key, count, obs_norm, fixed_horizon,
+                                 max_episode_steps, precision):
+    params = np.ascontiguousarray(params, np.float64)
+    m, e = params.shape[0], int(envs_per_agent)
+    count = e if count is None else int(count)
+    ed = _lib.EnvDescC(_lib.ENV_CARTPOLE if env == "cartpole" else _lib.ENV_PENDULUM,
+                       int(fixed_horizon), int(max_episode_steps))
+    od = 4 if env == "cartpole" else 3
+    H = int(max_episode_steps) if max_episode_steps else (500 if env == "cartpole" else 200)
+    cap = -(-count // e) * H
+    rows = m * e * cap
+    nc = _norm_c(obs_norm)
+    hi, lo = _key(key)
+    rets, steps = np.empty((m, count)), np.empty(m, np.int64)
+    obs, nxt = np.empty((rows, od)), np.empty((rows, od))
+    act, rew = np.empty(rows), np.empty(rows)
+    term, trunc = np.empty(rows, np.uint8), np.empty(rows, np.uint8)
+    lane_rows = np.empty(m * e, np.int64)
+    check(_lib.load().evorl_batched_rollout_transitions(
+        C.byref(ed), C.byref(net), C.byref(nc) if nc is not None else None, _p(params), m, e, count,
+        hi, lo, _lib.PRECISIONS[precision], _p(rets), _p(steps), cap, _p(obs), _p(act), _p(rew),
+        _p(term), _p(trunc), _p(nxt), _p(lane_rows)))
+    batches = []
+    for a in range(m):
+        sel = np.concatenate([np.arange(l * cap, l * cap + lane_rows[l]) for l in range(a * e, (a + 1) * e)])
+        bounds = np.concatenate([[0], np.cumsum(lane_rows[a * e:(a + 1) * e])])
+        batches.append(dict(obs=obs[sel], actions=act[sel].reshape(-1, 1), rewards=rew[sel],
+                            terminated=term[sel], truncated=trunc[sel], next_obs=nxt[sel],
+                            lane_bounds=bounds))
+    return rets, steps, batches
 
 
 def sym_eig(A):

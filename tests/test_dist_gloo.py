@@ -74,7 +74,7 @@ class OracleShardBackend:
             for j in range(self.e):
                 out = o.AgentRollout()
                 o.check(self.L.eo_rollout_lane(C.byref(env), C.byref(pol), o.ptr(p), 0, self.e, 1,
-                                               o.fold_in(o.fold_in(rk, a), j), 0, C.byref(out)))
+                                               o.fold_in(o.fold_in(rk, a), j), 0, 0, C.byref(out)))
                 s += out.episode_returns[0]
                 self.L.eo_agent_rollout_free(C.byref(out))
             fit[a - a0] = s / self.e

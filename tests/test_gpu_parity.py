@@ -505,3 +505,33 @@ def test_openes_noise_table_generations_match_oracle(oracle, evb, mirrored):
     with pytest.raises(evb.InvalidArgument, match="smaller than the parameter count"):
         evb.EsWorkflow(evb.EsConfig(algo="openes", hidden=(16, 16), openes_noise_table=True,
                                     openes_noise_table_size=100))
+
+
+@pytest.mark.parametrize("env,hidden,m,e,count,H,fixed", [
+    ("cartpole", [16], 4, 6, 6, 60, False),      # ERL / CEM-RL: 1 episode per lane, early terminations
+    ("pendulum", [64, 64], 3, 4, 8, 50, True),   # 2 episodes per lane, auto-reset inside the lane
+])
+def test_transitions_match_oracle(oracle, evb, env, hidden, m, e, count, H, fixed):
+    """collect_transitions (§8(f) row 4; proj/src/rollout.cpp:118-170): the
+    per-agent SampleBatch (lane-major rows, lane_bounds, next_obs = successor
+    before auto-reset) matches the oracle: rows and flags exactly, values at
+    the fp64 closed-loop bar."""
+    ospec, desc = _policy(oracle, evb, env, hidden)
+    params = np.array([oracle.init_params(ospec, oracle.key_from_seed(90 + a)) for a in range(m)])
+    params += 0.1 * np.random.default_rng(9).standard_normal(params.shape)
+    key = oracle.key_from_seed(91)
+    envspec = oracle.env_spec(env, fixed, H)
+    want_r, want_s, _, want_b = oracle.batched_rollout(envspec, ospec, None, params, e, key, count=count,
+                                                       workers=0, collect=True)
+    got_r, got_s, got_b = evb.batched_rollout(env, desc, params, e, key, count=count, fixed_horizon=fixed,
+                                              max_episode_steps=H, collect_transitions=True)
+    assert list(got_s) == list(want_s)
+    for a in range(m):
+        g, w = got_b[a], want_b[a]
+        assert np.array_equal(g["lane_bounds"], w["lane_bounds"])
+        assert np.array_equal(g["terminated"], w["terminated"]) and np.array_equal(g["truncated"], w["truncated"])
+        assert np.array_equal(g["actions"], w["actions"]) if env == "cartpole" else \
+            np.allclose(g["actions"], w["actions"], rtol=RTOL_CLOSED, atol=1e-12)
+        for k in ("obs", "next_obs", "rewards"):
+            assert np.allclose(g[k], w[k], rtol=RTOL_CLOSED, atol=1e-12), k
+        assert np.allclose(got_r[a], want_r[a], rtol=RTOL_CLOSED, atol=1e-12)

@@ -31,7 +31,7 @@ def test_grid_equals_solo_lanes_and_worker_invariance(oracle):
         for j in range(4):
             out = oracle.AgentRollout()
             oracle.check(L.eo_rollout_lane(C.byref(env), C.byref(pol), oracle.ptr(params[a]), 0, 1, 1,
-                                           oracle.fold_in(oracle.fold_in(key, a), j), 0,
+                                           oracle.fold_in(oracle.fold_in(key, a), j), 0, 0,
                                            C.byref(out)))
             solo.append(out.episode_returns[0])
             L.eo_agent_rollout_free(C.byref(out))
@@ -94,3 +94,29 @@ def test_openes_pendulum_improves(oracle):
     assert last > first
     it, steps, eps = es.counters()
     assert it == 30 and steps == 30 * 64 * 100 and eps == 30 * 64
+
+
+def test_oracle_transitions_follow_reference_semantics(oracle):
+    """collect_transitions (proj/src/rollout.cpp:118-170): one row per step,
+    lane-major per agent with lane_bounds; next_obs = final_obs (the true
+    successor even across auto-reset), so next_obs[i] == obs[i+1] inside an
+    episode; rewards of an episode sum to its return; flags close episodes."""
+    env = oracle.env_spec("cartpole", False, 40)
+    spec = oracle.policy_net_spec(env, [8])
+    m, e, count = 3, 2, 4  # 2 episodes per lane
+    params = np.array([oracle.init_params(spec, oracle.key_from_seed(70 + a)) for a in range(m)])
+    rets, steps, _, batches = oracle.batched_rollout(env, spec, None, params, e, oracle.key_from_seed(71),
+                                                     count=count, workers=0, collect=True)
+    for a in range(m):
+        b = batches[a]
+        n = len(b["rewards"])
+        assert n == steps[a] and b["lane_bounds"][0] == 0 and b["lane_bounds"][-1] == n
+        ends = np.flatnonzero(b["terminated"] | b["truncated"])
+        assert len(ends) == count
+        assert set(b["lane_bounds"][1:] - 1) <= set(ends)
+        start = 0
+        for k, end in enumerate(ends):
+            assert abs(b["rewards"][start:end + 1].sum() - rets[a][k]) < 1e-9
+            assert np.array_equal(b["next_obs"][start:end], b["obs"][start + 1:end + 1])
+            start = end + 1
+        assert b["actions"].shape == (n, 1) and set(np.unique(b["actions"])) <= {0.0, 1.0}
