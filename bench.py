@@ -71,7 +71,7 @@ def cma_lazy_gap(d, mu, pop):
 # `ncu --set full` capture of the same command (profiles/README.md)
 NCU_TRAFFIC = {
     ("3", "f64"): (2230139136 + 68040960, "ncu r01_f64_v6: rollout_kernel<double,1,16,4,1>"),
-    ("3", "tc"): (1104589568 + 10959616, "ncu r01_tc_v3: rollout_tc_kernel<2>"),
+    ("3", "tc"): (1104370432 + 10082304, "ncu r01_tc_v5: rollout_tc_kernel<2> (cta_group::2 pair)"),
 }
 
 
