@@ -45,7 +45,6 @@ constexpr float TC_LO_SCALE = 2048.0f;
 constexpr int TC_RANGE_ROW = 8;  // bad-layer row value: operand out of the split's range
 constexpr int TC_OK_ROW = 15;    // bad-layer row value: no fault
 constexpr int TC_MAXO = 8;
-constexpr int TC_MAX_ROUNDS = 4;  // layer-0 / MMA pipeline rounds of 8 k-steps: W1 <= 512
 
 #ifdef EVB_TC_PROFILE
 // Phase cycle counters (profiling build only, libevorl_b200_prof.so): thread 0
@@ -86,19 +85,6 @@ EVB_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
 // kind::f16 instruction descriptor: A = B = f16 (K-major), D = f32
 constexpr uint32_t tc_idesc(int M, int N) {
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-EVB_DEV void tc_mma_ss(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-}
-EVB_DEV void tc_mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
-      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
 // whole-warp variants: one elected lane issues (the operands are warp-uniform)
@@ -191,8 +177,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   for (int i = tid; i < P.bytes / 4; i += TC_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
-  uint64_t* l0bar = mbar + 1;  // [TC_MAX_ROUNDS]: layer-0 rounds stored
-  uint64_t* xbar = l0bar + TC_MAX_ROUNDS;  // [2]: partial outputs of every cluster CTA landed
+  uint64_t* l0bar = mbar + 1;  // layer-0 B rows stored (this CTA's warps, and the odd peer's on a pair)
+  uint64_t* xbar = mbar + 2;   // [2]: partial outputs of every cluster CTA landed
   __syncthreads();
   if (warp == 0) {
     if constexpr (PAIR) {  // both CTAs of the pair: same columns in each TMEM
@@ -207,9 +193,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   }
   if (tid == 0) {
     mbar_init(mbar, 1);
-    // layer-0 round rd stored: every warp of this CTA (and, on a pair's even
-    // CTA, of its odd peer) arrives once per step
-    for (int i = 0; i < TC_MAX_ROUNDS; ++i) mbar_init(&l0bar[i], (PAIR ? 2 : 1) * (TC_THREADS / 32));
+    // layer-0 rows stored: every warp of this CTA (and, on a pair's even CTA,
+    // of its odd peer) arrives once per step
+    mbar_init(l0bar, (PAIR ? 2 : 1) * (TC_THREADS / 32));
     mbar_init(&xbar[0], 1);  // output exchange, double-buffered by step parity
     mbar_init(&xbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -350,89 +336,83 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
       for (int eh = 0; eh < EH; ++eh)
 #pragma unroll
         for (int k = 0; k < 4; ++k) xr[eh][k] = k < K0 ? x0[k * TC_N + (eh + pv) * 8 + el] : 0.0f;
-      // one round: (pipelining layer 0 against the MMAs in rounds of 8 k-steps
-      // measured slower -- the pair's tensor pipe is shared with the SM's
-      // other team, so the MMAs do not start earlier in practice)
-      const int rounds = 1;
-      for (int rd = 0; rd < rounds; ++rd) {
-        for (int ks = warp; ks < KS; ks += TC_THREADS / 32) {
-          // this k-step's two row groups: weights and biases of rows r, r+1
-          float2 wv[2][4], bv[2];
+      // (pipelining layer 0 against the MMAs in rounds of 8 k-steps measured
+      // slower: the pair's tensor pipe is shared with the SM's other team)
+      for (int ks = warp; ks < KS; ks += TC_THREADS / 32) {
+        // this k-step's two row groups: weights and biases of rows r, r+1
+        float2 wv[2][4], bv[2];
 #pragma unroll
-          for (int gi = 0; gi < 2; ++gi) {
-            const int r = (ks * 2 + gi) * 8 + rp * 2;
+        for (int gi = 0; gi < 2; ++gi) {
+          const int r = (ks * 2 + gi) * 8 + rp * 2;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              wv[gi][k] = k < K0 ? *reinterpret_cast<const float2*>(W0 + k * W1p + r) : make_float2(0.f, 0.f);
-            bv[gi] = *reinterpret_cast<const float2*>(b0 + r);
-          }
-#pragma unroll
-          for (int u = 0; u < 2 * EH; ++u) {  // (lane half eh, row group gi)
-            const int eh = u % EH, gi = u / EH;
-            const int e = (eh + pv) * 8 + el, r = (ks * 2 + gi) * 8 + rp * 2;
-            float z0 = 0.0f, z1 = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (k < K0) {
-                z0 = fmaf(wv[gi][k].x, xr[eh][k], z0);
-                z1 = fmaf(wv[gi][k].y, xr[eh][k], z1);
-              }
-            }
-            z0 = z0 + bv[gi].x;
-            z1 = z1 + bv[gi].y;
-            const float h0 = z0 > 0.0f ? z0 : 0.0f;  // ReLU (NaN -> 0, as cwiseMax)
-            const float h1 = z1 > 0.0f ? z1 : 0.0f;
-            if (fmaxf(h0, h1) > 60000.0f) {
-              if (h0 == INFINITY || h1 == INFINITY) bad |= 1u << e;
-              else range |= 1u << e;  // finite but beyond the fp16 split's range
-            }
-            const __half2 hi = __floats2half2_rn(h0, h1);
-            const float2 hf = __half22float2(hi);
-            const __half2 lo = __floats2half2_rn((h0 - hf.x) * TC_LO_SCALE, (h1 - hf.y) * TC_LO_SCALE);
-            const int nh = PAIR ? el : eh * 8 + el;  // B row of (lane e, hi); lo rows follow NB/2 later
-            *reinterpret_cast<__half2*>(Bs + umma_off(nh, r, NB)) = hi;
-            *reinterpret_cast<__half2*>(Bs + umma_off(nh + NB / 2, r, NB)) = lo;
-          }
+          for (int k = 0; k < 4; ++k)
+            wv[gi][k] = k < K0 ? *reinterpret_cast<const float2*>(W0 + k * W1p + r) : make_float2(0.f, 0.f);
+          bv[gi] = *reinterpret_cast<const float2*>(b0 + r);
         }
-        if (tid == 0) TC_MARK(12);  // layer-0 math + stores
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          if (PAIR && pv) {
-            mbar_arrive_remote(&l0bar[rd], (uint32_t)(crank - 1));
-          } else {
-            mbar_arrive_local(&l0bar[rd]);
+#pragma unroll
+        for (int u = 0; u < 2 * EH; ++u) {  // (lane half eh, row group gi)
+          const int eh = u % EH, gi = u / EH;
+          const int e = (eh + pv) * 8 + el, r = (ks * 2 + gi) * 8 + rp * 2;
+          float z0 = 0.0f, z1 = 0.0f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (k < K0) {
+              z0 = fmaf(wv[gi][k].x, xr[eh][k], z0);
+              z1 = fmaf(wv[gi][k].y, xr[eh][k], z1);
+            }
           }
+          z0 = z0 + bv[gi].x;
+          z1 = z1 + bv[gi].y;
+          const float h0 = z0 > 0.0f ? z0 : 0.0f;  // ReLU (NaN -> 0, as cwiseMax)
+          const float h1 = z1 > 0.0f ? z1 : 0.0f;
+          if (fmaxf(h0, h1) > 60000.0f) {
+            if (h0 == INFINITY || h1 == INFINITY) bad |= 1u << e;
+            else range |= 1u << e;  // finite but beyond the fp16 split's range
+          }
+          const __half2 hi = __floats2half2_rn(h0, h1);
+          const float2 hf = __half22float2(hi);
+          const __half2 lo = __floats2half2_rn((h0 - hf.x) * TC_LO_SCALE, (h1 - hf.y) * TC_LO_SCALE);
+          const int nh = PAIR ? el : eh * 8 + el;  // B row of (lane e, hi); lo rows follow NB/2 later
+          *reinterpret_cast<__half2*>(Bs + umma_off(nh, r, NB)) = hi;
+          *reinterpret_cast<__half2*>(Bs + umma_off(nh + NB / 2, r, NB)) = lo;
         }
-        if (warp == TC_THREADS / 32 - 1 && !(PAIR && pv)) {  // layer 1 on tcgen05 for this round
+      }
+      if (tid == 0) TC_MARK(12);  // layer-0 math + stores
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR && pv) {
+          mbar_arrive_remote(l0bar, (uint32_t)(crank - 1));
+        } else {
+          mbar_arrive_local(l0bar);
+        }
+      }
+      if (warp == TC_THREADS / 32 - 1 && !(PAIR && pv)) {  // layer 1 on tcgen05
+        if constexpr (PAIR) {
+          mbar_wait_parity(l0bar, (uint32_t)(it & 1));
+        } else {
+          mbar_wait_parity_cta(l0bar, (uint32_t)(it & 1));
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t aLo = smem_u32(Alo), bS = smem_u32(Bs);
+        constexpr uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (NB / 8) * 128;
+        for (int k = 0; k < KS; ++k) {
+          const uint64_t bd = umma_desc(bS + k * 2 * b_lbo, b_lbo, 128);
+          const uint64_t ad = umma_desc(aLo + k * 2 * a_lbo, a_lbo, 128);
           if constexpr (PAIR) {
-            mbar_wait_parity(&l0bar[rd], (uint32_t)(it & 1));
+            // D[0:32] += Ahi.[Bhi|Blo] (per CTA v: cols 16v..16v+7 hi.hi, +8 hi.lo);
+            // D[32:64] += Alo.[Bhi|Blo] (cols 32+16v.. lo.hi; the lo.lo half is unused)
+            tc_mma2_ts_elect(tmem, tmem + TC_COL_A2 + k * 8, bd, id2, k > 0);
+            tc_mma2_ss_elect(tmem + 32, ad, bd, id2, k > 0);
           } else {
-            mbar_wait_parity_cta(&l0bar[rd], (uint32_t)(it & 1));
+            tc_mma_ts_elect(tmem, tmem + TC_COL_A + k * 8, bd, id32, k > 0);  // D[0:32] += Ahi.[Bhi|Blo]
+            tc_mma_ss_elect(tmem + 16, ad, bd, id16, 1);                      // D1 += Alo.Bhi
           }
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t aLo = smem_u32(Alo), bS = smem_u32(Bs);
-          constexpr uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (NB / 8) * 128;
-          for (int k = 0; k < KS; ++k) {
-            const uint64_t bd = umma_desc(bS + k * 2 * b_lbo, b_lbo, 128);
-            const uint64_t ad = umma_desc(aLo + k * 2 * a_lbo, a_lbo, 128);
-            if constexpr (PAIR) {
-              // D[0:32] += Ahi.[Bhi|Blo] (per CTA v: cols 16v..16v+7 hi.hi, +8 hi.lo);
-              // D[32:64] += Alo.[Bhi|Blo] (cols 32+16v.. lo.hi; the lo.lo half is unused)
-              tc_mma2_ts_elect(tmem, tmem + TC_COL_A2 + k * 8, bd, id2, k > 0);
-              tc_mma2_ss_elect(tmem + 32, ad, bd, id2, k > 0);
-            } else {
-              tc_mma_ts_elect(tmem, tmem + TC_COL_A + k * 8, bd, id32, k > 0);  // D[0:32] += Ahi.[Bhi|Blo]
-              tc_mma_ss_elect(tmem + 16, ad, bd, id16, 1);                      // D1 += Alo.Bhi
-            }
-          }
-          if (rd == rounds - 1) {
-            if constexpr (PAIR) {
-              tc_commit2_elect(mbar, (uint16_t)(3u << crank));  // crank is the pair's even rank
-            } else {
-              tc_commit_elect(mbar);
-            }
-          }
+        }
+        if constexpr (PAIR) {
+          tc_commit2_elect(mbar, (uint16_t)(3u << crank));  // crank is the pair's even rank
+        } else {
+          tc_commit_elect(mbar);
         }
       }
       bad = __reduce_or_sync(0xffffffffu, bad);
@@ -665,7 +645,7 @@ bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.off_mask = off;
   off = al(off + MAXL * 4, 16);
   p.off_bar = off;
-  off = al(off + 8 * (3 + TC_MAX_ROUNDS), 16);
+  off = al(off + 8 * 4, 16);  // mbar, l0bar, xbar[2]
   p.off_tslot = off;
   off = al(off + 16, 16);
   p.bytes = off;
