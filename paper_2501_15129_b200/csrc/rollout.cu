@@ -69,11 +69,6 @@ EVB_DEV const float* gparams<float>(const ParamDesc& P) {
   return P.params_f32;
 }
 
-EVB_DEV uint32_t ld_cluster_u32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-  return v;
-}
 
 __global__ void k_materialize(const ParamDesc P, long long d, int a0, int a1, double* out) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -346,51 +341,6 @@ EVB_DEV uint32_t hidden_dmma_direct(const double* __restrict__ Ws, int WS, int R
   return bad;
 }
 
-// Hidden-layer slice GEMM on the FP64 tensor cores (ET = 16 lanes).
-// Warp tile: 32 rows (4 m-tiles) x 16 lanes (2 n-tiles) over a k-chunk;
-// partial tiles go to the same swizzled `part` layout as the SIMT path
-// (psw<1,16>).  W rows are padded (stride WS = RSP + 4) so the four k-rows
-// of an A fragment fall in distinct bank groups.
-EVB_DEV void hidden_partial_dmma(const double* __restrict__ Ws, int WS, int RSP, int K, int KS,
-                                 const double* __restrict__ x, double* __restrict__ part, int tid) {
-  constexpr int ET = 16;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int nmw = RSP / 32;
-  const int kc = ((K + KS - 1) / KS + 3) & ~3;  // chunk, multiple of 4
-  for (int w = warp; w < nmw * KS; w += ROLLOUT_THREADS / 32) {
-    const int mg = w % nmw, ks = w / nmw;
-    const int k0 = ks * kc, k1 = min(K, k0 + kc);
-    double acc[4][2][2];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    const double* wb = Ws + mg * 32 + g;
-    for (int k = k0; k < k1; k += 4) {
-      const int kk = k + t;
-      const bool in = kk < k1;
-      double a[4], b[2];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) a[mt] = in ? wb[(size_t)kk * WS + mt * 8] : 0.0;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) b[nt] = in ? x[(size_t)kk * ET + nt * 8 + g] : 0.0;
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
-    }
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int r = mg * 32 + mt * 8 + g, e = nt * 8 + 2 * t + i;
-          part[((size_t)ks * RSP + r) * ET + (e ^ (r & (ET - 1)))] = acc[mt][nt][i];
-        }
-  }
-}
 
 template <typename T, int TR, int ET, int C, bool MMA>
 __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __grid_constant__ RolloutArgs A) {
