@@ -520,6 +520,75 @@ __global__ void __launch_bounds__(256) k_jacobi_apply_sym(double* __restrict__ W
   }
 }
 
+EVB_DEV void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+EVB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+EVB_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// V <- V J (the accumulated rotations, columns of every pair): persistent
+// CTAs walk (64-row tile, pair) work items with a 2-stage cp.async pipeline --
+// the next item's V panel and U block stream into shared memory while the
+// current one is multiplied on the FP64 tensor cores.
+constexpr int JV_STAGE = 2 * JP * (JP + 2);  // doubles per stage: panel + U
+__global__ void __launch_bounds__(256, 1) k_jacobi_apply_v(double* __restrict__ M, int dp, int nb, int round,
+                                                           const double* __restrict__ U) {
+  extern __shared__ __align__(16) double jsm[];
+  const int np = nb / 2, ntr = dp / JP;
+  const long long items = (long long)np * ntr;
+  const int tid = threadIdx.x;
+  auto issue = [&](long long item, int stage) {
+    double(*Ts)[JP + 2] = reinterpret_cast<double(*)[JP + 2]>(jsm + stage * JV_STAGE);
+    double(*Us)[JP + 2] = reinterpret_cast<double(*)[JP + 2]>(jsm + stage * JV_STAGE + JP * (JP + 2));
+    const int pair = (int)(item / ntr), tile0 = (int)(item % ntr) * JP;
+    int P, Q;
+    rr_pair(nb, round, pair, P, Q);
+    const double* Ug = U + (long long)pair * JP * JP;
+    for (int c = tid; c < JP * JP / 2; c += 256) {  // 16-byte chunks
+      const int r = c / (JP / 2), q = (c % (JP / 2)) * 2;
+      cp_async16(&Us[r][q], Ug + r * JP + q);
+      const int gc = q < JB ? P * JB + q : Q * JB + q - JB;
+      cp_async16(&Ts[r][q], M + (long long)(tile0 + r) * dp + gc);
+    }
+    cp_async_commit();
+  };
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  long long item = blockIdx.x;
+  if (item < items) issue(item, 0);
+  for (int it = 0; item < items; ++it, item += gridDim.x) {
+    const int st = it & 1;
+    const long long next = item + gridDim.x;
+    if (next < items) {
+      issue(next, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double(*Ts)[JP + 2] = reinterpret_cast<const double(*)[JP + 2]>(jsm + st * JV_STAGE);
+    const double(*Us)[JP + 2] = reinterpret_cast<const double(*)[JP + 2]>(jsm + st * JV_STAGE + JP * (JP + 2));
+    double acc[4][2][2];
+    jtile_gemm(Ts, false, Us, acc, wm, wn, g, t);
+    const int pair = (int)(item / ntr), tile0 = (int)(item % ntr) * JP;
+    int P, Q;
+    rr_pair(nb, round, pair, P, Q);
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int r = wm + mt * 8 + g, n = wn + nt * 8 + 2 * t;
+        const int gc = n < JB ? P * JB + n : Q * JB + n - JB;
+        *reinterpret_cast<double2*>(M + (long long)(tile0 + r) * dp + gc) =
+            make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      }
+    __syncthreads();  // this stage is refilled two items later
+  }
+}
+
 // off-diagonal / total squared mass of the leading d x d block
 __global__ void k_offdiag(const double* A, int d, int dp, double* red) {
   __shared__ double s0[256], s1[256];
@@ -627,11 +696,16 @@ int sym_eig_jacobi(CmaDev& w, const double* A, int d, double* evals_min, double*
   const long long n2 = (long long)dp * dp;
   const size_t sm_pairs = sizeof(double) * 2 * JP * (JP + 1), sm_apply = sizeof(double) * 2 * JP * (JP + 2);
   const size_t sm_sym = sizeof(double) * 3 * JP * (JP + 2);
+  const size_t sm_v = sizeof(double) * 2 * JV_STAGE;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned v_grid = (unsigned)std::min<long long>((long long)nsm, (long long)(nb / 2) * (dp / JP));
   const long long np = nb / 2;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_jacobi_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_pairs);
     cudaFuncSetAttribute(k_jacobi_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply);
+    cudaFuncSetAttribute(k_jacobi_apply_v, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v);
     cudaFuncSetAttribute(k_jacobi_apply_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sym);
     attr = true;
   }
@@ -691,7 +765,7 @@ int sym_eig_jacobi(CmaDev& w, const double* A, int d, double* evals_min, double*
     for (int r = 0; r < nb - 1; ++r) {
       k_jacobi_pairs<<<nb / 2, 256, sm_pairs, s>>>(w.W, dp, nb, r, w.U, inner_sweeps);
       k_jacobi_apply_sym<<<(unsigned)(np * (np + 1) / 2), 256, sm_sym, s>>>(w.W, dp, nb, r, w.U);
-      k_jacobi_apply<<<dim3(dp / JP, nb / 2), 256, sm_apply, s>>>(w.V, dp, nb, r, w.U, 1);
+      k_jacobi_apply_v<<<v_grid, 256, sm_v, s>>>(w.V, dp, nb, r, w.U);
       count_launch(3);
     }
   }
