@@ -189,7 +189,7 @@ int eo_ars_ask(const double* mean, int64_t d, double sigma, eo_key key, int n, d
 int eo_ars_tell(double* mean, int64_t d, const eo_ars_cfg* cfg, const double* deltas,
                 const double* r_plus, const double* r_minus, int half) {
   const int b = cfg->elites < half ? cfg->elites : half;
-  double* scores = (double*)malloc(sizeof(double) * (size_t)(half > 0 ? half : 1));
+  double* scores = (double*)calloc((size_t)(half > 0 ? half : 1), sizeof(double));
   int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)(half > 0 ? half : 1));
   /* r_plus.cwiseMax(r_minus): std::max(a, b) = (a < b) ? b : a */
   for (int i = 0; i < half; ++i) scores[i] = r_plus[i] < r_minus[i] ? r_minus[i] : r_plus[i];
