@@ -112,6 +112,7 @@ class CudaShardedEs:
         self.fall = torch.zeros(self.acs * world, dtype=torch.float64, device=dev)
         self.mbuf = torch.zeros(self.pcs, dtype=torch.float64, device=dev)
         self.mall = torch.zeros(self.pcs * world, dtype=torch.float64, device=dev)
+        self.cnt = torch.zeros(1, dtype=torch.int64, device=dev)
         self.track = cfg.algo == "ars" and cfg.obs_norm in ("auto", "running_stats")
         if self.track:
             self.sbuf = torch.zeros(self.acs * self.e * 9, dtype=torch.float64, device=dev)
@@ -131,6 +132,7 @@ class CudaShardedEs:
 
     def step(self):
         torch, dist = self.torch, self.dist
+        it0, steps0, eps0 = self.es.counters()
         self.es.phase_rollout()          # ask + rollout + fitness of [a0, a1) (synchronous)
         na = self.a1 - self.a0
         self.fbuf[:na].copy_(self.fitness[self.a0:self.a1])
@@ -157,5 +159,13 @@ class CudaShardedEs:
             lo, hi = r * self.pcs, min(self.d, (r + 1) * self.pcs)
             if hi > lo:
                 self.mean[lo:hi].copy_(self.mall[r * self.pcs: r * self.pcs + hi - lo])
+        # WorkflowState::env_steps counts the whole generation
+        # (proj/src/workflow_es.cpp:134): each rank summed only its shard's lane
+        # steps (episodes are pop x count on every rank), so the step deltas
+        # are summed over ranks (8 bytes)
+        it1, steps1, eps1 = self.es.counters()
+        self.cnt.copy_(torch.tensor([steps1 - steps0], dtype=torch.int64))
+        dist.all_reduce(self.cnt)
+        self.es.set_counters(it1, steps0 + int(self.cnt.item()), eps1)
         torch.cuda.synchronize()
         return m
