@@ -231,11 +231,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # EVORL_BENCH_ONE_GPU=1 / EVORL_BENCH_BACKEND=gloo: functional smoke test of
+    # the N>1 code path on a one-GPU box (all ranks on cuda:0; numbers meaningless)
+    if os.environ.get("EVORL_BENCH_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("EVORL_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     L = _lib.load()
 
     kw = {k: v for k, v in cfgd.items() if k != "desc"}
