@@ -535,3 +535,17 @@ def test_transitions_match_oracle(oracle, evb, env, hidden, m, e, count, H, fixe
         for k in ("obs", "next_obs", "rewards"):
             assert np.allclose(g[k], w[k], rtol=RTOL_CLOSED, atol=1e-12), k
         assert np.allclose(got_r[a], want_r[a], rtol=RTOL_CLOSED, atol=1e-12)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(algo="openes", pop=1), "openes_ask: population must be at least 2"),          # proj/src/ec.cpp:72
+    (dict(algo="openes", pop=7), "openes_ask: mirrored sampling needs an even population"),  # :74
+    (dict(algo="ars", pop=9), "ars_ask: population must be even"),                      # :114
+    (dict(algo="ves", pop=1), "ves_ask: population must be at least 2"),                # :165
+    (dict(algo="ves", pop=5), "ves_ask: mirrored sampling needs an even population"),   # :167
+])
+def test_ask_errors_carry_reference_messages(evb, kw, msg):
+    g = evb.EsWorkflow(evb.EsConfig(env="pendulum", hidden=(8,), max_episode_steps=10, **kw)).init((1, 2))
+    with pytest.raises(evb.InvalidArgument) as ei:
+        g.step()
+    assert str(ei.value) == msg
