@@ -129,6 +129,13 @@ def test_tc_workflow_generation(oracle, evb):
     # ranks: at most a few adjacent swaps between near-tied candidates
     ro, rg = np.argsort(np.argsort(fo)), np.argsort(np.argsort(fg))
     assert np.abs(ro - rg).max() <= 2
+    # Workflow::evaluate on the tensor-core team (32 episodes -> 16-lane teams)
+    ek = oracle.key_from_seed(99)
+    g.set_mean(o.mean())
+    mr_o, sd_o = o.evaluate(32, ek)
+    mr_g, sd_g = g.evaluate(32, ek)
+    assert mr_g == pytest.approx(mr_o, rel=RTOL_F32)
+    assert sd_g == pytest.approx(sd_o, rel=1e-2, abs=1e-3)
 
 
 def test_tc_operand_range_is_reported(oracle, evb):
