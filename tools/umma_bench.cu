@@ -9,9 +9,9 @@
 #include <cstdint>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ uint64_t desc(uint32_t a, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t desc(uint32_t a, uint32_t lbo, uint32_t sbo, uint32_t layout = 0) {
   return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
 }
 constexpr uint32_t idesc(int M, int N) { return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24); }
 
@@ -38,7 +38,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
 }
 
 // NMMA MMAs, rotating over NACC accumulators of N columns each
-template <int N, bool TS, int NACC>
+template <int N, bool TS, int NACC, bool SW128 = false>
 __global__ void bench(long long* out, int nmma) {
   __shared__ __align__(1024) unsigned char A[128 * 16 * 2 * 4];  // 4 k-steps of A (16 KB)
   __shared__ __align__(1024) unsigned char B[256 * 16 * 2];
@@ -64,7 +64,9 @@ __global__ void bench(long long* out, int nmma) {
       const long long t0 = clock64();
       for (int i = 0; i < nmma; ++i) {
         const int k = i & 3;
-        const uint64_t ad = desc(su32(A) + k * 2 * 2048, 2048, 128);
+        // SW128: 128-byte swizzle atoms (8 rows x 64 halves, 1024 B), the k-step
+        // advances the start address 32 B inside the atom
+        const uint64_t ad = SW128 ? desc(su32(A) + k * 32, 16, 1024, 2) : desc(su32(A) + k * 2 * 2048, 2048, 128);
         const uint64_t bd = desc(su32(B), (N / 8) * 128, 128);
         const uint32_t d = tmem + (uint32_t)((i % NACC) * N);
         mma<N, TS>(d, tmem + 256 + k * 8, ad, bd, i >= NACC ? 1u : 0u);
@@ -91,9 +93,9 @@ __global__ void bench(long long* out, int nmma) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int N, bool TS, int NACC>
+template <int N, bool TS, int NACC, bool SW128 = false>
 void run(const char* name, long long* d, int nmma) {
-  bench<N, TS, NACC><<<1, 128>>>(d, nmma);
+  bench<N, TS, NACC, SW128><<<1, 128>>>(d, nmma);
   long long h[2];
   cudaError_t e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) {
@@ -107,6 +109,11 @@ void run(const char* name, long long* d, int nmma) {
 int main() {
   long long* d;
   cudaMalloc(&d, 16 * sizeof(long long));
+  for (int n : {16, 64}) {
+    run<16, false, 1, true>("SS SW128 N=16 1 acc", d, n);
+    run<32, false, 1, true>("SS SW128 N=32 1 acc", d, n);
+    run<256, false, 1, true>("SS SW128 N=256 1 acc", d, n);
+  }
   for (int n : {1, 2, 4, 16, 64}) {
     run<16, false, 1>("SS N=16 1 acc", d, n);
     run<32, false, 1>("SS N=32 1 acc", d, n);
