@@ -1317,7 +1317,8 @@ static int batched_rollout_impl(const evorl_env_desc* envd, const evorl_mlp_desc
     return set_err(EVORL_E_INVALID_ARGUMENT, "unknown precision");
   // transitions are written by the cluster team (the tc team evaluates as f32)
   const bool cta_ok = plan_rollout(net, env.obs_dim, e, tr && precision == EVORL_PREC_TC ? EVORL_PREC_F32 : precision,
-                                   &plan);
+                                   &plan, tr != nullptr);
+  if (tr) plan.trn = 1;
   const bool use_warp =
       !tr && !(cta_ok && plan.tc) && plan_rollout_warp(net, env.obs_dim, e, precision, &wplan);
   if (!cta_ok && !use_warp)

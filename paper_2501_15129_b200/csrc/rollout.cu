@@ -342,7 +342,11 @@ EVB_DEV uint32_t hidden_dmma_direct(const double* __restrict__ Ws, int WS, int R
 }
 
 
-template <typename T, int TR, int ET, int C, bool MMA>
+// GW: global-weights plan (compile-time, so the SMEM-resident instances keep
+// provably-shared weight pointers -- LDS, not generic loads -- in the hot loop)
+// TRN: write SampleBatch rows (transition collection) -- compile-time, so the
+// generation kernels carry none of it
+template <typename T, int TR, int ET, int C, bool MMA, bool GW, bool TRN>
 __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __grid_constant__ RolloutArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemPlan& S = A.plan;
@@ -365,8 +369,8 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   for (int i = tid; i < S.bytes / 4; i += ROLLOUT_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
   __syncthreads();
   // global-weights plan: this agent's materialised candidate row (HBM / L2)
-  const T* gp = S.gw ? gparams<T>(A.par) + (long long)agent_local * N.d : nullptr;
-  for (int l = 0; l < nh && !S.gw; ++l) {
+  const T* gp = GW ? gparams<T>(A.par) + (long long)agent_local * N.d : nullptr;
+  for (int l = 0; l < nh && !GW; ++l) {
     const int K = N.dims[l], W = N.dims[l + 1];
     const int RS = S.RS[l], r0 = S.REP[l] ? 0 : crank * RS;
     const int RSv = max(0, min(RS, W - r0));
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   const int KRP = nh > 0 ? S.RSP[nh - 1] : Kout;
   const int k0out = nh > 0 ? crank * KRS : 0;
   const int KRv = max(0, min(KRS, Kout - k0out));
-  if (!S.gw) {
+  if (!GW) {
     T* Wo = reinterpret_cast<T*>(smem + S.off_wout);
     T* bo = reinterpret_cast<T*>(smem + S.off_bout);
     for (int i = tid; i < KRv * O; i += ROLLOUT_THREADS) {
@@ -438,8 +442,8 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem + S.off_mask);
   // output layer: flat p = w_off + k * O + o (column-major O x K), the same
   // k-major indexing as the SMEM copy
-  const T* Wo = S.gw ? gp + N.w_off[L - 1] + (long long)k0out * O : reinterpret_cast<const T*>(smem + S.off_wout);
-  const T* bo = S.gw ? gp + N.b_off[L - 1] : reinterpret_cast<const T*>(smem + S.off_bout);
+  const T* Wo = GW ? gp + N.w_off[L - 1] + (long long)k0out * O : reinterpret_cast<const T*>(smem + S.off_wout);
+  const T* bo = GW ? gp + N.b_off[L - 1] : reinterpret_cast<const T*>(smem + S.off_bout);
   const int OE = O * ET;
   const int OE1 = (O + 1) * ET;  // + one row carrying each lane's first non-finite layer
 
@@ -451,7 +455,8 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
     double raw[4];
     observe(E, s, raw);
     sin_th = raw[1];
-    for (int i = 0; i < 4; ++i) cur_raw[i] = raw[i];
+    if constexpr (TRN)
+      for (int i = 0; i < 4; ++i) cur_raw[i] = raw[i];
     if (act && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
       if (wc == 0.0) {
         for (int i = 0; i < E.obs_dim; ++i) {
@@ -502,8 +507,8 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
       const T* xin = l == 0 ? x0 : reinterpret_cast<const T*>(smem + S.off_h[l - 1]);
       // weights k-major with row stride WS: the SMEM slice, or (gw) the
       // candidate row itself -- flat p = w_off + k * W + r is k-major, stride W
-      const T* Ws = S.gw ? gp + N.w_off[l] + r0 : reinterpret_cast<const T*>(smem + S.off_w[l]);
-      const T* bs = S.gw ? gp + N.b_off[l] + r0 : reinterpret_cast<const T*>(smem + S.off_b[l]);
+      const T* Ws = GW ? gp + N.w_off[l] + r0 : reinterpret_cast<const T*>(smem + S.off_w[l]);
+      const T* bs = GW ? gp + N.b_off[l] + r0 : reinterpret_cast<const T*>(smem + S.off_b[l]);
       T* hb = reinterpret_cast<T*>(smem + S.off_h[l]);
       const bool last_hidden = l == nh - 1;
       const bool scatter = C > 1 && !rep && !last_hidden;
@@ -651,7 +656,7 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
         bool term = false, trunc = false;
         const uint32_t f =
             env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr);
-        if (!f && A.t_obs != nullptr && crank == 0) {  // one SampleBatch row (rollout.cpp:132-139)
+        if (TRN && !f && crank == 0) {  // one SampleBatch row (rollout.cpp:132-139)
           double nxt[4];
           observe(E, s, nxt);  // final_obs: the successor before any auto-reset
           const long long row = ((long long)agent_local * A.e + j) * A.t_cap + steps;
@@ -801,8 +806,18 @@ static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int
   return true;
 }
 
-bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan) {
+bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan, bool simple_only) {
   const int ET = e >= 5 ? 16 : (e >= 2 ? 4 : 1);
+  plan->trn = 0;
+  if (simple_only) {  // TR = 1 SIMT, resident or global-weights
+    plan->tc = 0;
+    const int ts = precision == 0 ? 8 : 4;
+    for (int C : {1, 2, 4, 8})
+      if (try_plan(net, obs_dim, ET, 1, C, ts, plan)) return true;
+    for (int C : {8, 4, 2, 1})
+      if (try_plan(net, obs_dim, ET, 1, C, ts, plan, false, true)) return true;
+    return false;
+  }
   if (precision == 2) {  // EVORL_PREC_TC: tcgen05 team if the shape fits, else the fp32 team
     if (plan_rollout_tc(net, obs_dim, e, &plan->tcp)) {
       plan->tc = 1;
@@ -833,9 +848,9 @@ bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPla
   return false;
 }
 
-template <typename T, int TR, int ET, int C, bool MMA>
+template <typename T, int TR, int ET, int C, bool MMA, bool GW = false, bool TRN = false>
 static cudaError_t launch_inst(const RolloutArgs& a, cudaStream_t stream) {
-  auto kern = rollout_kernel<T, TR, ET, C, MMA>;
+  auto kern = rollout_kernel<T, TR, ET, C, MMA, GW, TRN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -857,19 +872,32 @@ static cudaError_t launch_inst(const RolloutArgs& a, cudaStream_t stream) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <typename T, int TR, int ET, bool MMA = false>
+template <typename T, int TR, int ET, bool MMA = false, bool GW = false, bool TRN = false>
 static cudaError_t launch_c(const RolloutArgs& a, cudaStream_t s) {
   switch (a.plan.C) {
-    case 1: return launch_inst<T, TR, ET, 1, MMA>(a, s);
-    case 2: return launch_inst<T, TR, ET, 2, MMA>(a, s);
-    case 4: return launch_inst<T, TR, ET, 4, MMA>(a, s);
-    case 8: return launch_inst<T, TR, ET, 8, MMA>(a, s);
+    case 1: return launch_inst<T, TR, ET, 1, MMA, GW, TRN>(a, s);
+    case 2: return launch_inst<T, TR, ET, 2, MMA, GW, TRN>(a, s);
+    case 4: return launch_inst<T, TR, ET, 4, MMA, GW, TRN>(a, s);
+    case 8: return launch_inst<T, TR, ET, 8, MMA, GW, TRN>(a, s);
   }
   return cudaErrorInvalidValue;
 }
 
+template <typename T, bool GW>
+static cudaError_t launch_trn(const RolloutArgs& a, cudaStream_t s) {
+  if (a.plan.ET == 1) return launch_c<T, 1, 1, false, GW, true>(a, s);
+  if (a.plan.ET == 4) return launch_c<T, 1, 4, false, GW, true>(a, s);
+  return launch_c<T, 1, 16, false, GW, true>(a, s);
+}
+
 template <typename T>
 static cudaError_t launch_t(const RolloutArgs& a, cudaStream_t s) {
+  if (a.plan.trn) return a.plan.gw ? launch_trn<T, true>(a, s) : launch_trn<T, false>(a, s);
+  if (a.plan.gw) {  // global-weights plans are SIMT, TR = 1
+    if (a.plan.ET == 1) return launch_c<T, 1, 1, false, true>(a, s);
+    if (a.plan.ET == 4) return launch_c<T, 1, 4, false, true>(a, s);
+    return launch_c<T, 1, 16, false, true>(a, s);
+  }
   if (a.plan.ET == 1) return launch_c<T, 1, 1>(a, s);
   if (a.plan.ET == 4) return launch_c<T, 1, 4>(a, s);
   if (a.plan.TR == 2) return launch_c<T, 2, 16>(a, s);

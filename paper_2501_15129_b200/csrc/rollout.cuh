@@ -116,6 +116,7 @@ struct SmemPlan {
   int bytes;
   int gw;         // 1: weights read from the materialised candidates in HBM/L2
                  //    (policies too large for SMEM residency; SIMT slice GEMMs)
+  int trn;        // 1: collect transitions (RolloutArgs::t_*), TR = 1 SIMT plans only
   int tc;         // 1: EVORL_PREC_TC tcgen05 team (rollout_tc.cu), plan in tcp
   TcPlanOut tcp;
 };
@@ -154,7 +155,10 @@ struct RolloutArgs {
 // Host-side: launch the rollout with the plan's template instance.
 cudaError_t launch_rollout(const RolloutArgs& a, int precision, cudaStream_t stream);
 // Host-side: build the SMEM plan; returns false if no cluster size fits.
-bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan);
+// simple_only: only TR = 1 SIMT plans (SMEM-resident or global-weights) -- the
+// plans with a transition-collecting instantiation (SmemPlan::trn)
+bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan,
+                  bool simple_only = false);
 
 // Warp-team rollout for small policies (rollout_warp.cu): one warp per lane.
 struct WarpPlanOut {
