@@ -275,6 +275,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   NormParams nrm;
   nrm.active = 0;
   if (A.norm != nullptr) nrm = *A.norm;
+  double inv_den[4];
+  for (int i = 0; i < 4; ++i) inv_den[i] = nrm.active ? 1.0 / nrm.den[i] : 1.0;
   float* x0 = reinterpret_cast<float*>(smem + P.off_x0);    // [4][16]
   float* red = reinterpret_cast<float*>(smem + P.off_red);  // [4 quadrants][O][16]
   float* pout_base = reinterpret_cast<float*>(smem + P.off_pout);
@@ -301,9 +303,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
         }
       }
     }
+    // normalised policy input (policy arithmetic, fp32 tolerance): multiply by
+    // the reciprocal instead of the IEEE division the fp64 team uses
     for (int i = 0; i < E.obs_dim; ++i) {
       double v = raw[i];
-      if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
+      if (nrm.active) v = (v - nrm.mean[i]) * inv_den[i];
       x0[i * TC_N + tid] = act ? __double2float_rn(v) : 0.0f;
     }
   };
@@ -540,8 +544,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
           for (int o = 1; o < O; ++o)
             if (z[o] > z[arg]) arg = o;
           action = (double)arg;
-        } else if (N.head == HEAD_TANH) {
-          action = N.tanh_scale * tanh(z[0]);
+        } else if (N.head == HEAD_TANH) {  // fp32 head: part of the fp32-tolerance policy
+          action = N.tanh_scale * (double)tanhf((float)z[0]);
         } else {
           action = z[0];
         }
