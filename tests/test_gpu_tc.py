@@ -177,3 +177,21 @@ def test_sharded_materialised_ask_matches_unsharded(evb, precision, algo):
         a0, a1, _, _ = h.shard_ranges()
         got[a0:a1] = h.fitness()[a0:a1]
     assert np.array_equal(got, want)
+
+
+def test_tc_categorical_two_outputs(oracle, evb):
+    """CartPole (categorical head, O = 2 outputs through the epilogue's
+    per-output reduce-scatter) on the tensor-core team: episode lengths are
+    integers, so an fp32 argmax near-tie can change a return -- the bar is
+    that almost every episode matches the fp64 oracle exactly."""
+    ospec, desc = _policy(oracle, evb, "cartpole", [128, 256])
+    m, e = 8, 16
+    params = np.array([oracle.init_params(ospec, oracle.key_from_seed(950 + a)) for a in range(m)])
+    key = oracle.key_from_seed(951)
+    envspec = oracle.env_spec("cartpole", False, 200)
+    want, wsteps, _ = oracle.batched_rollout(envspec, ospec, None, params, e, key, workers=0)
+    got, steps, _ = evb.batched_rollout("cartpole", desc, params, e, key, max_episode_steps=200,
+                                        precision="tc")
+    w = np.array(want)
+    assert (got == w).mean() >= 0.95, (got == w).mean()
+    assert abs(got.mean() - w.mean()) <= 0.02 * w.mean()
