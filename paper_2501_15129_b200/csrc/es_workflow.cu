@@ -179,6 +179,7 @@ struct evorl_es {
   // fp32, materialised once by a fully parallel ask instead of being
   // regenerated in every CTA's prologue (null: regenerate, e.g. over the cap)
   float* d_cand_f32 = nullptr;
+  unsigned char* d_tc_blocks = nullptr;  // tc team: pre-split layer-1 weights (cand_cap agents)
   int cand_cap = 0;               // agents per materialised chunk (team path)
   // OpenES noise-table mode (proj/src/ec.cpp:50-86): the shared table and
   // this generation's window offsets
@@ -281,7 +282,7 @@ static void free_all(evorl_es* s) {
                   s->d_ep_returns, s->d_lane_stats, s->d_agent_stats, s->d_lane_steps, s->d_rank,
                   s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
                   s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand,
-                  s->d_cand_f32, s->d_tell_part, s->d_table, s->d_offsets};
+                  s->d_cand_f32, s->d_tell_part, s->d_table, s->d_offsets, s->d_tc_blocks};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
@@ -406,6 +407,8 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
       A(dalloc(&s->d_cand, (size_t)s->cand_cap * d));
     } else {
       A(dalloc(&s->d_cand_f32, (size_t)s->cand_cap * d));
+      if (s->plan.tc)
+        A(dalloc(&s->d_tc_blocks, (size_t)s->cand_cap * s->plan.tcp.data[0] * tc_block_bytes(s->plan.tcp)));
     }
   }
   if (cfg->algo == EVORL_ALGO_CMAES) {
@@ -743,6 +746,12 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
         CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream));
         ac.par.src = SRC_EXPLICIT_F32;
         ac.par.params_f32 = s->d_cand_f32;
+        if (s->d_tc_blocks) {  // the tc team's layer-1 weights, pre-split (bulk-copied by its prologue)
+          CK(run_tc_split(s->d_cand_f32, s->net, s->plan.tcp, c1 - c0, s->d_tc_blocks, s->stream));
+          count_launch();
+          ac.tc_blocks = s->d_tc_blocks;
+          ac.tc_block_bytes = tc_block_bytes(s->plan.tcp);
+        }
       } else {
         CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream));
         ac.par.src = SRC_EXPLICIT;

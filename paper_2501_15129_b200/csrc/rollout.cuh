@@ -150,6 +150,11 @@ struct RolloutArgs {
   unsigned char* t_trunc;
   double* t_next;     // rows x obs_dim (final_obs: successor before auto-reset)
   long long t_cap;
+  // tc team: per (agent, CTA) pre-split layer-1 weights in the UMMA canonical
+  // layout (A_hi then A_lo, tc_block_bytes each pair), bulk-copied by the
+  // prologue; null = split in the prologue from the parameters
+  const unsigned char* tc_blocks;
+  long long tc_block_bytes;
 };
 
 // Host-side: launch the rollout with the plan's template instance.
@@ -180,6 +185,11 @@ cudaError_t run_materialize_f32(const ParamDesc& par, long long d, int a0, int a
 // Tensor-core rollout (rollout_tc.cu, precision EVORL_PREC_TC): obs -> W1 -> W2 -> O
 // policies with W2 a multiple of 128; the W2 x W1 layer runs on tcgen05.
 bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out);
+// bytes of one (agent, CTA) pre-split weight block of a tc plan
+long long tc_block_bytes(const TcPlanOut& plan);
+// the fp32 candidates [n_agents x d] -> pre-split blocks [n_agents][C]
+cudaError_t run_tc_split(const float* cand, const NetDesc& net, const TcPlanOut& plan, int n_agents,
+                         unsigned char* blocks, cudaStream_t stream);
 cudaError_t launch_rollout_tc(const RolloutArgs& a, const TcPlanOut& plan, cudaStream_t stream);
 
 }  // namespace evorl_b200

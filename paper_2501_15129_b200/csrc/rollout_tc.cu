@@ -175,10 +175,12 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   long long tprev = clock64();
 #endif
   for (int i = tid; i < P.bytes / 4; i += TC_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before any bulk copy into the zeroed SMEM
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
   uint64_t* l0bar = mbar + 1;  // layer-0 B rows stored (this CTA's warps, and the odd peer's on a pair)
   uint64_t* xbar = mbar + 2;   // [2]: partial outputs of every cluster CTA landed
+  uint64_t* pbar = mbar + 4;   // prologue bulk copies of the pre-split weights
   __syncthreads();
   if (warp == 0) {
     if constexpr (PAIR) {  // both CTAs of the pair: same columns in each TMEM
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     mbar_init(l0bar, (PAIR ? 2 : 1) * (TC_THREADS / 32));
     mbar_init(&xbar[0], 1);  // output exchange, double-buffered by step parity
     mbar_init(&xbar[1], 1);
+    mbar_init(pbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -221,7 +224,38 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     b0[r] = (float)param_value(A.par, N.d, agent_local, agent, N.b_off[0] + r);
   // layer-1 weights of row `row`: A_hi -> TMEM (lanes = rows, 2 halves per
   // column), A_lo -> SMEM.  Warp halves take alternate 16-wide k chunks.
-  for (int c = half; c < W1p / 16; c += 2) {
+  if (A.tc_blocks != nullptr) {
+    // pre-split block (materialised ask): bulk-copy A_hi into the A_lo region,
+    // move it to TMEM, then bulk-copy A_lo in place (cp.async.bulk, mbarrier)
+    const unsigned char* blk = A.tc_blocks + ((long long)agent_local * C + crank) * A.tc_block_bytes;
+    const uint32_t hb = (uint32_t)(A.tc_block_bytes / 2);
+    if (tid == 0) {
+      mbar_arrive_expect_tx(pbar, hb);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(Alo)),
+                   "l"(blk), "r"(hb), "r"(smem_u32(pbar))
+                   : "memory");
+    }
+    mbar_wait_parity_cta(pbar, 0);
+    for (int c = half; c < W1p / 16; c += 2) {
+      uint32_t packed[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) packed[q] = *reinterpret_cast<const uint32_t*>(Alo + umma_off(row, c * 16 + 2 * q, TC_M));
+      tc_st8(tmem + ((uint32_t)(quad * 32) << 16) + (PAIR ? TC_COL_A2 : TC_COL_A) + c * 8, packed);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    __syncthreads();  // every thread done with A_hi in the region
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(pbar, hb);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(Alo)),
+                   "l"(blk + hb), "r"(hb), "r"(smem_u32(pbar))
+                   : "memory");
+    }
+    mbar_wait_parity_cta(pbar, 1);
+  }
+  for (int c = half; c < W1p / 16 && A.tc_blocks == nullptr; c += 2) {
     uint32_t packed[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -619,6 +653,57 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
 
 static int al(int x, int a) { return (x + a - 1) / a * a; }
 
+long long tc_block_bytes(const TcPlanOut& po) {
+  TcPlan p;
+  std::memcpy(&p, &po, sizeof p);
+  return 2LL * TC_M * p.W1p * 2;
+}
+
+// one thread per (agent, CTA, 8-wide k chunk, row): reads 8 weights of the
+// row (coalesced over rows), writes 16 B of A_hi and 16 B of A_lo -- the
+// rows of a k chunk are contiguous in the canonical layout
+__global__ void k_tc_split(const float* __restrict__ cand, long long d, long long w_off1, int W1, int W2, int W1p,
+                           int C, long long total, unsigned char* __restrict__ blocks) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int row = (int)(idx % TC_M);
+  const long long rest = idx / TC_M;
+  const int kc = (int)(rest % (W1p / 8));
+  const long long ac = rest / (W1p / 8);  // agent * C + crank
+  const int crank = (int)(ac % C);
+  const long long agent = ac / C;
+  const int r = crank * TC_M + row;
+  uint32_t hi[4], lo[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    __half h[2], l[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = kc * 8 + 2 * q + u;
+      const float w = (r < W2 && k < W1) ? cand[agent * d + w_off1 + (long long)k * W2 + r] : 0.0f;
+      split_f16(w, h[u], l[u]);
+    }
+    hi[q] = pack2(h[0], h[1]);
+    lo[q] = pack2(l[0], l[1]);
+  }
+  const long long half_bytes = (long long)TC_M * W1p * 2;
+  unsigned char* blk = blocks + ac * 2 * half_bytes;
+  const uint32_t off = umma_off(row, kc * 8, TC_M);
+  *reinterpret_cast<uint4*>(blk + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4*>(blk + half_bytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+}
+
+cudaError_t run_tc_split(const float* cand, const NetDesc& net, const TcPlanOut& po, int n_agents,
+                         unsigned char* blocks, cudaStream_t stream) {
+  TcPlan p;
+  std::memcpy(&p, &po, sizeof p);
+  const long long total = (long long)n_agents * p.C * (p.W1p / 8) * TC_M;
+  if (total <= 0) return cudaSuccess;
+  k_tc_split<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(cand, net.d, net.w_off[1], p.W1, p.W2, p.W1p, p.C,
+                                                                   total, blocks);
+  return cudaGetLastError();
+}
+
 bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   if (net.nlayers != 3 || obs_dim > 4 || e < 5) return false;  // 16-lane teams, obs -> W1 -> W2 -> O
   const int W1 = net.dims[1], W2 = net.dims[2], O = net.dims[3];
@@ -649,7 +734,7 @@ bool plan_rollout_tc(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.off_mask = off;
   off = al(off + MAXL * 4, 16);
   p.off_bar = off;
-  off = al(off + 8 * 4, 16);  // mbar, l0bar, xbar[2]
+  off = al(off + 8 * 5, 16);  // mbar, l0bar, xbar[2], pbar
   p.off_tslot = off;
   off = al(off + 16, 16);
   p.bytes = off;
