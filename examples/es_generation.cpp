@@ -1,0 +1,53 @@
+// es_generation.cpp -- a C++ host running EsWorkflow generations on the B200
+// through evorl_b200.hpp, the way the reference's learn() loop drives its
+// Workflow (proj/src/workflow.cpp:46-68): init, step, periodic evaluate,
+// checkpoint.  Prints one line per generation (values in %a for exact
+// comparison) and the final counters.
+//
+//   es_generation [algo] [pop] [gens] [hidden0] [hidden1] [episodes] [precision] [checkpoint]
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "evorl_b200.hpp"
+
+int main(int argc, char** argv) {
+  namespace eb = evorl_b200;
+  const char* algo = argc > 1 ? argv[1] : "openes";
+  evorl_es_config cfg = eb::default_config();
+  cfg.algo = !std::strcmp(algo, "ars") ? EVORL_ALGO_ARS : !std::strcmp(algo, "cmaes") ? EVORL_ALGO_CMAES
+                                                                                      : EVORL_ALGO_OPENES;
+  cfg.env_id = EVORL_ENV_PENDULUM;
+  cfg.fixed_horizon = 1;
+  cfg.max_episode_steps = 100;
+  cfg.pop = argc > 2 ? std::atoi(argv[2]) : 64;
+  const int gens = argc > 3 ? std::atoi(argv[3]) : 3;
+  cfg.n_hidden = 2;
+  cfg.hidden[0] = argc > 4 ? std::atoi(argv[4]) : 32;
+  cfg.hidden[1] = argc > 5 ? std::atoi(argv[5]) : 32;
+  cfg.fitness_episodes = argc > 6 ? std::atoi(argv[6]) : 1;
+  const std::string prec = argc > 7 ? argv[7] : "f64";
+  cfg.precision = prec == "tc" ? EVORL_PREC_TC : prec == "f32" ? EVORL_PREC_F32 : EVORL_PREC_F64;
+  cfg.vbn_samples = 500;
+  try {
+    eb::EsWorkflow wf(cfg);
+    wf.init({0x1234, 0x5678});
+    for (int g = 0; g < gens; ++g) {
+      const eb::StepMetrics m = wf.step();
+      std::printf("gen %d fitness_mean %a fitness_max %a sigma %a skipped %d\n", g, m.fitness_mean,
+                  m.fitness_max, m.sigma, m.update_skipped ? 1 : 0);
+    }
+    const eb::EvalReport ev = wf.evaluate(16, {7, 8});
+    std::printf("eval mean %a std %a\n", ev.mean_return, ev.return_std);
+    std::int64_t it = 0, steps = 0, eps = 0;
+    wf.counters(&it, &steps, &eps);
+    std::printf("counters %lld %lld %lld\n", (long long)it, (long long)steps, (long long)eps);
+    if (argc > 8) wf.save(argv[8]);
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 2;
+  }
+  return 0;
+}
