@@ -5,17 +5,43 @@
 // comparison) and the final counters.
 //
 //   es_generation [algo] [pop] [gens] [hidden0] [hidden1] [episodes] [precision] [checkpoint]
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
+#include <vector>
 
 #include "evorl_b200.hpp"
 
 int main(int argc, char** argv) {
   namespace eb = evorl_b200;
   const char* algo = argc > 1 ? argv[1] : "openes";
+  if (!std::strcmp(algo, "cma-sphere")) {  // proj/tests/test_ec.cpp:282-297 through the free functions
+    try {
+      const double target[8] = {0.7, -0.3, 0.5, 0.1, -0.8, 0.25, -0.4, 0.6};
+      eb::CmaEs cma(8, 16, 8, 0.3);
+      for (int g = 0; g < 200; ++g) {
+        const std::vector<double> cand = cma.ask(eb::fold_in(eb::key_from_seed(84), (std::uint64_t)g));
+        std::vector<double> fit(16);
+        for (int i = 0; i < 16; ++i) {
+          double s2 = 0;
+          for (int j = 0; j < 8; ++j) s2 += (cand[i * 8 + j] - target[j]) * (cand[i * 8 + j] - target[j]);
+          fit[i] = -s2;
+        }
+        cma.tell(cand, fit);
+      }
+      const std::vector<double> m = cma.mean();
+      double dist = 0;
+      for (int j = 0; j < 8; ++j) dist += (m[j] - target[j]) * (m[j] - target[j]);
+      std::printf("cma-sphere distance %a sigma %a\n", std::sqrt(dist), cma.sigma());
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "error: %s\n", e.what());
+      return 2;
+    }
+    return 0;
+  }
   evorl_es_config cfg = eb::default_config();
   cfg.algo = !std::strcmp(algo, "ars") ? EVORL_ALGO_ARS : !std::strcmp(algo, "cmaes") ? EVORL_ALGO_CMAES
                                                                                       : EVORL_ALGO_OPENES;

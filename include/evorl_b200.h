@@ -263,6 +263,20 @@ int evorl_es_cma_get(evorl_es* es, double* C, double* B, double* D, double* ps, 
 int evorl_es_cma_set(evorl_es* es, const double* C, const double* B, const double* D,
                      const double* ps, const double* pc, double sigma, int64_t generation,
                      int64_t recondition_count);
+/* CMA-ES free functions: CmaState::init / cmaes_ask / cmaes_tell
+ * (proj/src/ec.cpp:191-288, proj/include/evorl/ec.hpp:107-125) on a device
+ * state of dimension d with no env / policy attached: after create mean = 0,
+ * C = B = I, D = 1, ps = pc = 0, sigma = sigma0.  State moves through
+ * evorl_es_get/set_mean and evorl_es_cma_get/set; free with
+ * evorl_es_destroy.  ask writes pop x d row-major candidates
+ * (mean + sigma * B diag(D) z, z = gaussian_matrix(key, pop, d)); tell takes
+ * pop x d candidates and their fitness (maximised).  eig_every as
+ * evorl_es_config::cmaes_eig_every (1 = the reference's schedule). */
+int evorl_cma_create(int64_t d, int32_t pop, int32_t elites, double sigma0, int32_t max_dim,
+                     int32_t eig_every, evorl_es** out);
+int evorl_cma_ask(evorl_es* cma, uint64_t key_hi, uint64_t key_lo, double* candidates);
+int evorl_cma_tell(evorl_es* cma, const double* candidates, const double* fitness);
+
 /* The device eigensolver (blocked Jacobi), replacing
  * Eigen::SelfAdjointEigenSolver (proj/src/ec.cpp:278-287): A n x n symmetric
  * row-major; evals ascending; vecs[p*n + j] = component p of eigenvector j,

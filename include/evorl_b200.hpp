@@ -60,6 +60,17 @@ struct RngKey {
   std::uint64_t hi = 0, lo = 0;
 };
 
+// key_from_seed / fold_in (proj/src/rng.cpp:36-46) over evorl_threefry2x64
+inline RngKey fold_in(RngKey key, std::uint64_t index) {
+  const std::uint64_t k[2] = {key.hi, key.lo}, c[2] = {0, index};
+  std::uint64_t o[2];
+  check(evorl_threefry2x64(k, c, o, 1));
+  return {o[0], o[1]};
+}
+inline RngKey key_from_seed(std::uint64_t seed) {
+  return fold_in({0x9E3779B97F4A7C15ull, 0xBB67AE8584CAA73Bull}, seed);
+}
+
 // StepMetrics / EvalReport (proj/include/evorl/workflow.hpp)
 struct StepMetrics {
   double fitness_mean = 0, fitness_max = 0, fitness_min = 0, sigma = 0;
@@ -135,6 +146,52 @@ class EsWorkflow {
   struct Del {
     void operator()(evorl_es* h) const { evorl_es_destroy(h); }
   };
+  std::unique_ptr<evorl_es, Del> h_;
+};
+
+// ------------------------------------------------------------- CMA-ES
+// CmaState::init / cmaes_ask / cmaes_tell (proj/src/ec.cpp:191-288) on a
+// device state of dimension d; the caller evaluates the candidates.
+class CmaEs {
+ public:
+  CmaEs(std::int64_t d, int pop, int elites, double sigma0, int max_dim = 4096, int eig_every = 1)
+      : d_(d), pop_(pop) {
+    evorl_es* h = nullptr;
+    check(evorl_cma_create(d, pop, elites, sigma0, max_dim, eig_every, &h));
+    h_.reset(h);
+  }
+  // pop x d row-major candidates
+  std::vector<double> ask(RngKey key) {
+    std::vector<double> c((std::size_t)(pop_ * d_));
+    check(evorl_cma_ask(h_.get(), key.hi, key.lo, c.data()));
+    return c;
+  }
+  void tell(const std::vector<double>& candidates, const std::vector<double>& fitness) {
+    if ((std::int64_t)candidates.size() != pop_ * d_ || (int)fitness.size() != pop_)
+      throw std::invalid_argument("cmaes_tell: candidates / fitness size mismatch");
+    check(evorl_cma_tell(h_.get(), candidates.data(), fitness.data()));
+  }
+  std::vector<double> mean() {
+    std::vector<double> v((std::size_t)d_);
+    check(evorl_es_get_mean(h_.get(), v.data()));
+    return v;
+  }
+  void set_mean(const std::vector<double>& v) {
+    if ((std::int64_t)v.size() != d_) throw std::invalid_argument("set_mean: size mismatch");
+    check(evorl_es_set_mean(h_.get(), v.data()));
+  }
+  double sigma() {
+    double s = 0;
+    check(evorl_es_cma_get(h_.get(), nullptr, nullptr, nullptr, nullptr, nullptr, &s, nullptr, nullptr));
+    return s;
+  }
+
+ private:
+  struct Del {
+    void operator()(evorl_es* h) const { evorl_es_destroy(h); }
+  };
+  std::int64_t d_;
+  int pop_;
   std::unique_ptr<evorl_es, Del> h_;
 };
 

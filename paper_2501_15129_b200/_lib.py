@@ -135,6 +135,7 @@ EXPORTS = [
     "evorl_es_device_buffers", "evorl_es_stream", "evorl_es_last_timings",
     "evorl_measure_fp64_peak", "evorl_measure_dmma_peak", "evorl_es_cma_get", "evorl_es_cma_set",
     "evorl_sym_eig", "evorl_es_save", "evorl_es_load", "evorl_batched_rollout_transitions",
+    "evorl_cma_create", "evorl_cma_ask", "evorl_cma_tell",
 ]
 
 _lib = None
@@ -179,6 +180,9 @@ def load() -> C.CDLL:
     L.evorl_es_step.argtypes = [vp, C.POINTER(StepMetricsC)]
     L.evorl_es_evaluate.argtypes = [vp, i32, u64, u64, C.POINTER(dbl), C.POINTER(dbl)]
     L.evorl_es_save.argtypes = [vp, C.c_char_p]
+    L.evorl_cma_create.argtypes = [i64, i32, i32, dbl, i32, i32, C.POINTER(vp)]
+    L.evorl_cma_ask.argtypes = [vp, u64, u64, vp]
+    L.evorl_cma_tell.argtypes = [vp, vp, vp]
     L.evorl_es_load.argtypes = [vp, C.c_char_p]
     L.evorl_es_counters.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
     L.evorl_es_set_counters.argtypes = [vp, i64, i64, i64]

@@ -181,6 +181,7 @@ struct evorl_es {
   float* d_cand_f32 = nullptr;
   unsigned char* d_tc_blocks = nullptr;  // tc team: pre-split layer-1 weights (cand_cap agents)
   int cand_cap = 0;               // agents per materialised chunk (team path)
+  bool cma_only = false;          // evorl_cma_create: a CmaState of dimension d, no env / policy
   // OpenES noise-table mode (proj/src/ec.cpp:50-86): the shared table and
   // this generation's window offsets
   double* d_table = nullptr;
@@ -303,7 +304,10 @@ static int resolve_norm(const evorl_es_config& c) {  // proj/src/workflow.cpp:13
   return EVORL_NORM_VBN;
 }
 
-extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
+static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** out);
+extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) { return es_create(cfg, 0, out); }
+
+static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** out) {
   *out = nullptr;
   if (cfg->algo < 0 || cfg->algo > EVORL_ALGO_CEM) return set_err(EVORL_E_CONFIG, "ec.algo: unknown algorithm");
   if (cfg->env_id != EVORL_ENV_CARTPOLE && cfg->env_id != EVORL_ENV_PENDULUM)
@@ -331,6 +335,10 @@ extern "C" int evorl_es_create(const evorl_es_config* cfg, evorl_es** out) {
     return rc;
   }
   s->d = s->net.d;
+  if (forced_d > 0) {  // CMA-ES free functions: the state's own dimension
+    s->d = forced_d;
+    s->cma_only = true;
+  }
   const bool table = cfg->algo == EVORL_ALGO_OPENES && cfg->openes_noise_table;
   if (table && cfg->openes_noise_table_size < s->d) {  // the reference's span = size - d would wrap (UB)
     delete s;
@@ -556,7 +564,26 @@ static cudaError_t table_offsets(evorl_es* s, int base) {
 }
 
 // EsWorkflow::init (proj/src/workflow_es.cpp:68-85)
+// CmaState::init's matrices (proj/src/ec.cpp:214-223): C = B = I, D = 1, ps = pc = 0
+static int cma_state_init(evorl_es* s) {
+  CmaDev& v = s->cma.dev;
+  const size_t dp2 = (size_t)v.dp * v.dp;
+  std::vector<double> eye(dp2, 0.0);
+  for (int i = 0; i < v.dp; ++i) eye[(size_t)i * v.dp + i] = 1.0;
+  CK(cudaMemcpy(v.C, eye.data(), sizeof(double) * dp2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(v.B, eye.data(), sizeof(double) * dp2, cudaMemcpyHostToDevice));
+  std::vector<double> ones(v.dp, 1.0);
+  CK(cudaMemcpy(v.D, ones.data(), sizeof(double) * v.dp, cudaMemcpyHostToDevice));
+  CK(cudaMemset(v.ps, 0, sizeof(double) * v.dp));
+  CK(cudaMemset(v.pc, 0, sizeof(double) * v.dp));
+  s->cma.sigma = s->cfg.cmaes_sigma0;
+  s->cma.generation = 0;
+  s->cma.recondition_count = 0;
+  return EVORL_OK;
+}
+
 extern "C" int evorl_es_init(evorl_es* s, uint64_t key_hi, uint64_t key_lo) {
+  if (s->cma_only) return set_err(EVORL_E_INVALID_ARGUMENT, "cma-only handle: use evorl_cma_ask / evorl_cma_tell");
   CK(cudaSetDevice(s->cfg.device));
   const DKey key = mk(key_hi, key_lo);
   s->rng = key;
@@ -571,21 +598,8 @@ extern "C" int evorl_es_init(evorl_es* s, uint64_t key_hi, uint64_t key_lo) {
   CK(cudaMemsetAsync(s->d_m, 0, sizeof(double) * s->d, s->stream));
   CK(cudaMemsetAsync(s->d_v, 0, sizeof(double) * s->d, s->stream));
   CK(cudaMemsetAsync(s->d_t, 0, sizeof(long long), s->stream));
-  if (s->cfg.algo == EVORL_ALGO_CMAES) {  // C = B = I, D = 1, ps = pc = 0
-    CmaDev& v = s->cma.dev;
-    const size_t dp2 = (size_t)v.dp * v.dp;
-    std::vector<double> eye(dp2, 0.0);
-    for (int i = 0; i < v.dp; ++i) eye[(size_t)i * v.dp + i] = 1.0;
-    CK(cudaMemcpy(v.C, eye.data(), sizeof(double) * dp2, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(v.B, eye.data(), sizeof(double) * dp2, cudaMemcpyHostToDevice));
-    std::vector<double> ones(v.dp, 1.0);
-    CK(cudaMemcpy(v.D, ones.data(), sizeof(double) * v.dp, cudaMemcpyHostToDevice));
-    CK(cudaMemset(v.ps, 0, sizeof(double) * v.dp));
-    CK(cudaMemset(v.pc, 0, sizeof(double) * v.dp));
-    s->cma.sigma = s->cfg.cmaes_sigma0;
-    s->cma.generation = 0;
-    s->cma.recondition_count = 0;
-  }
+  if (s->cfg.algo == EVORL_ALGO_CMAES)
+    if (int rc = cma_state_init(s)) return rc;
   if (s->cfg.algo == EVORL_ALGO_CEM) {
     std::vector<double> v(s->d, s->cfg.cem_var_init);
     CK(cudaMemcpyAsync(s->d_var, v.data(), sizeof(double) * s->d, cudaMemcpyHostToDevice, s->stream));
@@ -685,8 +699,85 @@ static RolloutArgs rollout_args(const evorl_es* s) {
   return a;
 }
 
+// cmaes_tell (proj/src/ec.cpp:236-288) on the device state: d_fitness (n) and
+// d_cand (n x d) in, mean / paths / C / sigma updated, B and D re-factorised
+// every k-th generation
+static int cma_tell_device(evorl_es* s, int n, cudaStream_t st) {
+  auto& c = s->cma;
+  CmaDev& v = c.dev;
+  const int d = (int)s->d, mu = c.mu, dp = v.dp;
+  CK(run_rank(s->d_fitness, n, 1, s->d_rank, st));
+  CK(run_order_from_rank(s->d_rank, n, s->d_order, st));
+  CK(run_cma_ytop(s->d_cand, s->d_order, mu, d, s->d_mean, c.sigma, c.d_w, v.ytT, v.wyT, st));
+  CK(run_cma_yw_mean(v.ytT, c.d_w, mu, d, c.sigma, v.yw, s->d_mean, st));
+  CK(run_cma_gemv_t(v.B, dp, d, v.yw, v.D, v.t1, st));
+  CK(run_cma_gemv(v.B, dp, d, v.t1, v.cih, st));
+  const double cps = std::sqrt(c.cs * (2.0 - c.cs) * c.mueff);
+  CK(run_cma_ps(v.ps, v.cih, d, c.cs, cps, v.red, st));
+  double nrm2 = 0.0;
+  CK(cudaMemcpyAsync(&nrm2, v.red, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double gen1 = (double)(c.generation + 1);
+  const double ps_norm = std::sqrt(nrm2);
+  const bool hsig = ps_norm / std::sqrt(1.0 - std::pow(1.0 - c.cs, 2.0 * gen1)) <
+                    (1.4 + 2.0 / ((double)d + 1.0)) * c.chi_n;
+  const double cpc = hsig ? std::sqrt(c.cc * (2.0 - c.cc) * c.mueff) : 0.0;
+  CK(run_cma_pc(v.pc, v.yw, d, c.cc, cpc, st));
+  // C' = (1-c1-cmu) C + c1 (pc pc^T + dhsig C) + cmu sum_i w_i y_i y_i^T,
+  // the rank-mu sum as a K = mu DMMA GEMM with the blend in its epilogue
+  GemmEpi epi{};
+  epi.mode = GEMM_RANKMU;
+  epi.out = v.W;
+  epi.ldo = dp;
+  epi.Cold = v.C;
+  epi.pc = v.pc;
+  epi.a = 1.0 - c.c1 - c.cmu;
+  epi.c1 = c.c1;
+  epi.dh = (hsig ? 0.0 : 1.0) * c.cc * (2.0 - c.cc);
+  epi.cmu = c.cmu;
+  CK(run_gemm_nt(d, d, mu, v.wyT, mu, v.ytT, mu, epi, st));
+  CK(run_cma_symmetrize(v.W, v.C, d, dp, st));
+  c.sigma *= std::exp((c.cs / c.ds) * (ps_norm / c.chi_n - 1.0));
+  c.generation += 1;
+  // re-factorise; re-condition when eigenvalues fall to <= 0
+  // (EXTENSION: only every cmaes_eig_every-th generation; 1 = reference)
+  // k = 0: Hansen's lazy gap max(1, floor(1 / (10 d (c1 + cmu)))), which
+  // keeps the amortised eigendecomposition at O(d^2) per generation
+  const int k_eig = s->cfg.cmaes_eig_every > 0
+                        ? s->cfg.cmaes_eig_every
+                        : std::max(1, (int)std::floor(1.0 / (10.0 * d * (c.c1 + c.cmu))));
+  if (c.generation % k_eig != 0) return EVORL_OK;
+  double evmin = 0.0;
+  int sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st, v.B);
+  if (sw < 0) return set_err(EVORL_E_CUDA, "cmaes: eigensolver failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (evmin <= 0.0) {
+    CK(run_cma_add_diag(v.C, d, dp, 1e-10 - evmin, st));
+    sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st, v.B);
+    if (sw < 0) return set_err(EVORL_E_CUDA, "cmaes: eigensolver failed");
+    c.recondition_count += 1;
+  }
+  c.last_sweeps = sw;
+  CK(run_cma_sqrt_pos(v.evals, v.D, d, st));
+  return EVORL_OK;
+}
+
+// cmaes_ask (proj/src/ec.cpp:226-234): d_cand = ((z .* D^T) B^T) sigma + mean
+static int cma_ask_device(evorl_es* s, DKey key, int n, cudaStream_t st) {
+  CmaDev& v = s->cma.dev;
+  CK(run_cma_zD(key, n, (int)s->d, v.D, v.zD, st));
+  GemmEpi epi{};
+  epi.mode = GEMM_ASK;
+  epi.out = s->d_cand;
+  epi.ldo = s->d;
+  epi.sigma = s->cma.sigma;
+  epi.mean = s->d_mean;
+  CK(run_gemm_nt(n, (int)s->d, (int)s->d, v.zD, s->d, v.B, v.dp, epi, st));
+  return EVORL_OK;
+}
+
 // ask + rollout + fitness of agents [a0, a1)
 extern "C" int evorl_es_phase_rollout(evorl_es* s) {
+  if (s->cma_only) return set_err(EVORL_E_INVALID_ARGUMENT, "cma-only handle: use evorl_cma_ask / evorl_cma_tell");
   if (!s->initialised) return set_err(EVORL_E_INVALID_ARGUMENT, "evorl_es_step before evorl_es_init");
   CK(cudaSetDevice(s->cfg.device));
   int rc = check_ask(s);
@@ -703,16 +794,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
   if (s->cfg.algo == EVORL_ALGO_CMAES) {
     // cmaes_ask (proj/src/ec.cpp:226-234): all n candidates (every rank needs
     // the elites' rows for the tell), Y = ((z .* D^T) B^T) sigma + mean
-    CmaDev& v = s->cma.dev;
-    const int n = s->cfg.pop;
-    CK(run_cma_zD(s->ask_key, n, (int)s->d, v.D, v.zD, s->stream));
-    GemmEpi epi{};
-    epi.mode = GEMM_ASK;
-    epi.out = s->d_cand;
-    epi.ldo = s->d;
-    epi.sigma = s->cma.sigma;
-    epi.mean = s->d_mean;
-    CK(run_gemm_nt(n, (int)s->d, (int)s->d, v.zD, s->d, v.B, v.dp, epi, s->stream));
+    if (int rc = cma_ask_device(s, s->ask_key, s->cfg.pop, s->stream)) return rc;
     a.par.src = SRC_EXPLICIT;
     a.par.params = s->d_cand + (long long)s->a0 * s->d;
     CK(cudaEventRecord(s->ev_r0, s->stream));
@@ -860,65 +942,8 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       break;
     }
     case EVORL_ALGO_CMAES: {  // cmaes_tell (proj/src/ec.cpp:236-288), replicated on every rank
-      auto& c = s->cma;
-      CmaDev& v = c.dev;
-      const int d = (int)s->d, mu = c.mu, dp = v.dp;
-      CK(run_rank(s->d_fitness, n, 1, s->d_rank, st));
-      CK(run_order_from_rank(s->d_rank, n, s->d_order, st));
-      CK(run_cma_ytop(s->d_cand, s->d_order, mu, d, s->d_mean, c.sigma, c.d_w, v.ytT, v.wyT, st));
-      CK(run_cma_yw_mean(v.ytT, c.d_w, mu, d, c.sigma, v.yw, s->d_mean, st));
-      CK(run_cma_gemv_t(v.B, dp, d, v.yw, v.D, v.t1, st));
-      CK(run_cma_gemv(v.B, dp, d, v.t1, v.cih, st));
-      const double cps = std::sqrt(c.cs * (2.0 - c.cs) * c.mueff);
-      CK(run_cma_ps(v.ps, v.cih, d, c.cs, cps, v.red, st));
-      double nrm2 = 0.0;
-      CK(cudaMemcpyAsync(&nrm2, v.red, sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      const double gen1 = (double)(c.generation + 1);
-      const double ps_norm = std::sqrt(nrm2);
-      const bool hsig = ps_norm / std::sqrt(1.0 - std::pow(1.0 - c.cs, 2.0 * gen1)) <
-                        (1.4 + 2.0 / ((double)d + 1.0)) * c.chi_n;
-      const double cpc = hsig ? std::sqrt(c.cc * (2.0 - c.cc) * c.mueff) : 0.0;
-      CK(run_cma_pc(v.pc, v.yw, d, c.cc, cpc, st));
-      // C' = (1-c1-cmu) C + c1 (pc pc^T + dhsig C) + cmu sum_i w_i y_i y_i^T,
-      // the rank-mu sum as a K = mu DMMA GEMM with the blend in its epilogue
-      GemmEpi epi{};
-      epi.mode = GEMM_RANKMU;
-      epi.out = v.W;
-      epi.ldo = dp;
-      epi.Cold = v.C;
-      epi.pc = v.pc;
-      epi.a = 1.0 - c.c1 - c.cmu;
-      epi.c1 = c.c1;
-      epi.dh = (hsig ? 0.0 : 1.0) * c.cc * (2.0 - c.cc);
-      epi.cmu = c.cmu;
-      CK(run_gemm_nt(d, d, mu, v.wyT, mu, v.ytT, mu, epi, st));
-      CK(run_cma_symmetrize(v.W, v.C, d, dp, st));
-      c.sigma *= std::exp((c.cs / c.ds) * (ps_norm / c.chi_n - 1.0));
-      c.generation += 1;
-      // re-factorise; re-condition when eigenvalues fall to <= 0
-      // (EXTENSION: only every cmaes_eig_every-th generation; 1 = reference)
-      // k = 0: Hansen's lazy gap max(1, floor(1 / (10 d (c1 + cmu)))), which
-      // keeps the amortised eigendecomposition at O(d^2) per generation
-      const int k_eig = s->cfg.cmaes_eig_every > 0
-                            ? s->cfg.cmaes_eig_every
-                            : std::max(1, (int)std::floor(1.0 / (10.0 * d * (c.c1 + c.cmu))));
-      if (c.generation % k_eig != 0) {
-        sigma = c.sigma;
-        break;
-      }
-      double evmin = 0.0;
-      int sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st, v.B);
-      if (sw < 0) return set_err(EVORL_E_CUDA, "cmaes: eigensolver failed: %s", cudaGetErrorString(cudaGetLastError()));
-      if (evmin <= 0.0) {
-        CK(run_cma_add_diag(v.C, d, dp, 1e-10 - evmin, st));
-        sw = sym_eig_jacobi(v, v.C, d, &evmin, v.B, v.evals, st, v.B);
-        if (sw < 0) return set_err(EVORL_E_CUDA, "cmaes: eigensolver failed");
-        c.recondition_count += 1;
-      }
-      c.last_sweeps = sw;
-      CK(run_cma_sqrt_pos(v.evals, v.D, d, st));
-      sigma = c.sigma;
+      if (int rc = cma_tell_device(s, n, st)) return rc;
+      sigma = s->cma.sigma;
       break;
     }
     case EVORL_ALGO_CEM: {
@@ -953,6 +978,61 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
     out->sigma = sigma;
     out->update_skipped = ars && s->h->sel.skipped ? 1.0 : 0.0;
   }
+  return EVORL_OK;
+}
+
+// ------------------------------------------------- CMA-ES free functions
+// CmaState::init / cmaes_ask / cmaes_tell (proj/src/ec.cpp:191-288) on a device
+// state of dimension d with no env or policy attached (the free-function seam,
+// proj/include/evorl/ec.hpp:107-125).  The state (mean, sigma, C, B, D, ps, pc,
+// generation, recondition_count) is read / written with evorl_es_get/set_mean
+// and evorl_es_cma_get/set; release with evorl_es_destroy.
+extern "C" int evorl_cma_create(int64_t d, int32_t pop, int32_t elites, double sigma0, int32_t max_dim,
+                                int32_t eig_every, evorl_es** out) {
+  *out = nullptr;
+  if (d < 1) return set_err(EVORL_E_INVALID_ARGUMENT, "cmaes: dimension must be positive");
+  evorl_es_config cfg;
+  evorl_es_default_config(&cfg);
+  cfg.algo = EVORL_ALGO_CMAES;
+  cfg.env_id = EVORL_ENV_PENDULUM;  // not used by a cma-only handle
+  cfg.n_hidden = 0;
+  cfg.allow_linear = 1;
+  cfg.pop = pop;
+  cfg.cmaes_elites = elites;
+  cfg.cmaes_sigma0 = sigma0;
+  cfg.cmaes_max_dim = max_dim;
+  cfg.cmaes_eig_every = eig_every;
+  cfg.obs_norm_mode = EVORL_NORM_NONE;
+  evorl_es* s = nullptr;
+  if (int rc = es_create(&cfg, d, &s)) return rc;
+  if (int rc = cma_state_init(s)) {
+    evorl_es_destroy(s);
+    return rc;
+  }
+  CK(cudaMemset(s->d_mean, 0, sizeof(double) * d));
+  s->initialised = true;
+  *out = s;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_cma_ask(evorl_es* s, uint64_t key_hi, uint64_t key_lo, double* candidates) {
+  if (!s->cma_only) return set_err(EVORL_E_INVALID_ARGUMENT, "evorl_cma_ask needs an evorl_cma_create handle");
+  CK(cudaSetDevice(s->cfg.device));
+  const int n = s->cfg.pop;
+  if (int rc = cma_ask_device(s, mk(key_hi, key_lo), n, s->stream)) return rc;
+  CK(cudaMemcpyAsync(candidates, s->d_cand, sizeof(double) * n * s->d, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return EVORL_OK;
+}
+
+extern "C" int evorl_cma_tell(evorl_es* s, const double* candidates, const double* fitness) {
+  if (!s->cma_only) return set_err(EVORL_E_INVALID_ARGUMENT, "evorl_cma_tell needs an evorl_cma_create handle");
+  CK(cudaSetDevice(s->cfg.device));
+  const int n = s->cfg.pop;
+  CK(cudaMemcpyAsync(s->d_cand, candidates, sizeof(double) * n * s->d, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(s->d_fitness, fitness, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+  if (int rc = cma_tell_device(s, n, s->stream)) return rc;
+  CK(cudaStreamSynchronize(s->stream));
   return EVORL_OK;
 }
 
@@ -1130,6 +1210,7 @@ extern "C" int evorl_es_set_obs_norm(evorl_es* s, const evorl_obs_norm* o) {
 // Workflow::evaluate -> eval_params(m=1, e=episodes) (proj/src/workflow.cpp:103-129)
 extern "C" int evorl_es_evaluate(evorl_es* s, int32_t episodes, uint64_t key_hi, uint64_t key_lo,
                                  double* mean_return, double* return_std) {
+  if (s->cma_only) return set_err(EVORL_E_INVALID_ARGUMENT, "cma-only handle has no policy to evaluate");
   CK(cudaSetDevice(s->cfg.device));
   if (episodes < 1) return set_err(EVORL_E_INVALID_ARGUMENT, "episodes must be positive");
   SmemPlan plan{};

@@ -278,6 +278,61 @@ class EsWorkflow:
                                       int(recondition_count)))
 
 
+class CmaEs:
+    """CMA-ES as free functions on a device state (CmaState::init /
+    cmaes_ask / cmaes_tell, proj/src/ec.cpp:191-288): no env or policy, the
+    caller supplies the fitness.  State is HBM-resident between calls."""
+
+    def __init__(self, dim: int, pop: int, elites: int = 0, sigma0: float = 0.5, max_dim: int = 4096,
+                 eig_every: int = 1, mean0=None):
+        self.L = _lib.load()
+        h = C.c_void_p()
+        check(self.L.evorl_cma_create(int(dim), int(pop), int(elites), float(sigma0), int(max_dim),
+                                      int(eig_every), C.byref(h)))
+        self.h = h
+        self.dim, self.pop = int(dim), int(pop)
+        if mean0 is not None:
+            self.set_mean(mean0)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.evorl_es_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def ask(self, key) -> np.ndarray:
+        hi, lo = _key(key)
+        out = np.empty((self.pop, self.dim), np.float64)
+        check(self.L.evorl_cma_ask(self.h, hi, lo, _p(out)))
+        return out
+
+    def tell(self, candidates, fitness) -> None:
+        x = np.ascontiguousarray(candidates, np.float64)
+        f = np.ascontiguousarray(fitness, np.float64)
+        if x.shape != (self.pop, self.dim) or f.shape != (self.pop,):
+            raise ValueError("cmaes_tell: candidates / fitness shape mismatch")
+        check(self.L.evorl_cma_tell(self.h, _p(x), _p(f)))
+
+    def mean(self) -> np.ndarray:
+        m = np.empty(self.dim)
+        check(self.L.evorl_es_get_mean(self.h, _p(m)))
+        return m
+
+    def set_mean(self, m) -> None:
+        m = np.ascontiguousarray(m, np.float64)
+        if m.shape != (self.dim,):
+            raise ValueError("set_mean: size mismatch")
+        check(self.L.evorl_es_set_mean(self.h, _p(m)))
+
+    state = EsWorkflow.cma_state
+    set_state = EsWorkflow.set_cma_state
+
+
 # -------------------------------------------------------------- stateless
 def mlp_desc(input_dim: int, hidden: Sequence[int], output_dim: int, head: int,
              tanh_scale: float = 1.0, allow_linear: bool = False) -> _lib.MlpDesc:

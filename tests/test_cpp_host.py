@@ -39,6 +39,11 @@ int main() {
     evorl_env_desc env{EVORL_ENV_PENDULUM, 1, 10};
     evorl_mlp_desc net{};
     (void)eb::batched_rollout(env, net, nullptr, f, 1, 1, 1, {5, 6});
+    eb::CmaEs cma(4, 8, 4, 0.2);
+    std::vector<double> cand = cma.ask(eb::fold_in(eb::key_from_seed(1), 2));
+    cma.tell(cand, std::vector<double>(8, 0.0));
+    cma.set_mean(cma.mean());
+    (void)cma.sigma();
   } catch (const eb::DeviceError&) { return 3; }
   catch (const std::exception&) { return 4; }
   return 0;
@@ -99,3 +104,26 @@ def test_cpp_host_matches_python_host():
     ev = lines[3].split()
     assert float.fromhex(ev[2]) == mr and float.fromhex(ev[4]) == sd
     assert lines[4] == "counters %d %d %d" % g.counters()
+
+
+@pytest.mark.gpu
+def test_cpp_cma_free_functions_match_python():
+    """proj/tests/test_ec.cpp:282-297 through the C++ CmaEs wrapper; the same
+    loop through the Python binding gives the bit-identical final state."""
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_ffi as oracle
+    import paper_2501_15129_b200 as evb
+    _build()
+    r = subprocess.run([EXE, "cma-sphere"], capture_output=True, text=True, check=True)
+    _, _, dist, _, sigma = r.stdout.split()
+    target = np.array([0.7, -0.3, 0.5, 0.1, -0.8, 0.25, -0.4, 0.6])
+    cma = evb.CmaEs(8, 16, 8, 0.3)
+    for g in range(200):
+        k = oracle.fold_in(oracle.key_from_seed(84), g)
+        cand = cma.ask((k.hi, k.lo))
+        cma.tell(cand, -((cand - target) ** 2).sum(1))
+    d = cma.mean() - target
+    assert float.fromhex(dist) == np.sqrt(np.sum(d * d)) or abs(float.fromhex(dist) - np.linalg.norm(d)) < 1e-15
+    assert float.fromhex(dist) < 1e-3
+    assert float.fromhex(sigma) == cma.state()["sigma"]
