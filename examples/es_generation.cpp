@@ -5,6 +5,8 @@
 // comparison) and the final counters.
 //
 //   es_generation [algo] [pop] [gens] [hidden0] [hidden1] [episodes] [precision] [checkpoint]
+//   es_generation learn <out_dir>      learn() + metrics.jsonl / timings.log / checkpoint.bin
+//   es_generation cma-sphere           the reference's CMA offset-sphere test via CmaEs
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +20,34 @@
 int main(int argc, char** argv) {
   namespace eb = evorl_b200;
   const char* algo = argc > 1 ? argv[1] : "openes";
+  if (!std::strcmp(algo, "learn") && argc > 2) {  // learn() + metrics stream (proj/src/workflow.cpp:46-68)
+    try {
+      evorl_es_config c = eb::default_config();
+      c.env_id = EVORL_ENV_PENDULUM;
+      c.fixed_horizon = 1;
+      c.max_episode_steps = 60;
+      c.pop = 32;
+      c.n_hidden = 2;
+      c.hidden[0] = c.hidden[1] = 16;
+      c.vbn_samples = 300;
+      const std::string dir = argv[2];
+      const eb::RngKey root = eb::key_from_seed(3);
+      eb::EsWorkflow wf(c);
+      wf.init(root);
+      eb::MetricsWriter mw(dir + "/metrics.jsonl", dir + "/timings.log");
+      mw.write_header("es", {{"workflow", "es"}, {"seed", "3"}, {"ec.pop", "32"}});
+      eb::LearnOptions lo;
+      lo.budget.iterations = 5;
+      lo.eval_interval = 2;
+      lo.eval_episodes = 8;
+      lo.checkpoint_path = dir + "/checkpoint.bin";
+      eb::learn(wf, root, lo, mw);
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "error: %s\n", e.what());
+      return 2;
+    }
+    return 0;
+  }
   if (!std::strcmp(algo, "cma-sphere")) {  // proj/tests/test_ec.cpp:282-297 through the free functions
     try {
       const double target[8] = {0.7, -0.3, 0.5, 0.1, -0.8, 0.25, -0.4, 0.6};

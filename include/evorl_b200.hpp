@@ -5,10 +5,17 @@
 // Link with -levorl_b200.
 #pragma once
 
+#include <charconv>
+#include <chrono>
+#include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <fstream>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "evorl_b200.h"
@@ -231,6 +238,158 @@ inline RolloutResult batched_rollout(const evorl_env_desc& env, const evorl_mlp_
   check(evorl_batched_rollout(&env, &net, norm, params.data(), m, envs_per_agent, count, key.hi, key.lo,
                               precision, r.returns.data(), r.steps.data(), nullptr));
   return r;
+}
+
+// ------------------------------------------------------ metrics stream
+// MetricsWriter (proj/include/evorl/metrics.hpp, proj/src/metrics.cpp:12-67):
+// metrics.jsonl (one nlohmann::json dump() per line: keys sorted, no
+// whitespace, doubles shortest round-trip placed as nlohmann's format_buffer
+// does, non-finite -> null) and the timings sidecar.  paper_2501_15129_b200/
+// learn.py writes the same bytes.
+namespace detail {
+inline std::string json_double(double x) {
+  if (!std::isfinite(x)) return "null";
+  if (x == 0.0) return std::signbit(x) ? "-0.0" : "0.0";
+  char buf[64];
+  const auto r = std::to_chars(buf, buf + sizeof buf, std::fabs(x), std::chars_format::scientific);
+  const std::string sci(buf, r.ptr);  // d[.ddd]e[+-]XX, shortest round-trip
+  const std::size_t epos = sci.find('e');
+  std::string ds = sci.substr(0, epos);
+  if (ds.size() > 1) ds.erase(1, 1);  // drop the '.'
+  while (ds.size() > 1 && ds.back() == '0') ds.pop_back();
+  const int k = (int)ds.size(), n = std::atoi(sci.c_str() + epos + 1) + 1;
+  std::string out = x < 0 ? "-" : "";
+  if (k <= n && n <= 15) return out + ds + std::string((std::size_t)(n - k), '0') + ".0";
+  if (0 < n && n <= 15) return out + ds.substr(0, (std::size_t)n) + "." + ds.substr((std::size_t)n);
+  if (-4 < n && n <= 0) return out + "0." + std::string((std::size_t)-n, '0') + ds;
+  const int e = n - 1;
+  out += k == 1 ? ds : ds.substr(0, 1) + "." + ds.substr(1);
+  char eb[16];
+  std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+  return out + eb;
+}
+inline std::string json_string(const std::string& s) {
+  std::string o = "\"";
+  for (unsigned char c : s) {
+    switch (c) {
+      case '"': o += "\\\""; break;
+      case '\\': o += "\\\\"; break;
+      case '\b': o += "\\b"; break;
+      case '\f': o += "\\f"; break;
+      case '\n': o += "\\n"; break;
+      case '\r': o += "\\r"; break;
+      case '\t': o += "\\t"; break;
+      default:
+        if (c < 0x20) {
+          char u[16];
+          std::snprintf(u, sizeof u, "\\u%04x", c);
+          o += u;
+        } else {
+          o += (char)c;
+        }
+    }
+  }
+  return o + "\"";
+}
+// a flat JSON object: key -> already-serialised value, emitted in std::map order
+inline std::string json_object(const std::map<std::string, std::string>& kv) {
+  std::string o = "{";
+  for (const auto& [k, v] : kv) {
+    if (o.size() > 1) o += ',';
+    o += json_string(k) + ":" + v;
+  }
+  return o + "}";
+}
+}  // namespace detail
+
+class MetricsWriter {
+ public:
+  MetricsWriter(const std::string& metrics_path, const std::string& timings_path)
+      : metrics_(metrics_path, std::ios::trunc), timings_(timings_path, std::ios::trunc) {
+    if (!metrics_) throw std::runtime_error("cannot open metrics file: " + metrics_path);
+    if (!timings_) throw std::runtime_error("cannot open timings file: " + timings_path);
+  }
+  void write_header(const std::string& workflow_id, const std::map<std::string, std::string>& config) {
+    std::map<std::string, std::string> conf;
+    for (const auto& [k, v] : config) conf[k] = detail::json_string(v);
+    metrics_ << detail::json_object({{"type", "\"header\""},
+                                     {"workflow", detail::json_string(workflow_id)},
+                                     {"config", detail::json_object(conf)}})
+             << '\n';
+    flush();
+  }
+  void write_step(std::int64_t iteration, std::int64_t env_steps, std::int64_t episodes,
+                  std::int64_t rl_updates, const std::vector<std::pair<std::string, double>>& scalars) {
+    auto rec = base("step", iteration, env_steps, episodes, rl_updates);
+    for (const auto& [k, v] : scalars) rec[k] = detail::json_double(v);
+    metrics_ << detail::json_object(rec) << '\n';
+  }
+  void write_eval(std::int64_t iteration, std::int64_t env_steps, std::int64_t episodes,
+                  std::int64_t rl_updates, double mean_return, double return_std, int eval_episodes) {
+    auto rec = base("eval", iteration, env_steps, episodes, rl_updates);
+    rec["eval/episode_return_mean"] = detail::json_double(mean_return);
+    rec["eval/episode_return_std"] = detail::json_double(return_std);
+    rec["eval/episodes"] = std::to_string(eval_episodes);
+    metrics_ << detail::json_object(rec) << '\n';
+    flush();
+  }
+  void write_timing(std::int64_t iteration, double wall_ms) { timings_ << iteration << '\t' << wall_ms << '\n'; }
+  void flush() {
+    metrics_.flush();
+    timings_.flush();
+  }
+
+ private:
+  static std::map<std::string, std::string> base(const char* type, std::int64_t it, std::int64_t steps,
+                                                 std::int64_t eps, std::int64_t rl) {
+    return {{"type", detail::json_string(type)}, {"iteration", std::to_string(it)},
+            {"env_steps", std::to_string(steps)}, {"episodes", std::to_string(eps)},
+            {"rl_updates", std::to_string(rl)}};
+  }
+  std::ofstream metrics_, timings_;
+};
+
+// Budget / LearnOptions / learn (proj/include/evorl/workflow.hpp:74-98,
+// proj/src/workflow.cpp:46-68) over the device workflow; `rng` is the root
+// key the workflow was initialised with (eval key = fold_in(fold_in(rng, 1), it)).
+struct Budget {
+  std::int64_t iterations = 0, episodes = 0, env_steps = 0;  // 0 = off
+  bool reached(std::int64_t it, std::int64_t steps, std::int64_t eps) const {
+    return (iterations > 0 && it >= iterations) || (episodes > 0 && eps >= episodes) ||
+           (env_steps > 0 && steps >= env_steps);
+  }
+};
+struct LearnOptions {
+  Budget budget;
+  int eval_interval = 10;
+  int eval_episodes = 128;
+  int checkpoint_interval = 0;
+  std::string checkpoint_path;
+};
+inline std::vector<std::pair<std::string, double>> step_scalars(const StepMetrics& m) {
+  // EsWorkflow::step's StepMetrics (proj/src/workflow_es.cpp:140-169)
+  return {{"es/sigma", m.sigma}, {"fitness/mean", m.fitness_mean}, {"fitness/max", m.fitness_max},
+          {"fitness/min", m.fitness_min}, {"es/update_skipped", m.update_skipped ? 1.0 : 0.0}};
+}
+inline void learn(EsWorkflow& wf, RngKey rng, const LearnOptions& opt, MetricsWriter& metrics) {
+  using clock = std::chrono::steady_clock;
+  std::int64_t it = 0, steps = 0, eps = 0;
+  for (wf.counters(&it, &steps, &eps); !opt.budget.reached(it, steps, eps);) {
+    const auto t0 = clock::now();
+    const StepMetrics sm = wf.step();
+    const double ms = std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+    wf.counters(&it, &steps, &eps);
+    metrics.write_step(it, steps, eps, 0, step_scalars(sm));
+    metrics.write_timing(it, ms);
+    if (opt.eval_interval > 0 && it % opt.eval_interval == 0) {
+      const EvalReport er = wf.evaluate(opt.eval_episodes, fold_in(fold_in(rng, 1), (std::uint64_t)it));
+      metrics.write_eval(it, steps, eps, 0, er.mean_return, er.return_std, er.episodes);
+    }
+    if (opt.checkpoint_interval > 0 && !opt.checkpoint_path.empty() && it % opt.checkpoint_interval == 0)
+      wf.save(opt.checkpoint_path);
+  }
+  if (!opt.checkpoint_path.empty()) wf.save(opt.checkpoint_path);
+  metrics.flush();
 }
 
 }  // namespace evorl_b200
