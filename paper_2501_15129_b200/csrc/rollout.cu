@@ -716,6 +716,428 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   if constexpr (C > 1) cluster_sync_all();  // no CTA may exit while peers still address its SMEM
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined fp64 DMMA team (the fp64 parity path of 2-hidden-layer policies
+// with ET = 16 lanes, BASELINE config 3).  The plain cluster team runs one
+// serial chain per step -- layer 0, the DMMA slice GEMM, the output exchange,
+// then the fp64 env on 16 threads -- so the FP64 tensor pipe idles for the
+// env / exchange half of every step (one CTA per SM: the weight slice fills
+// SMEM).  Here the 16 lanes are two independent groups of 8 and the CTA is
+// warp-specialised: 8 compute warps run group A's layers while a 9th (env)
+// warp steps group B's environments, then the roles swap, so the env, the
+// DSMEM exchange latency and the GEMMs of the other group overlap.
+//   compute warps: [x0(g) ready] L0(g) | L1(g) | out-partial(g) -> st.async
+//   env warp     : [partials(g) landed] head, env_step, observe -> x0(g)
+// Handshakes: named barrier 1+g (env arrives, compute syncs) for x0 / the
+// group-alive flag; the output partials ride st.async + mbarrier complete_tx
+// (double-buffered by step parity) exactly as in the plain team.  Groups are
+// 8 lanes = one n8 tile of mma.m8n8k4, activation rows 8 doubles apart
+// (conflict-free fragment loads).  Numerics per lane are the plain team's.
+constexpr int PIPE_EW = 4;  // env warps: one per SM sub-partition, so the env's fp64
+                             // work does not pile onto one sub-partition's FP64 pipe
+constexpr int PIPE_THREADS = ROLLOUT_THREADS + 32 * PIPE_EW;
+constexpr int PG = 8;                  // lanes per group
+constexpr int PIPE_CHAINS = 4;         // independent DMMA accumulator chains per warp tile
+constexpr int PIPE_LPW = PG / PIPE_EW;  // lanes of one group per env warp
+
+EVB_DEV void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+EVB_DEV void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// 8 weight rows x 8 lanes over K; x is [K][8]; returns the D fragment
+// (row g, lanes 2t, 2t+1).  Four accumulator chains: a warp owns one n8
+// tile, so the chains are its only DMMA latency cover.
+EVB_DEV void dmma_tile8(const double* __restrict__ wb, int WS, int K, const double* __restrict__ x, int g,
+                        int t, double& d0, double& d1) {
+  constexpr int NC = PIPE_CHAINS;
+  double acc[NC][2];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) acc[q][0] = acc[q][1] = 0.0;
+  int k = 0;
+  for (; k + 4 * NC <= K; k += 4 * NC) {
+    double a[NC], b[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      a[q] = wb[(size_t)(k + 4 * q + t) * WS];
+      b[q] = x[(k + 4 * q + t) * PG + g];
+    }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) dmma(acc[q][0], acc[q][1], a[q], b[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {  // remainder: at most NC - 1 full k4 steps + one partial
+    const int kk = k + 4 * q + t;
+    if (k + 4 * q < K) {
+      const bool in = kk < K;
+      dmma(acc[q][0], acc[q][1], in ? wb[(size_t)kk * WS] : 0.0, in ? x[kk * PG + g] : 0.0);
+    }
+  }
+#pragma unroll
+  for (int w = 1; w < NC; w <<= 1)
+#pragma unroll
+    for (int q = 0; q < NC; q += 2 * w) {
+      acc[q][0] += acc[q + w][0];
+      acc[q][1] += acc[q + w][1];
+    }
+  d0 = acc[0][0];
+  d1 = acc[0][1];
+}
+
+// bias + ReLU + store of one tile; returns the lanes with an infinite activation
+EVB_DEV uint32_t tile8_epilogue(double d0, double d1, int row, int nrows, const double* bs, double* h, int t) {
+  if (row >= nrows) return 0u;
+  const double b = bs[row];
+  const double z0 = d0 + b, z1 = d1 + b;
+  const double h0 = z0 > 0.0 ? z0 : 0.0, h1 = z1 > 0.0 ? z1 : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
+  *reinterpret_cast<double2*>(h + row * PG + 2 * t) = make_double2(h0, h1);
+  return (h0 == INFINITY ? 1u << (2 * t) : 0u) | (h1 == INFINITY ? 2u << (2 * t) : 0u);
+}
+
+template <int C>
+__global__ void __launch_bounds__(PIPE_THREADS, 1) rollout_pipe_kernel(const __grid_constant__ RolloutArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemPlan& S = A.plan;
+  const NetDesc& N = A.net;
+  const EnvDesc& E = A.env;
+  const int tid = threadIdx.x;
+  const int crank = (int)cluster_ctarank();
+  const int team = blockIdx.x / C;
+  const int agent_local = team / A.groups;
+  const int group = team % A.groups;
+  const int agent = A.agent_offset + agent_local;
+  const int L = 3, O = N.dims[3];
+  const int K0 = N.dims[0], W0 = N.dims[1], W1 = N.dims[2];
+  const int RS1 = S.RS[1], r01 = crank * RS1, RSv1 = max(0, min(RS1, W1 - r01));
+
+  // ------------------------------------------------------------ prologue
+  for (int i = tid; i < S.bytes / 4; i += PIPE_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  __syncthreads();
+  {
+    double* W0s = reinterpret_cast<double*>(smem + S.off_w[0]);
+    double* b0s = reinterpret_cast<double*>(smem + S.off_b[0]);
+    for (int i = tid; i < K0 * W0; i += PIPE_THREADS) {
+      const int k = i / W0, r = i % W0;
+      W0s[k * S.WS[0] + r] = param_value(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W0 + r);
+    }
+    for (int r = tid; r < W0; r += PIPE_THREADS)
+      b0s[r] = param_value(A.par, N.d, agent_local, agent, N.b_off[0] + r);
+    double* W1s = reinterpret_cast<double*>(smem + S.off_w[1]);
+    double* b1s = reinterpret_cast<double*>(smem + S.off_b[1]);
+    for (int i = tid; i < W0 * RSv1; i += PIPE_THREADS) {
+      const int k = i / RSv1, r = i % RSv1;
+      W1s[(size_t)k * S.WS[1] + r] =
+          param_value(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W1 + r01 + r);
+    }
+    for (int r = tid; r < RSv1; r += PIPE_THREADS)
+      b1s[r] = param_value(A.par, N.d, agent_local, agent, N.b_off[1] + r01 + r);
+    double* Wo = reinterpret_cast<double*>(smem + S.off_wout);
+    double* bo = reinterpret_cast<double*>(smem + S.off_bout);
+    for (int i = tid; i < RSv1 * O; i += PIPE_THREADS) {
+      const int k = i / O, o = i % O;
+      Wo[i] = param_value(A.par, N.d, agent_local, agent, N.w_off[2] + (long long)(r01 + k) * O + o);
+    }
+    for (int o = tid; o < O; o += PIPE_THREADS) bo[o] = param_value(A.par, N.d, agent_local, agent, N.b_off[2] + o);
+  }
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(smem + S.off_bar);  // [group][parity]
+  int* alive_flag = reinterpret_cast<int*>(smem + S.off_bar + 32);  // [group][env warp]
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&xbar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_sync_all();
+
+  double* x0 = reinterpret_cast<double*>(smem + S.off_x0);       // [group][4][8]
+  double* pout0 = reinterpret_cast<double*>(smem + S.off_pout);  // [group][parity][C][(O+1)*8]
+  uint32_t* mask0 = reinterpret_cast<uint32_t*>(smem + S.off_mask);  // [group][parity][2]
+  const int OE = O * PG, OE1 = (O + 1) * PG;
+  const uint32_t xbytes = (uint32_t)(C * OE1 * sizeof(double));
+
+#ifdef EVB_TC_PROFILE
+  unsigned long long rk_prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long rk_prev = clock64();
+#endif
+  if (tid < ROLLOUT_THREADS) {
+    // ====================================================== compute warps
+    const int warp = tid >> 5, lane = tid & 31;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const double* W0s = reinterpret_cast<const double*>(smem + S.off_w[0]);
+    const double* b0s = reinterpret_cast<const double*>(smem + S.off_b[0]);
+    const double* W1s = reinterpret_cast<const double*>(smem + S.off_w[1]);
+    const double* b1s = reinterpret_cast<const double*>(smem + S.off_b[1]);
+    const double* Wo = reinterpret_cast<const double*>(smem + S.off_wout);
+    double* h0 = reinterpret_cast<double*>(smem + S.off_h[0]);
+    double* opart = reinterpret_cast<double*>(smem + S.off_part);  // [warp][o][8 lanes]
+    int alive = 3;  // bit g: group g still has active lanes
+    for (int it = 0;; ++it) {
+      const int par = it & 1;
+#pragma unroll 1
+      for (int gq = 0; gq < 2; ++gq) {
+        if (!((alive >> gq) & 1)) continue;
+        uint32_t* cm = mask0 + (gq * 2 + par) * 2;
+        if (tid < 2) cm[tid] = 0u;  // last read by this group's output pass two steps ago
+        RK_MARK(7);
+        named_sync(1 + gq, PIPE_THREADS);  // x0(g) of this step + alive flag
+        RK_MARK(0);
+        int any_alive = 0;
+#pragma unroll
+        for (int w = 0; w < PIPE_EW; ++w) any_alive |= alive_flag[gq * PIPE_EW + w];
+        if (!any_alive) {
+          alive &= ~(1 << gq);
+          continue;
+        }
+        const double* xg = x0 + gq * 4 * PG;
+        // layer 0 (replicated, K0 <= 4): one DMMA per 8-row tile, the B
+        // fragment (this group's observations) shared by all of a warp's tiles
+        uint32_t bad = 0u;
+        {
+          const bool kin = t4 < K0;
+          const double xb = kin ? xg[t4 * PG + g8] : 0.0;
+          const int nt0 = (W0 + 7) / 8;
+          for (int mg0 = warp; mg0 < nt0; mg0 += 4 * (ROLLOUT_THREADS / 32)) {
+            double d[4][2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int mg = mg0 + q * (ROLLOUT_THREADS / 32);
+              d[q][0] = d[q][1] = 0.0;
+              if (mg < nt0) dmma(d[q][0], d[q][1], kin ? W0s[t4 * S.WS[0] + mg * 8 + g8] : 0.0, xb);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int mg = mg0 + q * (ROLLOUT_THREADS / 32);
+              if (mg < nt0) bad |= tile8_epilogue(d[q][0], d[q][1], mg * 8 + g8, W0, b0s, h0, t4);
+            }
+          }
+        }
+        if (bad) atomicOr(&cm[0], bad);
+        named_sync(3, ROLLOUT_THREADS);
+        RK_MARK(1);
+        // layer 1: this CTA's RS1-row slice (DMMA over K = W0); the output
+        // layer's partial is folded into the epilogue: each warp reduces its
+        // tile's rows (shuffles over g) into opart[warp][o][lane]
+        bad = 0u;
+        for (int mg = warp; mg * 8 < RSv1; mg += ROLLOUT_THREADS / 32) {
+          double d0, d1;
+          dmma_tile8(W1s + mg * 8 + g8, S.WS[1], W0, h0, g8, t4, d0, d1);
+          const int row = mg * 8 + g8;
+          double hv0 = 0.0, hv1 = 0.0;
+          if (row < RSv1) {
+            const double b = b1s[row];
+            const double z0 = d0 + b, z1 = d1 + b;
+            hv0 = z0 > 0.0 ? z0 : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
+            hv1 = z1 > 0.0 ? z1 : 0.0;
+            bad |= (hv0 == INFINITY ? 1u << (2 * t4) : 0u) | (hv1 == INFINITY ? 2u << (2 * t4) : 0u);
+          }
+          for (int o = 0; o < O; ++o) {
+            const double w = row < RSv1 ? Wo[row * O + o] : 0.0;
+            double c0 = w * hv0, c1 = w * hv1;
+#pragma unroll
+            for (int sh = 4; sh < 32; sh <<= 1) {
+              c0 += __shfl_xor_sync(0xffffffffu, c0, sh);
+              c1 += __shfl_xor_sync(0xffffffffu, c1, sh);
+            }
+            if (g8 == 0) {
+              double2* dst = reinterpret_cast<double2*>(opart + (warp * 8 + o) * PG + 2 * t4);
+              if (mg == warp) {
+                *dst = make_double2(c0, c1);
+              } else {
+                const double2 v = *dst;
+                *dst = make_double2(v.x + c0, v.y + c1);
+              }
+            }
+          }
+        }
+        if (bad) atomicOr(&cm[1], bad);
+        named_sync(3, ROLLOUT_THREADS);
+        RK_MARK(2);
+        // output partials (sum over warps in order) + the NetFault row,
+        // st.async to all C CTAs
+        double* pout = pout0 + (gq * 2 + par) * C * OE1;
+        const uint32_t lb = smem_u32(&xbar[gq * 2 + par]);
+        const int nw1 = min(ROLLOUT_THREADS / 32, (RSv1 + 7) / 8);  // warps that own a tile
+        if (tid < OE) {
+          double v = 0.0;
+          for (int w = 0; w < nw1; ++w) v += opart[w * 8 * PG + tid];
+          const uint32_t la = smem_u32(pout + crank * OE1 + tid);
+#pragma unroll
+          for (int c = 0; c < C; ++c) st_async(map_cluster(la, (uint32_t)c), v, map_cluster(lb, (uint32_t)c));
+        } else if (tid < OE1) {
+          const int e = tid - OE;
+          int bl = L;
+          for (int l = 1; l >= 0; --l)
+            if ((cm[l] >> e) & 1u) bl = l;
+          const uint32_t la = smem_u32(pout + crank * OE1 + tid);
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            st_async(map_cluster(la, (uint32_t)c), (double)bl, map_cluster(lb, (uint32_t)c));
+        }
+        RK_MARK(3);
+      }
+      if (!alive) break;
+    }
+  } else {
+    // ========================================================== env warp
+    const int ew = (tid - ROLLOUT_THREADS) >> 5, lane = tid & 31;
+    const bool mine = lane < 2 * PIPE_LPW;  // this thread owns a lane of the team
+    const int gq_me = mine ? lane / PIPE_LPW : 2, e = ew * PIPE_LPW + lane % PIPE_LPW;
+    const int j = group * 16 + gq_me * PG + e;  // lane index within the agent
+    const bool valid = mine && j < A.e;
+    const int per = A.count / A.e, rem = A.count % A.e;
+    const int eps_this = valid ? per + (j < rem ? 1 : 0) : 0;
+    const int slot0 = valid ? j * per + min(j, rem) : 0;
+    LaneEnv s{};
+    double ep_ret = 0.0, wc = 0.0;
+    double wmean[4] = {0, 0, 0, 0}, wm2[4] = {0, 0, 0, 0};
+    int ep_len = 0, eps_done = 0;
+    long long steps = 0;
+    uint32_t myfault = 0, myfault_layer = 0;
+    if (valid) {
+      const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
+      env_reset(E, fold_in(lane_key, 0), s);  // proj/src/rollout.cpp:104
+    }
+    NormParams nrm;
+    nrm.active = 0;
+    nrm.dim = 0;
+    if (A.norm != nullptr) nrm = *A.norm;
+    const double* bo = reinterpret_cast<const double*>(smem + S.off_bout);
+    double sin_th = 0.0;
+    auto observe_into_x0 = [&](bool act) {
+      double raw[4];
+      observe(E, s, raw);
+      sin_th = raw[1];
+      if (act && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
+        if (wc == 0.0) {
+          for (int i = 0; i < E.obs_dim; ++i) {
+            wmean[i] = raw[i];
+            wm2[i] = 0.0;
+          }
+          wc = 1.0;
+        } else {
+          wc = dadd(wc, 1.0);
+          for (int i = 0; i < E.obs_dim; ++i) {
+            const double delta = dsub(raw[i], wmean[i]);
+            wmean[i] = dadd(wmean[i], ddiv(delta, wc));
+            wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
+          }
+        }
+      }
+      for (int i = 0; i < E.obs_dim; ++i) {
+        double v = raw[i];
+        if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
+        x0[(gq_me * 4 + i) * PG + e] = act ? v : 0.0;
+      }
+    };
+    bool act = valid && eps_this > 0 && A.max_iters > 0;
+    if (mine) observe_into_x0(act);
+    int alive = 0;
+#pragma unroll
+    for (int gq = 0; gq < 2; ++gq) {
+      const bool a = __any_sync(0xffffffffu, act && gq_me == gq);
+      if (lane == 0) alive_flag[gq * PIPE_EW + ew] = a ? 1 : 0;
+    }
+    named_sync(4, 32 * PIPE_EW);
+#pragma unroll
+    for (int gq = 0; gq < 2; ++gq)
+      for (int w = 0; w < PIPE_EW; ++w) alive |= alive_flag[gq * PIPE_EW + w] ? 1 << gq : 0;
+    named_arrive(1, PIPE_THREADS);
+    named_arrive(2, PIPE_THREADS);
+    for (int it = 0; alive; ++it) {
+      const int par = it & 1;
+#pragma unroll 1
+      for (int gq = 0; gq < 2; ++gq) {
+        if (!((alive >> gq) & 1)) continue;
+        uint64_t* bar = &xbar[gq * 2 + par];
+        if (ew == 0 && lane == 0) mbar_arrive_expect_tx(bar, xbytes);
+        RK_MARK(6);
+        mbar_wait_parity(bar, (uint32_t)((it >> 1) & 1));
+        RK_MARK(4);
+        const double* pout = pout0 + (gq * 2 + par) * C * OE1;
+        if (gq_me == gq && act) {
+          // head + env step (proj/src/rollout.cpp:57-90, :131-153)
+          double z[8];
+          bool nonfinite_out = false;
+          int bad_layer = L;
+          for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pout[c * OE1 + OE + e]);
+          for (int o = 0; o < O && o < 8; ++o) {
+            double v = pout[o * PG + e];
+            for (int c = 1; c < C; ++c) v += pout[c * OE1 + o * PG + e];
+            z[o] = v + bo[o];
+            if (!isfinite(z[o])) nonfinite_out = true;
+          }
+          if (bad_layer >= L && nonfinite_out) bad_layer = L - 1;
+          if (bad_layer < L) {  // NetFault: the lowest layer with a non-finite activation
+            myfault = FAULT_NET;
+            myfault_layer = (uint32_t)bad_layer;
+          } else {
+            double action;
+            if (N.head == HEAD_CATEGORICAL) {
+              int arg = 0;
+              for (int o = 1; o < O; ++o)
+                if (z[o] > z[arg]) arg = o;  // maxCoeff: first maximum
+              action = (double)arg;
+            } else if (N.head == HEAD_TANH) {
+              action = N.tanh_scale * tanh(z[0]);
+            } else {
+              action = z[0];
+            }
+            double reward = 0.0;
+            bool term = false, trunc = false;
+            const uint32_t f =
+                env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr);
+            if (f) {
+              myfault = f;
+            } else {
+              ep_ret = dadd(ep_ret, reward);  // proj/src/rollout.cpp:143
+              ep_len += 1;
+              steps += 1;
+              if (term || trunc) {
+                if (crank == 0) {
+                  const long long slot = (long long)agent_local * A.count + slot0 + eps_done;
+                  A.ep_returns[slot] = ep_ret;
+                  if (A.ep_lengths) A.ep_lengths[slot] = ep_len;
+                }
+                ep_ret = 0.0;
+                ep_len = 0;
+                eps_done += 1;
+                if (eps_done < eps_this) env_reset(E, s.rng, s);  // auto-reset, env.cpp:163-167
+              }
+            }
+          }
+          act = myfault == 0 && eps_done < eps_this && it + 1 < A.max_iters;
+          observe_into_x0(act);
+        }
+        const bool a = __any_sync(0xffffffffu, act && gq_me == gq);
+        if (lane == 0) alive_flag[gq * PIPE_EW + ew] = a ? 1 : 0;
+        named_sync(4, 32 * PIPE_EW);  // every env warp sees the group's flags
+        int any_alive = 0;
+#pragma unroll
+        for (int w = 0; w < PIPE_EW; ++w) any_alive |= alive_flag[gq * PIPE_EW + w];
+        if (!any_alive) alive &= ~(1 << gq);
+        named_arrive(1 + gq, PIPE_THREADS);
+        RK_MARK(5);
+      }
+    }
+    if (valid && crank == 0) {
+      const long long ln = (long long)agent_local * A.e + j;
+      if (A.lane_steps) A.lane_steps[ln] = steps;
+      if (A.track_stats && A.lane_stats) {
+        double* st = A.lane_stats + ln * 9;
+        st[0] = wc;
+        for (int i = 0; i < 4; ++i) {
+          st[1 + i] = wmean[i];
+          st[5 + i] = wm2[i];
+        }
+      }
+      if (myfault) record_fault(A.fault, (uint64_t)((long long)agent * A.e + j), myfault, myfault_layer);
+    }
+  }
+#ifdef EVB_TC_PROFILE
+  if (tid == 0 || tid == ROLLOUT_THREADS) {  // compute warp 0 / env warp 0
+    for (int i = 0; i < 8; ++i) atomicAdd(&g_rk_prof[i], rk_prof[i]);
+    if (tid == 0) atomicAdd(&g_rk_prof[8], 1ull);
+  }
+#endif
+  cluster_sync_all();  // no CTA may exit while peers still address its SMEM
+}
+
 #ifdef EVB_TC_PROFILE
 extern "C" int evorl_debug_rk_profile(unsigned long long* out16) {
   if (cudaMemcpyFromSymbol(out16, g_rk_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 6;
@@ -806,9 +1228,73 @@ static bool try_plan(const NetDesc& net, int obs_dim, int ET, int TR, int C, int
   return true;
 }
 
+// Pipelined fp64 DMMA team (rollout_pipe_kernel): 2 hidden layers, the
+// first replicated (K <= 8), the second sliced over C CTAs; activations in
+// 8-lane groups (rows 8 doubles apart).
+constexpr int PG_HOST = 8;
+static bool try_plan_pipe(const NetDesc& net, int obs_dim, int C, SmemPlan* P) {
+  if (net.nlayers != 3) return false;
+  const int K0 = net.dims[0], W0 = net.dims[1], W1 = net.dims[2], O = net.dims[3];
+  if (K0 > 4 || obs_dim > 4 || O > 8 || W1 < C || W0 < 8) return false;
+  SmemPlan p{};
+  p.C = C;
+  p.TR = 1;
+  p.ET = 16;
+  p.mma = 1;
+  p.pipe = 1;
+  p.XS = 8;
+  const int RS1 = (W1 + C - 1) / C, RSP1 = (RS1 + 7) / 8 * 8;
+  p.REP[0] = 1;
+  p.RS[0] = p.RSP[0] = (W0 + 7) / 8 * 8;
+  p.WS[0] = p.RSP[0] + 4;
+  p.RS[1] = RS1;
+  p.RSP[1] = RSP1;
+  p.WS[1] = RSP1 + 4;  // 4 k-rows of an A fragment land 8 banks apart
+  p.KS[0] = p.KS[1] = 1;
+  int off = 0;
+  p.off_w[0] = off;
+  off = align16(off + K0 * p.WS[0] * 8);
+  p.off_b[0] = off;
+  off = align16(off + p.RSP[0] * 8);
+  p.off_w[1] = off;
+  off = align16(off + W0 * p.WS[1] * 8);
+  p.off_b[1] = off;
+  off = align16(off + RSP1 * 8);
+  p.off_wout = off;
+  off = align16(off + RSP1 * O * 8);
+  p.off_bout = off;
+  off = align16(off + O * 8);
+  p.off_x0 = off;
+  off = align16(off + 2 * 4 * 8 * 8);
+  p.off_h[0] = off;
+  off = align16(off + p.RSP[0] * 8 * 8);
+  p.off_h[1] = off;  // (unused: the output partial is folded into layer 1's epilogue)
+  p.off_part = off;
+  off = align16(off + 8 * 8 * PG_HOST * 8);
+  p.off_pout = off;
+  off = align16(off + 2 * 2 * C * (O + 1) * 8 * 8);
+  p.off_mask = off;
+  off = align16(off + 2 * 2 * 2 * 4);
+  p.off_bar = off;  // 4 mbarriers [group][parity] + group-alive flags [group][env warp]
+  off = align16(off + 32 + 2 * 8 * 4);
+  p.bytes = off;
+  if (off > 227 * 1024) return false;
+  *P = p;
+  return true;
+}
+
+// opt-in (EVORL_FP64_PIPE=1): measured slower than the plain DMMA team on
+// B200 (profiles/README.md): DMMA and the env's DFMA share the FP64 pipe, and
+// 8-lane groups lose the A-fragment reuse of 16-lane tiles
+static bool pipe_enabled() {
+  const char* v = getenv("EVORL_FP64_PIPE");
+  return v && v[0] == '1';
+}
+
 bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPlan* plan, bool simple_only) {
   const int ET = e >= 5 ? 16 : (e >= 2 ? 4 : 1);
   plan->trn = 0;
+  plan->pipe = 0;
   if (simple_only) {  // TR = 1 SIMT, resident or global-weights
     plan->tc = 0;
     const int ts = precision == 0 ? 8 : 4;
@@ -829,6 +1315,9 @@ bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPla
   }
   plan->tc = 0;
   const int tsize = precision == 0 ? 8 : 4;
+  if (precision == 0 && ET == 16 && pipe_enabled())
+    for (int C : {2, 4, 8})
+      if (try_plan_pipe(net, obs_dim, C, plan)) return true;
   for (int C : {1, 2, 4, 8}) {
     // fp64 with 16 lanes: hidden-layer GEMMs on the FP64 tensor cores
     if (precision == 0 && ET == 16 && try_plan(net, obs_dim, ET, 1, C, tsize, plan, true)) return true;
@@ -872,6 +1361,39 @@ static cudaError_t launch_inst(const RolloutArgs& a, cudaStream_t stream) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+template <int C>
+static cudaError_t launch_pipe_inst(const RolloutArgs& a, cudaStream_t stream) {
+  auto kern = rollout_pipe_kernel<C>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(a.n_agents * a.groups * C));
+  cfg.blockDim = dim3(PIPE_THREADS);
+  cfg.dynamicSmemBytes = (size_t)a.plan.bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+static cudaError_t launch_pipe(const RolloutArgs& a, cudaStream_t s) {
+  switch (a.plan.C) {
+    case 2: return launch_pipe_inst<2>(a, s);
+    case 4: return launch_pipe_inst<4>(a, s);
+    case 8: return launch_pipe_inst<8>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <typename T, int TR, int ET, bool MMA = false, bool GW = false, bool TRN = false>
 static cudaError_t launch_c(const RolloutArgs& a, cudaStream_t s) {
   switch (a.plan.C) {
@@ -909,6 +1431,7 @@ static cudaError_t launch_t(const RolloutArgs& a, cudaStream_t s) {
 cudaError_t launch_rollout(const RolloutArgs& a, int precision, cudaStream_t stream) {
   if (a.n_agents <= 0) return cudaSuccess;
   if (a.plan.tc) return launch_rollout_tc(a, a.plan.tcp, stream);
+  if (a.plan.pipe) return launch_pipe(a, stream);
   return precision == 0 ? launch_t<double>(a, stream) : launch_t<float>(a, stream);
 }
 

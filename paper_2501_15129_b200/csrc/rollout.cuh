@@ -118,6 +118,7 @@ struct SmemPlan {
                  //    (policies too large for SMEM residency; SIMT slice GEMMs)
   int trn;        // 1: collect transitions (RolloutArgs::t_*), TR = 1 SIMT plans only
   int tc;         // 1: EVORL_PREC_TC tcgen05 team (rollout_tc.cu), plan in tcp
+  int pipe;       // 1: pipelined fp64 DMMA team (two 8-lane groups, env warp)
   TcPlanOut tcp;
 };
 
