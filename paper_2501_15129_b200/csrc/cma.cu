@@ -293,8 +293,13 @@ EVB_HD void rr_pair(int n, int r, int k, int& a, int& b) {
 }
 
 // One CTA per block pair: diagonalise the 64x64 subproblem in shared memory.
+// Threshold Jacobi: a pair whose off-diagonal mass is already below `thr`
+// (the global stop tolerance split over all block pairs) is skipped -- its
+// rotation is the identity, flagged in skipf so the apply kernels leave its
+// rows / columns alone; convergence is still judged on the whole matrix.
 __global__ void __launch_bounds__(256) k_jacobi_pairs(const double* __restrict__ A, int dp, int nb, int round,
-                                                      double* __restrict__ Uout, int max_sweeps) {
+                                                      double* __restrict__ Uout, int max_sweeps, double thr,
+                                                      int* __restrict__ skipf) {
   extern __shared__ __align__(16) double jsm[];
   double(*S)[JP + 1] = reinterpret_cast<double(*)[JP + 1]>(jsm);
   double(*Us)[JP + 1] = reinterpret_cast<double(*)[JP + 1]>(jsm + JP * (JP + 1));
@@ -329,7 +334,10 @@ __global__ void __launch_bounds__(256) k_jacobi_pairs(const double* __restrict__
       __syncthreads();
     }
     const bool done = red[0][0] <= 1e-30 * red[1][0] || red[0][0] == 0.0;
+    const bool skip = sweep == 0 && (done || red[0][0] <= thr);
     __syncthreads();
+    if (sweep == 0 && tid == 0) skipf[pair] = skip ? 1 : 0;
+    if (skip) return;
     if (done) break;
     for (int r = 0; r < JP - 1; ++r) {
       const int k = tid >> 3, sub = tid & 7;  // 32 pairs x 8 threads
@@ -457,7 +465,8 @@ EVB_DEV void jtile_gemm(const double (*As)[JP + 2], bool transA, const double (*
 // Replaces the column pass + row pass: W stays exactly symmetric, each entry is
 // read and written once per round and the flops halve.
 __global__ void __launch_bounds__(256) k_jacobi_apply_sym(double* __restrict__ W, int dp, int nb, int round,
-                                                          const double* __restrict__ U) {
+                                                          const double* __restrict__ U,
+                                                          const int* __restrict__ skipf) {
   extern __shared__ __align__(16) double jsm[];
   double(*Ts)[JP + 2] = reinterpret_cast<double(*)[JP + 2]>(jsm);
   double(*Ua)[JP + 2] = reinterpret_cast<double(*)[JP + 2]>(jsm + JP * (JP + 2));
@@ -469,6 +478,8 @@ __global__ void __launch_bounds__(256) k_jacobi_apply_sym(double* __restrict__ W
     ++a;
   }
   const int b = a + rem;
+  const bool ska = skipf[a] != 0, skb = skipf[b] != 0;  // identity rotations (U not written)
+  if (ska && skb) return;                                 // I^T W I
   int Pa, Qa, Pb, Qb;
   rr_pair(nb, round, a, Pa, Qa);
   rr_pair(nb, round, b, Pb, Qb);
@@ -476,8 +487,8 @@ __global__ void __launch_bounds__(256) k_jacobi_apply_sym(double* __restrict__ W
   const double* Ugb = U + (long long)b * JP * JP;
   for (int i = tid; i < JP * JP; i += 256) {
     const int r = i / JP, c = i % JP;
-    Ua[r][c] = Uga[i];
-    Ub[r][c] = Ugb[i];
+    if (!ska) Ua[r][c] = Uga[i];
+    if (!skb) Ub[r][c] = Ugb[i];
     const int gr = r < JB ? Pa * JB + r : Qa * JB + r - JB;
     const int gc = c < JB ? Pb * JB + c : Qb * JB + c - JB;
     Ts[r][c] = W[(long long)gr * dp + gc];
@@ -486,24 +497,28 @@ __global__ void __launch_bounds__(256) k_jacobi_apply_sym(double* __restrict__ W
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
   double acc[4][2][2];
-  jtile_gemm(Ts, false, Ub, acc, wm, wn, g, t);  // X = T U_b
-  __syncthreads();
+  if (!skb) {
+    jtile_gemm(Ts, false, Ub, acc, wm, wn, g, t);  // X = T U_b
+    __syncthreads();
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) Ts[wm + mt * 8 + g][wn + nt * 8 + 2 * t + i] = acc[mt][nt][i];
-  __syncthreads();
-  jtile_gemm(Ua, true, Ts, acc, wm, wn, g, t);  // Y = U_a^T X
-  __syncthreads();
+        for (int i = 0; i < 2; ++i) Ts[wm + mt * 8 + g][wn + nt * 8 + 2 * t + i] = acc[mt][nt][i];
+    __syncthreads();
+  }
+  if (!ska) {
+    jtile_gemm(Ua, true, Ts, acc, wm, wn, g, t);  // Y = U_a^T X
+    __syncthreads();
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) Ts[wm + mt * 8 + g][wn + nt * 8 + 2 * t + i] = acc[mt][nt][i];
-  __syncthreads();
+        for (int i = 0; i < 2; ++i) Ts[wm + mt * 8 + g][wn + nt * 8 + 2 * t + i] = acc[mt][nt][i];
+    __syncthreads();
+  }
   for (int i = tid; i < JP * JP; i += 256) {  // coalesced: column index fastest
     const int r = i / JP, c = i % JP;
     const int gr = r < JB ? Pa * JB + r : Qa * JB + r - JB;
@@ -535,7 +550,8 @@ EVB_DEV void cp_async_wait() {
 // current one is multiplied on the FP64 tensor cores.
 constexpr int JV_STAGE = 2 * JP * (JP + 2);  // doubles per stage: panel + U
 __global__ void __launch_bounds__(256, 1) k_jacobi_apply_v(double* __restrict__ M, int dp, int nb, int round,
-                                                           const double* __restrict__ U) {
+                                                           const double* __restrict__ U,
+                                                           const int* __restrict__ skipf) {
   extern __shared__ __align__(16) double jsm[];
   const int np = nb / 2, ntr = dp / JP;
   const long long items = (long long)np * ntr;
@@ -557,11 +573,15 @@ __global__ void __launch_bounds__(256, 1) k_jacobi_apply_v(double* __restrict__ 
   };
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
-  long long item = blockIdx.x;
+  auto live = [&](long long i) {  // next work item at or after i whose pair rotated
+    while (i < items && skipf[i / ntr]) i += gridDim.x;
+    return i;
+  };
+  long long item = live(blockIdx.x);
   if (item < items) issue(item, 0);
-  for (int it = 0; item < items; ++it, item += gridDim.x) {
+  for (int it = 0; item < items; ++it) {
     const int st = it & 1;
-    const long long next = item + gridDim.x;
+    const long long next = live(item + gridDim.x);
     if (next < items) {
       issue(next, st ^ 1);
       cp_async_wait<1>();
@@ -586,6 +606,7 @@ __global__ void __launch_bounds__(256, 1) k_jacobi_apply_v(double* __restrict__ 
             make_double2(acc[mt][nt][0], acc[mt][nt][1]);
       }
     __syncthreads();  // this stage is refilled two items later
+    item = next;
   }
 }
 
@@ -752,6 +773,10 @@ int sym_eig_jacobi(CmaDev& w, const double* A, int d, double* evals_min, double*
   // inner sweeps per block-pair visit: the outer sweeps revisit every pair, so
   // the subproblem need not be diagonalised exactly each time
   static const int inner_sweeps = getenv("EVORL_EIG_INNER") ? atoi(getenv("EVORL_EIG_INNER")) : 1;
+  static const bool skip_pairs = !(getenv("EVORL_EIG_NOSKIP") && getenv("EVORL_EIG_NOSKIP")[0] == '1');
+  // threshold Jacobi: also skip pairs holding less than skip_frac of the mean
+  // per-pair share of the current off-diagonal mass (revisited next sweep)
+  static const double skip_frac = getenv("EVORL_EIG_SKIPFRAC") ? atof(getenv("EVORL_EIG_SKIPFRAC")) : 0.0;
   for (; sweep < 30; ++sweep) {
     cudaMemsetAsync(w.red, 0, 2 * sizeof(double), s);
     k_offdiag<<<296, 256, 0, s>>>(w.W, d, dp, w.red);
@@ -762,10 +787,14 @@ int sym_eig_jacobi(CmaDev& w, const double* A, int d, double* evals_min, double*
     if (h[0] <= tol * h[1] || h[0] == 0.0) break;
     if (h[0] >= 0.9 * prev_off && h[0] <= 1e-20 * h[1]) break;  // stagnated at the noise floor
     prev_off = h[0];
+    // per-pair skip threshold: if every block pair sat below it, the whole
+    // off-diagonal mass would be under the stop tolerance
+    const double npairs = 0.5 * nb * (nb - 1);
+    const double thr = skip_pairs ? std::max(tol * h[1], skip_frac * h[0]) / npairs : -1.0;
     for (int r = 0; r < nb - 1; ++r) {
-      k_jacobi_pairs<<<nb / 2, 256, sm_pairs, s>>>(w.W, dp, nb, r, w.U, inner_sweeps);
-      k_jacobi_apply_sym<<<(unsigned)(np * (np + 1) / 2), 256, sm_sym, s>>>(w.W, dp, nb, r, w.U);
-      k_jacobi_apply_v<<<v_grid, 256, sm_v, s>>>(w.V, dp, nb, r, w.U);
+      k_jacobi_pairs<<<nb / 2, 256, sm_pairs, s>>>(w.W, dp, nb, r, w.U, inner_sweeps, thr, w.skipf);
+      k_jacobi_apply_sym<<<(unsigned)(np * (np + 1) / 2), 256, sm_sym, s>>>(w.W, dp, nb, r, w.U, w.skipf);
+      k_jacobi_apply_v<<<v_grid, 256, sm_v, s>>>(w.V, dp, nb, r, w.U, w.skipf);
       count_launch(3);
     }
   }

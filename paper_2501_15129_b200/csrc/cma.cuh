@@ -37,6 +37,7 @@ struct CmaDev {
   double* Bt;           // dp x dp scratch (warm start)
   double* Tt;           // dp x dp scratch (warm start)
   double* U;            // (dp/64) * 64 * 64: per-pair 64x64 rotations
+  int* skipf;           // dp/64: pair skipped this round (identity rotation)
   double* evals;        // dp
   int* order;           // dp
   double* zD;           // n x d

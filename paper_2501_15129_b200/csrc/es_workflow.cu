@@ -290,7 +290,7 @@ static void free_all(evorl_es* s) {
   for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1})
     if (ev) cudaEventDestroy(ev);
   void* cm[] = {s->cma.d_w, s->cma.dev.C, s->cma.dev.B, s->cma.dev.D, s->cma.dev.ps, s->cma.dev.pc,
-                s->cma.dev.W, s->cma.dev.V, s->cma.dev.Bt, s->cma.dev.Tt, s->cma.dev.U, s->cma.dev.evals, s->cma.dev.order, s->cma.dev.zD,
+                s->cma.dev.W, s->cma.dev.V, s->cma.dev.Bt, s->cma.dev.Tt, s->cma.dev.U, s->cma.dev.skipf, s->cma.dev.evals, s->cma.dev.order, s->cma.dev.zD,
                 s->cma.dev.ytT, s->cma.dev.wyT, s->cma.dev.yw, s->cma.dev.t1, s->cma.dev.cih, s->cma.dev.red};
   for (void* p : cm)
     if (p) cudaFree(p);
@@ -470,6 +470,7 @@ static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** 
     A(dalloc(&v.Bt, dp2));
     A(dalloc(&v.Tt, dp2));
     A(dalloc(&v.U, (size_t)(v.dp / 64) * 64 * 64));
+    A(dalloc(&v.skipf, (size_t)(v.dp / 64)));
     A(dalloc(&v.D, v.dp));
     A(dalloc(&v.ps, v.dp));
     A(dalloc(&v.pc, v.dp));
@@ -1679,7 +1680,7 @@ extern "C" int evorl_sym_eig(const double* A, int32_t n, double* evals, double* 
   v.d = n;
   v.dp = (n + 63) / 64 * 64;
   const size_t dp2 = (size_t)v.dp * v.dp;
-  Scratch a, b, w, vv, u, ev, od, t1, red;
+  Scratch a, b, w, vv, u, ev, od, t1, red, sk;
   double *dA, *dB;
   if (int rc = up(a, (const double*)nullptr, dp2, &dA)) return rc;
   if (int rc = up(b, (const double*)nullptr, dp2, &dB)) return rc;
@@ -1690,6 +1691,7 @@ extern "C" int evorl_sym_eig(const double* A, int32_t n, double* evals, double* 
   if (int rc = up(od, (const int*)nullptr, v.dp, &v.order)) return rc;
   if (int rc = up(t1, (const double*)nullptr, v.dp, &v.t1)) return rc;
   if (int rc = up(red, (const double*)nullptr, 8, &v.red)) return rc;
+  if (int rc = up(sk, (const int*)nullptr, v.dp / 64, &v.skipf)) return rc;
   CK(cudaMemset(dA, 0, sizeof(double) * dp2));
   CK(cudaMemcpy2D(dA, sizeof(double) * v.dp, A, sizeof(double) * n, sizeof(double) * n, n, cudaMemcpyHostToDevice));
   double evmin = 0.0;
