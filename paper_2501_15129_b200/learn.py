@@ -231,7 +231,14 @@ def es_config_entries(cfg: EsConfig, seed: Optional[int] = None, budget: Optiona
     workflows' keys are out of scope).  Values use the registry's spelling
     (``true``/``false``, ``64,64``)."""
     b = budget or Budget(iterations=2000)
-    f = lambda x: repr(float(x))
+    # a value equal to the registry default keeps the registry's spelling
+    # (proj/src/config.cpp:23-70: "1e-3", "4194304", ...)
+    spelled = {"ec.cem.var_init": "1e-3", "ec.cem.noise_start": "1e-3", "ec.cem.noise_end": "1e-5"}
+
+    def f(x, key=None):
+        if key in spelled and float(x) == float(spelled[key]):
+            return spelled[key]
+        return repr(float(x))
     t = lambda x: "true" if x else "false"
     out = {
         "workflow": "es", "env.id": cfg.env, "env.fixed_horizon": t(cfg.fixed_horizon),
@@ -249,8 +256,9 @@ def es_config_entries(cfg: EsConfig, seed: Optional[int] = None, budget: Optiona
         "ec.ves.elites": str(cfg.ves_elites), "ec.ves.mirrored": t(cfg.ves_mirrored),
         "ec.cmaes.sigma0": f(cfg.cmaes_sigma0), "ec.cmaes.elites": str(cfg.cmaes_elites),
         "ec.cmaes.max_dim": str(cfg.cmaes_max_dim), "ec.cem.elites": str(cfg.cem_elites),
-        "ec.cem.var_init": f(cfg.cem_var_init), "ec.cem.noise_start": f(cfg.cem_noise_start),
-        "ec.cem.noise_end": f(cfg.cem_noise_end), "ec.cem.decay_iters": str(cfg.cem_decay_iters),
+        "ec.cem.var_init": f(cfg.cem_var_init, "ec.cem.var_init"),
+        "ec.cem.noise_start": f(cfg.cem_noise_start, "ec.cem.noise_start"),
+        "ec.cem.noise_end": f(cfg.cem_noise_end, "ec.cem.noise_end"), "ec.cem.decay_iters": str(cfg.cem_decay_iters),
     }
     if seed is not None:
         out["seed"] = str(seed)

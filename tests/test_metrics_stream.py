@@ -133,3 +133,13 @@ def test_learn_python_and_cpp_hosts_write_identical_records(tmp_path):
     mr, sd = h.evaluate(8, eval_key(root, 4))
     assert recs[6]["eval/episode_return_mean"] == mr and recs[6]["eval/episode_return_std"] == sd
     assert len(open(pdir / "timings.log").read().splitlines()) == 5
+
+
+def test_es_config_entries_use_registry_spelling():
+    import paper_2501_15129_b200 as evb
+    from paper_2501_15129_b200.learn import es_config_entries
+    e = es_config_entries(evb.EsConfig(), seed=0)
+    # registry defaults (proj/src/config.cpp:23-70)
+    assert e["ec.openes.sigma"] == "0.02" and e["ec.cem.var_init"] == "1e-3" and e["ec.cem.noise_end"] == "1e-5"
+    assert e["net.hidden"] == "64,64" and e["env.fixed_horizon"] == "false" and e["ec.openes.mirrored"] == "true"
+    assert e["ec.openes.noise_table_size"] == "4194304" and e["workflow"] == "es" and e["seed"] == "0"
