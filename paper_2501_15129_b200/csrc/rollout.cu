@@ -580,29 +580,7 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
     // rides on the same DSMEM exchange: no remote loads in the env phase)
     {
       const T* xin = nh > 0 ? reinterpret_cast<const T*>(smem + S.off_h[nh - 1]) : x0;
-      const int KSo = S.KS_out;
-      const int kc = (KRP + KSo - 1) / KSo;
-      for (int w = tid; w < OE * KSo; w += ROLLOUT_THREADS) {
-        const int oe = w % OE, ks = w / OE;
-        const int o = oe / ET, e = oe % ET;
-        const int k0 = ks * kc, k1 = min(KRv, k0 + kc);
-        T acc = T(0);
-        for (int k = k0; k < k1; ++k) acc = fma(Wo[k * O + o], xin[(size_t)k * XS + e], acc);
-        part[w] = acc;
-      }
-      __syncthreads();
-      for (int oe = tid; oe < OE1; oe += ROLLOUT_THREADS) {
-        T v;
-        if (oe < OE) {
-          v = part[oe];
-          for (int ks = 1; ks < KSo; ++ks) v += part[ks * OE + oe];
-        } else {
-          const int e = oe - OE;
-          int bl = L;
-          for (int l = nh - 1; l >= 0; --l)
-            if ((cur_mask[l] >> e) & 1u) bl = l;
-          v = T(bl);
-        }
+      auto publish = [&](int oe, T v) {
         if constexpr (C > 1) {
           const uint32_t la = smem_u32(pout + crank * OE1 + oe), lb = smem_u32(&xbar[it & 1]);
 #pragma unroll
@@ -610,6 +588,48 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
             st_async(map_cluster(la, (uint32_t)c), v, map_cluster(lb, (uint32_t)c));
         } else {
           pout[oe] = v;
+        }
+      };
+      auto bad_row = [&](int e) {
+        int bl = L;
+        for (int l = nh - 1; l >= 0; --l)
+          if ((cur_mask[l] >> e) & 1u) bl = l;
+        return T(bl);
+      };
+      if constexpr (ET == 1) {
+        // one lane: warp o reduces output o over a 32-way k split with
+        // shuffles (no partial buffer, no extra barrier)
+        const int warp = tid >> 5, lane = tid & 31;
+        if (warp < O) {
+          const int kc = (KRv + 31) / 32, k0 = lane * kc, k1 = min(KRv, k0 + kc);
+          T acc = T(0);
+          for (int k = k0; k < k1; ++k) acc = fma(Wo[k * O + warp], xin[(size_t)k * XS], acc);
+#pragma unroll
+          for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+          if (lane == 0) publish(warp, acc);
+        }
+        if (tid == (O < ROLLOUT_THREADS / 32 ? O * 32 : 1)) publish(OE, bad_row(0));
+      } else {
+        const int KSo = S.KS_out;
+        const int kc = (KRP + KSo - 1) / KSo;
+        for (int w = tid; w < OE * KSo; w += ROLLOUT_THREADS) {
+          const int oe = w % OE, ks = w / OE;
+          const int o = oe / ET, e = oe % ET;
+          const int k0 = ks * kc, k1 = min(KRv, k0 + kc);
+          T acc = T(0);
+          for (int k = k0; k < k1; ++k) acc = fma(Wo[k * O + o], xin[(size_t)k * XS + e], acc);
+          part[w] = acc;
+        }
+        __syncthreads();
+        for (int oe = tid; oe < OE1; oe += ROLLOUT_THREADS) {
+          T v;
+          if (oe < OE) {
+            v = part[oe];
+            for (int ks = 1; ks < KSo; ++ks) v += part[ks * OE + oe];
+          } else {
+            v = bad_row(oe - OE);
+          }
+          publish(oe, v);
         }
       }
       if constexpr (C > 1) {
