@@ -250,6 +250,9 @@ int evorl_es_set_adam(evorl_es* es, const double* m, const double* v, int64_t t)
 int evorl_es_get_fitness(evorl_es* es, double* fitness);
 int evorl_es_get_obs_norm(evorl_es* es, evorl_obs_norm* out);
 int evorl_es_set_obs_norm(evorl_es* es, const evorl_obs_norm* in);
+/* WorkflowState::rng (the root key of init / the loaded checkpoint); eval keys
+ * are fold_in(fold_in(rng, 1), iteration) (proj/include/evorl/workflow.hpp:42) */
+int evorl_es_get_rng(const evorl_es* es, uint64_t* hi, uint64_t* lo);
 int evorl_es_set_counters(evorl_es* es, int64_t iteration, int64_t env_steps,
                           int64_t episodes);
 
@@ -298,6 +301,15 @@ int evorl_es_phase_rollout(evorl_es* es);            /* ask + rollout of [a0,a1)
 int evorl_es_phase_tell(evorl_es* es, evorl_step_metrics* out); /* ranks + tell of [p0,p1) */
 /* fitness (pop doubles), mean (d doubles), lane stats (pop*e*9 doubles) */
 int evorl_es_device_buffers(evorl_es* es, void** fitness, void** mean, void** lane_stats);
+/* CEM diagonal variance (d doubles; CemState::diag_var, proj/include/evorl/ec.hpp:129-135):
+ * the sharded tell updates [p0,p1) only, so the caller all-gathers it like the
+ * mean, then reads the es/sigma metric with evorl_es_cem_sigma (phase_tell
+ * reports NaN for it on a sharded handle). */
+int evorl_es_device_var(evorl_es* es, void** var);
+int evorl_es_cem_sigma(evorl_es* es, double* sigma); /* sqrt(diag_var.mean()), workflow_es.cpp:162 */
+/* resolved obs_norm mode (EVORL_NORM_*): the lane stats are tracked, and must
+ * be all-gathered by a sharded caller, iff it is EVORL_NORM_RS */
+int evorl_es_norm_mode(const evorl_es* es, int32_t* mode);
 void* evorl_es_stream(evorl_es* es);
 /* device time (ms) of the last rollout launch and last full step, from CUDA
  * events on the handle's stream */

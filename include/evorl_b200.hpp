@@ -147,6 +147,12 @@ class EsWorkflow {
   void counters(std::int64_t* iteration, std::int64_t* env_steps, std::int64_t* episodes) const {
     check(evorl_es_counters(h_.get(), iteration, env_steps, episodes));
   }
+  // WorkflowState::rng: the key of init() or of the loaded checkpoint
+  RngKey rng() const {
+    RngKey k;
+    check(evorl_es_get_rng(h_.get(), &k.hi, &k.lo));
+    return k;
+  }
   evorl_es* handle() { return h_.get(); }
 
  private:
@@ -350,8 +356,10 @@ class MetricsWriter {
 };
 
 // Budget / LearnOptions / learn (proj/include/evorl/workflow.hpp:74-98,
-// proj/src/workflow.cpp:46-68) over the device workflow; `rng` is the root
-// key the workflow was initialised with (eval key = fold_in(fold_in(rng, 1), it)).
+// proj/src/workflow.cpp:46-68) over the device workflow.  Eval keys derive
+// from the handle's own WorkflowState::rng (fold_in(fold_in(rng, 1), it),
+// proj/include/evorl/workflow.hpp:42), so a resumed workflow evaluates like the
+// reference; a caller key that differs from the state's throws invalid_argument.
 struct Budget {
   std::int64_t iterations = 0, episodes = 0, env_steps = 0;  // 0 = off
   bool reached(std::int64_t it, std::int64_t steps, std::int64_t eps) const {
@@ -371,8 +379,9 @@ inline std::vector<std::pair<std::string, double>> step_scalars(const StepMetric
   return {{"es/sigma", m.sigma}, {"fitness/mean", m.fitness_mean}, {"fitness/max", m.fitness_max},
           {"fitness/min", m.fitness_min}, {"es/update_skipped", m.update_skipped ? 1.0 : 0.0}};
 }
-inline void learn(EsWorkflow& wf, RngKey rng, const LearnOptions& opt, MetricsWriter& metrics) {
+inline void learn(EsWorkflow& wf, const LearnOptions& opt, MetricsWriter& metrics) {
   using clock = std::chrono::steady_clock;
+  const RngKey rng = wf.rng();
   std::int64_t it = 0, steps = 0, eps = 0;
   for (wf.counters(&it, &steps, &eps); !opt.budget.reached(it, steps, eps);) {
     const auto t0 = clock::now();
@@ -390,6 +399,12 @@ inline void learn(EsWorkflow& wf, RngKey rng, const LearnOptions& opt, MetricsWr
   }
   if (!opt.checkpoint_path.empty()) wf.save(opt.checkpoint_path);
   metrics.flush();
+}
+inline void learn(EsWorkflow& wf, RngKey rng, const LearnOptions& opt, MetricsWriter& metrics) {
+  const RngKey st = wf.rng();
+  if (rng.hi != st.hi || rng.lo != st.lo)
+    throw std::invalid_argument("learn(): rng is not the workflow state's key (eval keys derive from WorkflowState::rng)");
+  learn(wf, opt, metrics);
 }
 
 }  // namespace evorl_b200

@@ -135,7 +135,8 @@ EXPORTS = [
     "evorl_es_device_buffers", "evorl_es_stream", "evorl_es_last_timings",
     "evorl_measure_fp64_peak", "evorl_measure_dmma_peak", "evorl_es_cma_get", "evorl_es_cma_set",
     "evorl_sym_eig", "evorl_es_save", "evorl_es_load", "evorl_batched_rollout_transitions",
-    "evorl_cma_create", "evorl_cma_ask", "evorl_cma_tell",
+    "evorl_cma_create", "evorl_cma_ask", "evorl_cma_tell", "evorl_es_device_var",
+    "evorl_es_norm_mode", "evorl_es_get_rng", "evorl_es_cem_sigma",
 ]
 
 _lib = None
@@ -199,6 +200,10 @@ def load() -> C.CDLL:
     L.evorl_es_phase_rollout.argtypes = [vp]
     L.evorl_es_phase_tell.argtypes = [vp, C.POINTER(StepMetricsC)]
     L.evorl_es_device_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
+    L.evorl_es_device_var.argtypes = [vp, C.POINTER(vp)]
+    L.evorl_es_norm_mode.argtypes = [vp, C.POINTER(i32)]
+    L.evorl_es_get_rng.argtypes = [vp, C.POINTER(u64), C.POINTER(u64)]
+    L.evorl_es_cem_sigma.argtypes = [vp, C.POINTER(dbl)]
     L.evorl_es_stream.argtypes = [vp]
     L.evorl_es_stream.restype = vp
     L.evorl_es_last_timings.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]

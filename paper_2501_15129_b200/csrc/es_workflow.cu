@@ -20,6 +20,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -863,6 +864,8 @@ static double cem_floor(const evorl_es* s) {  // CemState::noise_floor, proj/src
   return s->cfg.cem_noise_start * std::pow(s->cfg.cem_noise_end / s->cfg.cem_noise_start, frac);
 }
 
+static int cem_sigma_metric(evorl_es* s, double* sigma);
+
 // ranks + tell on [p0, p1) + metrics; expects the full fitness vector.
 extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
   CK(cudaSetDevice(s->cfg.device));
@@ -903,7 +906,7 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       t.table = s->d_table;
       t.offsets = s->d_offsets;
       {
-        const long long need = (long long)openes_tell_chunks(t.base, s->p1 - s->p0) * (s->p1 - s->p0);
+        const long long need = (long long)openes_tell_chunks(t.base, s->d) * (s->p1 - s->p0);
         if (need > s->tell_part_cap) {
           if (s->d_tell_part) cudaFree(s->d_tell_part);
           s->d_tell_part = nullptr;
@@ -960,12 +963,15 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
   CK(cudaMemcpyAsync(s->h->metrics, s->d_metrics, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(s->ev_s1, st));
   CK(cudaStreamSynchronize(st));
-  if (s->cfg.algo == EVORL_ALGO_CEM) {  // es/sigma = sqrt(diag_var.mean()) (proj/src/workflow_es.cpp:162)
-    std::vector<double> v(s->d);
-    CK(cudaMemcpy(v.data(), s->d_var, sizeof(double) * s->d, cudaMemcpyDeviceToHost));
-    double acc = 0.0;
-    for (double x : v) acc += x;
-    sigma = std::sqrt(acc / (double)s->d);
+  // es/sigma = sqrt(diag_var.mean()) (proj/src/workflow_es.cpp:162); a sharded
+  // handle holds only its [p0, p1) slice of the new variance here, so the
+  // caller gathers it and asks evorl_es_cem_sigma (NaN until then)
+  if (s->cfg.algo == EVORL_ALGO_CEM) {
+    if (s->world == 1) {
+      if (int rc = cem_sigma_metric(s, &sigma)) return rc;
+    } else {
+      sigma = std::numeric_limits<double>::quiet_NaN();
+    }
   }
   cudaEventElapsedTime(&s->last_rollout_ms, s->ev_r0, s->ev_r1);
   cudaEventElapsedTime(&s->last_step_ms, s->ev_s0, s->ev_s1);
@@ -1074,6 +1080,46 @@ extern "C" int evorl_es_device_buffers(evorl_es* s, void** fitness, void** mean,
   if (mean) *mean = s->d_mean;
   if (lane_stats) *lane_stats = s->d_lane_stats;
   return EVORL_OK;
+}
+
+// CEM's diagonal variance (CemState::diag_var, proj/include/evorl/ec.hpp:129-135):
+// k_cem_tell updates it on [p0, p1) only, so a sharded caller gathers it like
+// the mean (the next ask reads every coordinate).
+extern "C" int evorl_es_device_var(evorl_es* s, void** var) {
+  if (var) *var = s->d_var;
+  return EVORL_OK;
+}
+
+// The resolved obs_norm mode (EVORL_NORM_NONE/VBN/RS): per-lane RunningStats
+// are tracked (and must be gathered by a sharded caller) iff it is RS.
+extern "C" int evorl_es_norm_mode(const evorl_es* s, int32_t* mode) {
+  *mode = s->norm_mode;
+  return EVORL_OK;
+}
+
+// The WorkflowState root key (state.rng) the workflow was initialised or
+// loaded with; learn() derives eval keys from it (proj/include/evorl/workflow.hpp:42).
+extern "C" int evorl_es_get_rng(const evorl_es* s, uint64_t* hi, uint64_t* lo) {
+  *hi = s->rng.hi;
+  *lo = s->rng.lo;
+  return EVORL_OK;
+}
+
+// es/sigma of a CEM workflow = sqrt(diag_var.mean()) (proj/src/workflow_es.cpp:162),
+// summed sequentially over the FULL variance (a sharded caller calls it after
+// gathering the variance slices).
+static int cem_sigma_metric(evorl_es* s, double* sigma) {
+  std::vector<double> v(s->d);
+  CK(cudaMemcpy(v.data(), s->d_var, sizeof(double) * s->d, cudaMemcpyDeviceToHost));
+  double acc = 0.0;
+  for (double x : v) acc += x;
+  *sigma = std::sqrt(acc / (double)s->d);
+  return EVORL_OK;
+}
+extern "C" int evorl_es_cem_sigma(evorl_es* s, double* sigma) {
+  if (s->cfg.algo != EVORL_ALGO_CEM) return set_err(EVORL_E_INVALID_ARGUMENT, "not a cem workflow");
+  CK(cudaSetDevice(s->cfg.device));
+  return cem_sigma_metric(s, sigma);
 }
 extern "C" void* evorl_es_stream(evorl_es* s) { return (void*)s->stream; }
 
@@ -1987,22 +2033,21 @@ extern "C" int evorl_es_load(evorl_es* s, const char* path) {
     return ckpt_err("checkpoint: segment '%s' has wrong size", "obs_norm/mean");
   const std::vector<double>* mean;
   if (int rc = vec("ec/mean", d, &mean)) return rc;
-  // stage everything before touching the handle (no partial state on error)
+  // Every segment is parsed and validated before the handle is touched; the
+  // device setters below can then only fail on a CUDA error, and the host-side
+  // scalars (OpenES sigma / table seed, CEM iteration, keys, counters) are
+  // applied last, once every device write has succeeded.
+  double os_sigma = 0;
+  int64_t os_seed = 0, cem_iter = 0;
   switch (s->cfg.algo) {
     case EVORL_ALGO_OPENES: {
-      double sigma = 0;
-      int64_t t = 0, seed = 0;
+      int64_t t = 0;
       const std::vector<double>*m, *v;
-      if (int rc = scal_f("ec/sigma", &sigma)) return rc;
+      if (int rc = scal_f("ec/sigma", &os_sigma)) return rc;
       if (int rc = vec("ec/adam/m", d, &m)) return rc;
       if (int rc = vec("ec/adam/v", d, &v)) return rc;
       if (int rc = scal_i("ec/adam/t", &t)) return rc;
-      if (int rc = scal_i("ec/table_seed", &seed)) return rc;
-      s->cfg.openes_sigma = sigma;
-      if (s->d_table) {  // openes_rebuild_table (proj/src/workflow_es.cpp:223-224)
-        s->table_seed = (uint64_t)seed;
-        CK(rebuild_table(s));
-      }
+      if (int rc = scal_i("ec/table_seed", &os_seed)) return rc;
       if (int rc = evorl_es_set_adam(s, m->data(), v->data(), t)) return rc;
       break;
     }
@@ -2030,11 +2075,9 @@ extern "C" int evorl_es_load(evorl_es* s, const char* path) {
     }
     default: {  // CEM
       const std::vector<double>* var;
-      int64_t iter = 0;
       if (int rc = vec("ec/var", d, &var)) return rc;
-      if (int rc = scal_i("ec/iter", &iter)) return rc;
+      if (int rc = scal_i("ec/iter", &cem_iter)) return rc;
       CK(cudaMemcpy(s->d_var, var->data(), sizeof(double) * d, cudaMemcpyHostToDevice));
-      s->cem_iter = iter;
       break;
     }
   }
@@ -2048,6 +2091,22 @@ extern "C" int evorl_es_load(evorl_es* s, const char* path) {
   }
   on.count = count;
   if (int rc = evorl_es_set_obs_norm(s, &on)) return rc;
+  if (s->cfg.algo == EVORL_ALGO_OPENES) {
+    const double old_sigma = s->cfg.openes_sigma;
+    const uint64_t old_seed = s->table_seed;
+    s->cfg.openes_sigma = os_sigma;
+    if (s->d_table) {  // openes_rebuild_table (proj/src/workflow_es.cpp:223-224)
+      s->table_seed = (uint64_t)os_seed;
+      const cudaError_t e = rebuild_table(s);
+      if (e != cudaSuccess) {
+        s->cfg.openes_sigma = old_sigma;
+        s->table_seed = old_seed;
+        CK(e);
+      }
+    }
+  } else if (s->cfg.algo == EVORL_ALGO_CEM) {
+    s->cem_iter = cem_iter;
+  }
   s->rng = DKey{(uint64_t)(*key)[0], (uint64_t)(*key)[1]};
   s->iteration = it;
   s->env_steps = steps;

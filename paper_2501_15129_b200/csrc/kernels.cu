@@ -403,10 +403,13 @@ __global__ void k_openes_adam(const OpenEsTellArgs a, int chunks) {
   a.mean[p] = prm;
 }
 
-int openes_tell_chunks(int rows, long long span) {
+int openes_tell_chunks(int rows, long long d) {
   // fill ~8 resident CTAs of TELL_T threads per SM over 148 SMs, keeping
-  // >= 32 rows per chunk so the Box-Muller work dominates the partial traffic
-  const long long coord_threads = (span + TELL_V - 1) / TELL_V;
+  // >= 32 rows per chunk so the Box-Muller work dominates the partial traffic.
+  // Sized from the FULL dimension d, never from a shard's span: the row-chunk
+  // boundaries fix the summation order of g_p, which must not depend on the
+  // world size (dist.py: bit-identical results for any sharding).
+  const long long coord_threads = (d + TELL_V - 1) / TELL_V;
   const long long want = (148LL * 8 * TELL_T + coord_threads - 1) / std::max(1LL, coord_threads);
   const long long by_rows = std::max(1, rows / 32);
   return (int)std::max(1LL, std::min({want, by_rows, 256LL}));
@@ -416,7 +419,7 @@ cudaError_t run_openes_tell(const OpenEsTellArgs& a, cudaStream_t s) {
   const long long span = a.p1 - a.p0;
   if (span <= 0) return cudaSuccess;
   const int rows = a.mirrored ? a.base : a.n;
-  const int chunks = openes_tell_chunks(rows, span);
+  const int chunks = openes_tell_chunks(rows, a.d);
   const int chunk_rows = (rows + chunks - 1) / chunks;
   const long long threads = (span + TELL_V - 1) / TELL_V;
   dim3 grid((unsigned)((threads + TELL_T - 1) / TELL_T), (unsigned)chunks);

@@ -56,7 +56,7 @@ struct OpenEsTellArgs {
 };
 // Row chunks of the tell's noise contraction for a coordinate span (so the
 // grid fills the GPU; the chunk partials are summed in a fixed order).
-int openes_tell_chunks(int rows, long long span);
+int openes_tell_chunks(int rows, long long d);  // row chunks: a function of (rows, d) only
 cudaError_t run_openes_tell(const OpenEsTellArgs& a, cudaStream_t s);
 cudaError_t run_inc_counter(long long* t, cudaStream_t s);
 cudaError_t run_openes_ask(const double* mean, long long d, double sigma, int mirrored, DKey key, int n,

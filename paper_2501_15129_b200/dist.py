@@ -4,11 +4,12 @@ One process per GPU.  Rank r rolls out the contiguous agent block
 [a0, a1) of the population; the only data-path exchanges per generation are
 
   C1  all-gather of the fitness vector (pop x fp64), plus the per-lane
-      RunningStats (ARS only), and
+      RunningStats (when the resolved obs_norm mode is running_stats), and
   C2  all-gather of the coordinate-sharded mean update: every rank holds the
       full fitness, computes identical ranks, applies the tell (and Adam) to
       coordinates [p0, p1) only -- regenerating the noise rows it needs from
-      the replicated ask key -- and the slices are gathered back.
+      the replicated ask key -- and the slices are gathered back (CEM: the
+      diagonal variance slices too).
 
 Every rank derives the same keys from the replicated (rng, iteration), so no
 noise or candidate traffic crosses NVLink, and the result is bit-identical for
@@ -113,7 +114,18 @@ class CudaShardedEs:
         self.mbuf = torch.zeros(self.pcs, dtype=torch.float64, device=dev)
         self.mall = torch.zeros(self.pcs * world, dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.track = cfg.algo == "ars" and cfg.obs_norm in ("auto", "running_stats")
+        # per-lane RunningStats are tracked iff the handle's RESOLVED obs_norm
+        # mode is running_stats (ARS's "auto", or an explicit running_stats for
+        # any algorithm): every rank then merges all pop x e lanes in phase_tell
+        from . import _lib
+        self.track = self.es.norm_mode() == _lib.NORM["running_stats"]
+        # CEM's tell updates diag_var on [p0, p1) only and the next ask reads
+        # every coordinate: the variance is gathered like the mean
+        self.cem = cfg.algo == "cem"
+        if self.cem:
+            self.var = self._view(self.es.device_var(), self.d)
+            self.vbuf = torch.zeros(self.pcs, dtype=torch.float64, device=dev)
+            self.vall = torch.zeros(self.pcs * world, dtype=torch.float64, device=dev)
         if self.track:
             self.sbuf = torch.zeros(self.acs * self.e * 9, dtype=torch.float64, device=dev)
             self.sall = torch.zeros(self.acs * self.e * 9 * world, dtype=torch.float64, device=dev)
@@ -126,6 +138,16 @@ class CudaShardedEs:
         o.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
                                       "version": 3, "strides": None}
         return self.torch.as_tensor(o, device="cuda")
+
+    def _gather_slices(self, full, buf, allbuf):
+        """All-gather the coordinate slices [p0, p1) of a d-vector in place."""
+        npc = self.p1 - self.p0
+        buf[:npc].copy_(full[self.p0:self.p1])
+        self.dist.all_gather_into_tensor(allbuf, buf)
+        for r in range(self.world):
+            lo, hi = r * self.pcs, min(self.d, (r + 1) * self.pcs)
+            if hi > lo:
+                full[lo:hi].copy_(allbuf[r * self.pcs: r * self.pcs + hi - lo])
 
     def init(self, key):
         self.es.init(key)
@@ -152,13 +174,11 @@ class CudaShardedEs:
                         self.sall[r * self.acs * w: r * self.acs * w + (hi - lo) * w])
         torch.cuda.synchronize()
         m = self.es.phase_tell()         # ranks + tell of [p0, p1) (synchronous)
-        npc = self.p1 - self.p0
-        self.mbuf[:npc].copy_(self.mean[self.p0:self.p1])
-        dist.all_gather_into_tensor(self.mall, self.mbuf)                         # C2
-        for r in range(self.world):
-            lo, hi = r * self.pcs, min(self.d, (r + 1) * self.pcs)
-            if hi > lo:
-                self.mean[lo:hi].copy_(self.mall[r * self.pcs: r * self.pcs + hi - lo])
+        self._gather_slices(self.mean, self.mbuf, self.mall)                      # C2
+        if self.cem:
+            self._gather_slices(self.var, self.vbuf, self.vall)
+            torch.cuda.synchronize()
+            m.values["es/sigma"] = self.es.cem_sigma()
         # WorkflowState::env_steps counts the whole generation
         # (proj/src/workflow_es.cpp:134): each rank summed only its shard's lane
         # steps (episodes are pop x count on every rank), so the step deltas

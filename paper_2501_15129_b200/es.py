@@ -227,6 +227,24 @@ class EsWorkflow:
         check(self.L.evorl_es_counters(self.h, C.byref(it), C.byref(st), C.byref(ep)))
         return it.value, st.value, ep.value
 
+    def rng(self) -> tuple[int, int]:
+        """WorkflowState::rng: the root key of init() or of the loaded checkpoint."""
+        hi, lo = C.c_uint64(), C.c_uint64()
+        check(self.L.evorl_es_get_rng(self.h, C.byref(hi), C.byref(lo)))
+        return hi.value, lo.value
+
+    def norm_mode(self) -> int:
+        """The resolved obs_norm mode (_lib.NORM values; "auto" already resolved)."""
+        m = C.c_int32()
+        check(self.L.evorl_es_norm_mode(self.h, C.byref(m)))
+        return m.value
+
+    def cem_sigma(self) -> float:
+        """es/sigma of a CEM workflow, sqrt(diag_var.mean()) over the full variance."""
+        v = C.c_double()
+        check(self.L.evorl_es_cem_sigma(self.h, C.byref(v)))
+        return v.value
+
     def set_counters(self, iteration: int, env_steps: int, episodes: int) -> None:
         check(self.L.evorl_es_set_counters(self.h, iteration, env_steps, episodes))
 
@@ -257,6 +275,12 @@ class EsWorkflow:
         f, m, s = C.c_void_p(), C.c_void_p(), C.c_void_p()
         check(self.L.evorl_es_device_buffers(self.h, C.byref(f), C.byref(m), C.byref(s)))
         return f.value, m.value, s.value
+
+    def device_var(self) -> int:
+        """Device pointer of CEM's diagonal variance (d doubles)."""
+        v = C.c_void_p()
+        check(self.L.evorl_es_device_var(self.h, C.byref(v)))
+        return v.value
 
     def stream(self) -> int:
         return self.L.evorl_es_stream(self.h)

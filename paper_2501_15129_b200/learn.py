@@ -198,12 +198,22 @@ def eval_key(rng, iteration: int) -> tuple:
 
 
 def learn(wf: EsWorkflow, rng, opt: LearnOptions, metrics: MetricsWriter, clock=None) -> None:
-    """learn() (proj/src/workflow.cpp:46-68) over the device workflow; ``rng``
-    is the WorkflowState root key the workflow was initialised (or loaded)
-    with.  Wall time per step is measured on the host around the blocking
-    ``step`` call, as the reference does with steady_clock."""
+    """learn() (proj/src/workflow.cpp:46-68) over the device workflow.  Eval
+    keys come from the handle's own WorkflowState::rng (``wf.rng()``, the key
+    of init() or of the loaded checkpoint), as WorkflowState::eval_key does
+    (proj/include/evorl/workflow.hpp:42); ``rng`` may be None, and a key that
+    differs from the state's raises ValueError instead of silently producing
+    other eval records.  Wall time per step is measured on the host around the
+    blocking ``step`` call, as the reference does with steady_clock."""
     import time
     clock = clock or time.perf_counter
+    state_rng = wf.rng()
+    if rng is not None:
+        hi, lo = (rng.hi, rng.lo) if hasattr(rng, "hi") else rng
+        if (int(hi), int(lo)) != state_rng:
+            raise ValueError(f"learn(): rng {(int(hi), int(lo))} is not the workflow state's key "
+                             f"{state_rng} (eval keys derive from WorkflowState::rng)")
+    rng = state_rng
     while True:
         it, steps, eps = wf.counters()
         if opt.budget.reached(it, steps, eps):

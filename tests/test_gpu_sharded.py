@@ -22,6 +22,19 @@ CFGS = {
     "ars": dict(algo="ars", env="pendulum", fixed_horizon=True, pop=34, hidden=(8,), max_episode_steps=60),
     "cmaes": dict(algo="cmaes", env="pendulum", fixed_horizon=True, pop=16, hidden=(4,), max_episode_steps=40,
                   vbn_samples=200, cmaes_elites=8, cmaes_sigma0=0.2),
+    # CEM: the diagonal variance is coordinate-sharded too (gathered like the mean)
+    "cem": dict(algo="cem", env="pendulum", fixed_horizon=True, pop=20, hidden=(8,), max_episode_steps=40,
+                vbn_samples=200, cem_elites=6),
+    "ves": dict(algo="ves", env="pendulum", fixed_horizon=True, pop=24, hidden=(8,), max_episode_steps=40,
+                vbn_samples=200, ves_elites=6),
+    # running_stats with a non-ARS algorithm: the lane stats must be gathered
+    "openes_rs": dict(algo="openes", env="pendulum", fixed_horizon=True, pop=22, hidden=(8,),
+                      max_episode_steps=50, obs_norm="running_stats", fitness_episodes=2),
+    # many row chunks in the tell (384 base rows, d = 133121): sized from the
+    # shard span the chunking would be 10 row chunks on one GPU and 12 per rank
+    # at world 2 (a different summation order of the search gradient)
+    "openes_chunks": dict(algo="openes", env="pendulum", fixed_horizon=True, pop=768, hidden=(256, 512),
+                          max_episode_steps=20, vbn_samples=200),
 }
 GENS = 3
 
@@ -40,9 +53,10 @@ def _rank_main(rank, world, algo, port, out_dir):
     r = CudaShardedEs(evb.EsConfig(**CFGS[algo]), rank, world)
     r.init((61, 62))
     for _ in range(GENS):
-        r.step()
+        m = r.step()
     torch.cuda.synchronize()
     if rank == 0:
+        np.save(os.path.join(out_dir, "sigma.npy"), np.array([m["es/sigma"]]))
         np.save(os.path.join(out_dir, "mean.npy"), r.es.mean())
         np.save(os.path.join(out_dir, "fitness.npy"), r.es.fitness())
         np.save(os.path.join(out_dir, "counters.npy"), np.array(r.es.counters()))
@@ -60,7 +74,9 @@ def test_two_rank_sharded_generations_bit_identical(algo, tmp_path):
     mp.spawn(_rank_main, args=(2, algo, port, str(tmp_path)), nprocs=2, join=True)
     g = evb.EsWorkflow(evb.EsConfig(**CFGS[algo])).init((61, 62))
     for _ in range(GENS):
-        g.step()
+        m = g.step()
     assert np.array_equal(np.load(tmp_path / "mean.npy"), g.mean())
     assert np.array_equal(np.load(tmp_path / "fitness.npy"), g.fitness())
     assert tuple(np.load(tmp_path / "counters.npy")) == g.counters()
+    if algo == "cem":
+        assert np.array_equal(np.load(tmp_path / "sigma.npy"), np.array([m["es/sigma"]]))

@@ -143,3 +143,31 @@ def test_es_config_entries_use_registry_spelling():
     assert e["ec.openes.sigma"] == "0.02" and e["ec.cem.var_init"] == "1e-3" and e["ec.cem.noise_end"] == "1e-5"
     assert e["net.hidden"] == "64,64" and e["env.fixed_horizon"] == "false" and e["ec.openes.mirrored"] == "true"
     assert e["ec.openes.noise_table_size"] == "4194304" and e["workflow"] == "es" and e["seed"] == "0"
+
+
+@pytest.mark.gpu
+def test_learn_eval_keys_follow_the_loaded_state_rng(tmp_path):
+    """Eval keys derive from WorkflowState::rng (proj/include/evorl/workflow.hpp:42):
+    after load(), learn() evaluates at the checkpoint's key, and a caller key
+    that differs from the state's is refused instead of silently used."""
+    import paper_2501_15129_b200 as evb
+    from paper_2501_15129_b200.learn import eval_key, key_from_seed, learn
+    cfg = evb.EsConfig(algo="openes", env="pendulum", fixed_horizon=True, max_episode_steps=40, pop=16,
+                       hidden=(8,), vbn_samples=200)
+    root = key_from_seed(11)
+    a = evb.EsWorkflow(cfg).init(root)
+    a.step()
+    a.save(str(tmp_path / "ck.bin"))
+    b = evb.EsWorkflow(cfg).init(key_from_seed(12)).load(str(tmp_path / "ck.bin"))
+    assert b.rng() == root
+    with pytest.raises(ValueError):
+        learn(b, key_from_seed(12), LearnOptions(Budget(iterations=2)), MetricsWriter(
+            str(tmp_path / "m.jsonl"), str(tmp_path / "t.log")))
+    mw = MetricsWriter(str(tmp_path / "m2.jsonl"), str(tmp_path / "t2.log"))
+    learn(b, None, LearnOptions(Budget(iterations=2), eval_interval=2, eval_episodes=4), mw)
+    mw.close()
+    recs = [json.loads(x) for x in open(tmp_path / "m2.jsonl").read().splitlines()]
+    ev = [r for r in recs if r["type"] == "eval"][0]
+    a.step()
+    mr, _ = a.evaluate(4, eval_key(root, 2))
+    assert ev["eval/episode_return_mean"] == mr
