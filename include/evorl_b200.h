@@ -27,6 +27,11 @@
  *    (W2 a multiple of 128, W1 <= 256) on the tcgen05 tensor cores as a
  *    3-pass fp16 hi/lo split with fp32 accumulation in TMEM (fp32-level
  *    accuracy) and the other layers in fp32; other shapes run as EVORL_PREC_F32.
+ *    EVORL_PREC_OZ keeps fp64-level accuracy on the tensor cores: the dense
+ *    hidden layer of obs -> W1 -> W2 -> O policies (W1 <= 256) runs as exact
+ *    int8 tcgen05 MMAs over 6 byte slices of per-row / per-lane fixed-point
+ *    operands (Ozaki scheme, ~47 bits per operand, int32 accumulation), every
+ *    other layer, the head and the env in fp64; other shapes run as F64.
  */
 #ifndef EVORL_B200_H
 #define EVORL_B200_H
@@ -52,7 +57,7 @@ enum {
   EVORL_E_CHECKPOINT = 8        /* evorl::CheckpointError (proj/include/evorl/checkpoint.hpp:14-16) */
 };
 
-enum { EVORL_PREC_F64 = 0, EVORL_PREC_F32 = 1, EVORL_PREC_TC = 2 };
+enum { EVORL_PREC_F64 = 0, EVORL_PREC_F32 = 1, EVORL_PREC_TC = 2, EVORL_PREC_OZ = 3 };
 enum { EVORL_ENV_CARTPOLE = 0, EVORL_ENV_PENDULUM = 1 };
 enum { EVORL_ALGO_OPENES = 0, EVORL_ALGO_ARS = 1, EVORL_ALGO_VES = 2, EVORL_ALGO_CMAES = 3,
        EVORL_ALGO_CEM = 4 };

@@ -25,8 +25,8 @@ EVORL_E_CUDA = 6
 EVORL_E_UNSUPPORTED = 7
 EVORL_E_CHECKPOINT = 8
 
-PREC_F64, PREC_F32, PREC_TC = 0, 1, 2
-PRECISIONS = {"f64": PREC_F64, "f32": PREC_F32, "tc": PREC_TC}
+PREC_F64, PREC_F32, PREC_TC, PREC_OZ = 0, 1, 2, 3
+PRECISIONS = {"f64": PREC_F64, "f32": PREC_F32, "tc": PREC_TC, "oz": PREC_OZ}
 ENV_CARTPOLE, ENV_PENDULUM = 0, 1
 ALGO = {"openes": 0, "ars": 1, "ves": 2, "cmaes": 3, "cem": 4}
 NORM = {"auto": -1, "none": 0, "vbn": 1, "running_stats": 2}

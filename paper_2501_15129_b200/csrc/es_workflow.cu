@@ -313,8 +313,9 @@ static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** 
   if (cfg->algo < 0 || cfg->algo > EVORL_ALGO_CEM) return set_err(EVORL_E_CONFIG, "ec.algo: unknown algorithm");
   if (cfg->env_id != EVORL_ENV_CARTPOLE && cfg->env_id != EVORL_ENV_PENDULUM)
     return set_err(EVORL_E_INVALID_ARGUMENT, "unknown env id");
-  if (cfg->precision != EVORL_PREC_F64 && cfg->precision != EVORL_PREC_F32 && cfg->precision != EVORL_PREC_TC)
-    return set_err(EVORL_E_INVALID_ARGUMENT, "precision must be EVORL_PREC_F64, EVORL_PREC_F32 or EVORL_PREC_TC");
+  if (cfg->precision < EVORL_PREC_F64 || cfg->precision > EVORL_PREC_OZ)
+    return set_err(EVORL_E_INVALID_ARGUMENT,
+                   "precision must be EVORL_PREC_F64, EVORL_PREC_F32, EVORL_PREC_TC or EVORL_PREC_OZ");
   if (cfg->pop < 1 || cfg->fitness_episodes < 1)
     return set_err(EVORL_E_INVALID_ARGUMENT, "ec.pop and ec.fitness_episodes must be positive");
   auto* s = new evorl_es();
@@ -352,7 +353,7 @@ static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** 
   const bool cta_ok = plan_rollout(s->net, s->env.obs_dim, s->e, cfg->precision, &s->plan);
   // warp-per-lane only pays when there are enough lanes to fill the SMs
   // (>= 512 lanes); fewer lanes get a whole CTA each to cut step latency.
-  s->warp_path = !(cta_ok && s->plan.tc) && (long long)cfg->pop * s->e >= 512 &&
+  s->warp_path = !(cta_ok && (s->plan.tc || s->plan.oz)) && (long long)cfg->pop * s->e >= 512 &&
                  plan_rollout_warp(s->net, s->env.obs_dim, s->e, cfg->precision, &s->wplan);
   if (!cta_ok && !s->warp_path) {
     delete s;
@@ -410,9 +411,10 @@ static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** 
     A(dalloc(&s->d_offsets, (size_t)n));
   }
   if (team_mat) {
-    const size_t tsz = cfg->precision == EVORL_PREC_F64 ? sizeof(double) : sizeof(float);
+    const bool f64 = cfg->precision == EVORL_PREC_F64 || cfg->precision == EVORL_PREC_OZ;  // fp64 candidates
+    const size_t tsz = f64 ? sizeof(double) : sizeof(float);
     s->cand_cap = (int)std::max(1.0, std::min((double)n, std::floor(kCandCap / ((double)d * tsz))));
-    if (cfg->precision == EVORL_PREC_F64) {
+    if (f64) {
       A(dalloc(&s->d_cand, (size_t)s->cand_cap * d));
     } else {
       A(dalloc(&s->d_cand_f32, (size_t)s->cand_cap * d));
@@ -1289,7 +1291,7 @@ extern "C" int evorl_es_evaluate(evorl_es* s, int32_t episodes, uint64_t key_hi,
   a.lane_steps = steps;
   a.fault = s->d_fault;
   float* mean_f32 = nullptr;
-  if (plan.gw && s->cfg.precision != EVORL_PREC_F64) {  // global-weights fp32 team reads an fp32 row
+  if (plan.gw && s->cfg.precision != EVORL_PREC_F64 && s->cfg.precision != EVORL_PREC_OZ) {  // fp32 gw team: fp32 row
     CK(cudaMallocAsync((void**)&mean_f32, sizeof(float) * s->d, s->stream));
     CK(run_materialize_f32(a.par, s->d, 0, 1, mean_f32, s->stream));
     a.par.src = SRC_EXPLICIT_F32;
@@ -1450,14 +1452,14 @@ static int batched_rollout_impl(const evorl_env_desc* envd, const evorl_mlp_desc
   if (netd->input_dim != env.obs_dim) return set_err(EVORL_E_INVALID_ARGUMENT, "net input_dim != obs_dim");
   SmemPlan plan{};
   WarpPlanOut wplan{};
-  if (precision < EVORL_PREC_F64 || precision > EVORL_PREC_TC)
+  if (precision < EVORL_PREC_F64 || precision > EVORL_PREC_OZ)
     return set_err(EVORL_E_INVALID_ARGUMENT, "unknown precision");
   // transitions are written by the cluster team (the tc team evaluates as f32)
   const bool cta_ok = plan_rollout(net, env.obs_dim, e, tr && precision == EVORL_PREC_TC ? EVORL_PREC_F32 : precision,
                                    &plan, tr != nullptr);
   if (tr) plan.trn = 1;
   const bool use_warp =
-      !tr && !(cta_ok && plan.tc) && plan_rollout_warp(net, env.obs_dim, e, precision, &wplan);
+      !tr && !(cta_ok && (plan.tc || plan.oz)) && plan_rollout_warp(net, env.obs_dim, e, precision, &wplan);
   if (!cta_ok && !use_warp)
     return set_err(EVORL_E_UNSUPPORTED, "policy too large for a shared-memory resident team");
   const long long d = net.d;
@@ -1519,7 +1521,7 @@ static int batched_rollout_impl(const evorl_env_desc* envd, const evorl_mlp_desc
     a.t_cap = tr->row_cap;
   }
   Scratch sf32;
-  if (!use_warp && plan.gw && precision != EVORL_PREC_F64) {  // global-weights fp32 team reads fp32 rows
+  if (!use_warp && plan.gw && precision != EVORL_PREC_F64 && precision != EVORL_PREC_OZ) {  // fp32 gw team
     float* pf = nullptr;
     if (int rc = up(sf32, (const float*)nullptr, (size_t)m * d, &pf)) return rc;
     CK(run_materialize_f32(a.par, d, 0, m, pf, 0));

@@ -1315,6 +1315,17 @@ bool plan_rollout(const NetDesc& net, int obs_dim, int e, int precision, SmemPla
   const int ET = e >= 5 ? 16 : (e >= 2 ? 4 : 1);
   plan->trn = 0;
   plan->pipe = 0;
+  plan->oz = 0;
+  if (precision == 3) {  // EVORL_PREC_OZ: int8-sliced tcgen05 team if the shape fits, else the fp64 team
+    if (!simple_only && plan_rollout_oz(net, obs_dim, e, &plan->tcp)) {
+      plan->oz = 1;
+      plan->tc = 0;
+      plan->ET = 16;
+      plan->C = plan->tcp.data[0];
+      return true;
+    }
+    precision = 0;
+  }
   if (simple_only) {  // TR = 1 SIMT, resident or global-weights
     plan->tc = 0;
     const int ts = precision == 0 ? 8 : 4;
@@ -1451,8 +1462,9 @@ static cudaError_t launch_t(const RolloutArgs& a, cudaStream_t s) {
 cudaError_t launch_rollout(const RolloutArgs& a, int precision, cudaStream_t stream) {
   if (a.n_agents <= 0) return cudaSuccess;
   if (a.plan.tc) return launch_rollout_tc(a, a.plan.tcp, stream);
+  if (a.plan.oz) return launch_rollout_oz(a, a.plan.tcp, stream);
   if (a.plan.pipe) return launch_pipe(a, stream);
-  return precision == 0 ? launch_t<double>(a, stream) : launch_t<float>(a, stream);
+  return (precision == 0 || precision == 3) ? launch_t<double>(a, stream) : launch_t<float>(a, stream);
 }
 
 }  // namespace evorl_b200

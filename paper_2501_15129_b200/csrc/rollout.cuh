@@ -119,6 +119,7 @@ struct SmemPlan {
   int trn;        // 1: collect transitions (RolloutArgs::t_*), TR = 1 SIMT plans only
   int tc;         // 1: EVORL_PREC_TC tcgen05 team (rollout_tc.cu), plan in tcp
   int pipe;       // 1: pipelined fp64 DMMA team (two 8-lane groups, env warp)
+  int oz;         // 1: EVORL_PREC_OZ int8-sliced tcgen05 team (rollout_oz.cu), plan in tcp
   TcPlanOut tcp;
 };
 
@@ -192,5 +193,11 @@ long long tc_block_bytes(const TcPlanOut& plan);
 cudaError_t run_tc_split(const float* cand, const NetDesc& net, const TcPlanOut& plan, int n_agents,
                          unsigned char* blocks, cudaStream_t stream);
 cudaError_t launch_rollout_tc(const RolloutArgs& a, const TcPlanOut& plan, cudaStream_t stream);
+
+// fp64-accurate tensor-core rollout (rollout_oz.cu, precision EVORL_PREC_OZ):
+// obs -> W1 -> W2 -> O policies, W1 <= 256; the W2 x W1 layer as S byte-sliced
+// fixed-point int8 tcgen05 MMAs, everything else fp64.
+bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out);
+cudaError_t launch_rollout_oz(const RolloutArgs& a, const TcPlanOut& plan, cudaStream_t stream);
 
 }  // namespace evorl_b200

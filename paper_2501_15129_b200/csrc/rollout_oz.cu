@@ -1,0 +1,663 @@
+// rollout_oz.cu -- the population rollout with the hidden-layer GEMM on the
+// int8 tensor cores (tcgen05 kind::i8) at fp64-level accuracy: precision
+// EVORL_PREC_OZ (sliced fixed point, the Ozaki scheme).
+//
+// Same lane-team semantics as rollout_kernel (proj/src/rollout.cpp:94-174,
+// one team per (agent, group of 16 lanes)); the env, the observation
+// normaliser, layer 0, the output layer and the head stay fp64 on the CUDA
+// cores in the fp64 team's operation order.  What changes is the dense
+// W2 x W1 layer (proj/src/net.cpp:96, z = W h + b):
+//   * Each weight row r is a signed fixed-point integer W_int = trunc(W 2^F_r)
+//     with |W_int| < 2^(8S-1) (F_r from the row's largest |w|), cut into S
+//     bytes from the top: A_0 = W_int >> 8(S-1) (s8), A_i = byte i (u8).
+//     Each activation column (lane) e is h_int = trunc(h 2^G_e) < 2^(8S-1)
+//     (h >= 0 after ReLU; G_e from a per-lane bound), bytes B_j (u8).
+//   * W_int h_int = sum_{i,j} A_i B_j 2^(8(2S-2-i-j)); the terms i + j < S are
+//     kept: D_t = sum_{i+j=t} A_i B_j, t < S, exact in int32 (|D_t| < S 2^24).
+//     z = 2^(8(S-1) - F_r - G_e) sum_t D_t 2^(8(S-1-t)), combined in fp64.
+//     S = 6 keeps ~47 bits of every operand: the policy output differs from
+//     fp64 arithmetic by ~1e-13 relative (fitness differences at the level of
+//     the fp64 path's own libm/ordering differences from the reference CPU).
+//   * One accumulator for all t: the B operand lives in SMEM as S data blocks
+//     behind S-1 zero blocks of 16 lanes, [0 .. 0 | B_0 .. B_(S-1)], and MMA i
+//     (A_i from TMEM) reads the window that starts at block S-1-i, so column
+//     block c of D receives A_i B_(c-i) (zero for c < i): D[:, 16t..16t+15] = D_t.
+//     Per k-step of 32: S TS MMAs of M = 128, N = 16 S, K = 32 (S = 6: 48 MMAs
+//     of ~50 cycles per env step, measured by tools/umma_i8_bench.cu at the
+//     int8 peak rate).
+//   * TMEM (512 columns, one team CTA per SM): A slices at columns 512 - S W1p/4
+//     (written once by tcgen05.st), D at columns 0 .. 16 S.
+//   * Per env step (one CTA = 128 weight rows; C = W2/128 CTAs per agent):
+//     layer 0 (fp64, replicated) -> per-lane bound, fixed point, bytes -> B
+//     (STS.128 per slice) | MMAs (one elected thread) | epilogue: tcgen05.ld of
+//     D_0..D_(S-1), fp64 combine, bias, ReLU, output-layer partial (warp
+//     reduce-scatter) | st.async partial outputs to every CTA of the cluster |
+//     16 env threads: head, fp64 env step, observe.
+//   * Rows holding a non-finite weight (a diverged mean) are computed by an
+//     fp64 dot product instead (IEEE propagation and NetFault as the fp64 team).
+#include <algorithm>
+#include <cstring>
+
+#include "rollout.cuh"
+
+namespace evorl_b200 {
+
+constexpr int OZ_THREADS = 256;
+constexpr int OZ_M = 128;  // weight rows per CTA (UMMA M)
+constexpr int OZ_N = 16;   // lanes per team
+constexpr int OZ_MAXO = 8;
+constexpr int OZ_TMEM_COLS = 512;
+constexpr int OZ_MIN_SMEM = 120 * 1024;  // > half an SM's shared memory: one team CTA per SM (TMEM)
+
+#ifdef EVB_TC_PROFILE
+__device__ unsigned long long g_oz_prof[16];
+#define OZ_MARK(i)                               \
+  do {                                           \
+    const long long t_ = clock64();              \
+    prof[i] += (unsigned long long)(t_ - tprev); \
+    tprev = t_;                                  \
+  } while (0)
+#else
+#define OZ_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
+struct OzPlan {
+  int C;       // CTAs per agent (cluster): power of two >= W2 / 128
+  int S;       // byte slices per operand
+  int W1, W2;  // hidden widths
+  int W1p;     // W1 rounded up to the MMA K step (32)
+  int off_B, off_W0, off_b0, off_mk, off_x0, off_sce, off_red, off_pout, off_mask, off_bar, off_tslot, off_h0s,
+      off_rmax;
+  int used;   // bytes of the layout (zeroed by the prologue)
+  int bytes;  // dynamic SMEM requested: >= OZ_MIN_SMEM
+};
+
+EVB_DEV uint64_t oz_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1, SWIZZLE_NONE
+}
+// kind::i8 instruction descriptor: D = s32 (c_format 2), A = s8 (1) or u8 (0),
+// B = u8, both K-major
+constexpr uint32_t oz_idesc(int M, int N, bool a_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+EVB_DEV void oz_mma_ts_elect(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+EVB_DEV void oz_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+EVB_DEV void oz_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+}
+EVB_DEV void oz_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+// fmax over finite values only (NaN / inf weights are handled by the fp64 row path)
+EVB_DEV double fin_abs(double v) { return isfinite(v) ? fabs(v) : 0.0; }
+// the power-of-two exponent e with |v| < 2^e (v finite, >= 0), clamped so that
+// 2^(+-(8S + e)) stays a normal double
+EVB_DEV int bound_exp(double v) {
+  int e = 0;
+  if (v > 0.0) frexp(v, &e);
+  return max(-960, min(960, e));
+}
+// atomic max of a non-negative double (bit patterns order like the values)
+EVB_DEV void smem_max_nonneg(double* p, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
+}
+
+template <int S, int C>
+__global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_constant__ RolloutArgs A,
+                                                                   const __grid_constant__ OzPlan P) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const NetDesc& N = A.net;
+  const EnvDesc& E = A.env;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant, lane half (epilogue)
+  const int crank = C > 1 ? (int)cluster_ctarank() : 0;
+  const int team = blockIdx.x / C;
+  const int agent_local = team / A.groups;
+  const int group = team % A.groups;
+  const int agent = A.agent_offset + agent_local;
+  const int W1 = P.W1, W1p = P.W1p, W2 = P.W2, O = N.dims[3], K0 = N.dims[0];
+  const int r0 = crank * OZ_M;  // this CTA's rows of layer 1
+  const int row = quad * 32 + lane;
+  constexpr int RB = OZ_N * (2 * S - 1);         // rows (N) of the zero-padded B buffer
+  const uint32_t LBO = (uint32_t)(RB / 8) * 128;  // K-direction core-matrix stride
+  const uint32_t colA = (uint32_t)(OZ_TMEM_COLS - S * (W1p / 4));
+
+#ifdef EVB_TC_PROFILE
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+#endif
+  for (int i = tid; i < P.used / 4; i += OZ_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
+  uint64_t* xbar = mbar + 1;  // [2]: partial outputs of every cluster CTA landed (by step parity)
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(OZ_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  double* W0 = reinterpret_cast<double*>(smem + P.off_W0);  // [k][W1p], zero past W1
+  double* b0 = reinterpret_cast<double*>(smem + P.off_b0);  // W1p
+  double* mk = reinterpret_cast<double*>(smem + P.off_mk);  // [0..3] max_r |W0[r][k]|, [4] max_r |b0[r]|
+  double* rmax = reinterpret_cast<double*>(smem + P.off_rmax);  // [2][128] row max |W1| per k half
+  unsigned char* Bs = smem + P.off_B;
+  // ---- prologue: layer 0 (fp64, replicated) and its per-column maxima
+  for (int i = tid; i < K0 * W1; i += OZ_THREADS) {
+    const int k = i / W1, r = i % W1;
+    const double w = param_value(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W1 + r);
+    W0[k * W1p + r] = w;
+    smem_max_nonneg(&mk[k], fin_abs(w));  // (SMEM atomics: once per rollout)
+  }
+  for (int r = tid; r < W1; r += OZ_THREADS) {
+    const double b = param_value(A.par, N.d, agent_local, agent, N.b_off[0] + r);
+    b0[r] = b;
+    smem_max_nonneg(&mk[4], fin_abs(b));
+  }
+  // ---- layer-1 weights of row `row`: per-row fixed point, S byte slices -> TMEM.
+  // Warp halves take alternate 32-wide k chunks (one tcgen05.st.x8 per slice).
+  const bool row_ok = r0 + row < W2;  // zero rows past W2
+  auto w1 = [&](int k) -> double {
+    return (row_ok && k < W1) ? param_value(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + row)
+                              : 0.0;
+  };
+  double rm = 0.0;
+  bool rfin = true;
+  for (int c = half; c < W1p / 32; c += 2)
+    for (int q = 0; q < 32; ++q) {
+      const double w = w1(c * 32 + q);
+      rm = fmax(rm, fin_abs(w));
+      rfin = rfin && isfinite(w);
+    }
+  rmax[half * OZ_M + row] = rm;
+  // any non-finite weight in this CTA's slice: rows with one take the fp64 path
+  // (and the CTA keeps an fp64 copy of the layer-1 input for them)
+  const bool slow_cta = __syncthreads_or(!rfin) != 0;
+  rm = fmax(rmax[row], rmax[OZ_M + row]);
+  const int Fr = 8 * S - 1 - bound_exp(rm);  // |W_int| < 2^(8S-1)
+  const double wscale = ldexp(1.0, Fr);
+  for (int c = half; c < W1p / 32; c += 2) {
+    long long wi[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const double w = w1(c * 32 + q);
+      wi[q] = isfinite(w) ? __double2ll_rz(w * wscale) : 0ll;
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      uint32_t packed[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint32_t word = 0u;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) word |= (uint32_t)((wi[4 * u + b] >> (8 * (S - 1 - i))) & 0xFF) << (8 * b);
+        packed[u] = word;
+      }
+      oz_st8(tmem + ((uint32_t)(quad * 32) << 16) + colA + (uint32_t)(i * (W1p / 4) + c * 8), packed);
+    }
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  // per-thread epilogue constants: this row's scale 2^(8(S-1) - F_r), bias, output weights
+  bool rbad = false;  // this row holds a non-finite weight (fp64 path)
+  if (slow_cta)
+    for (int k = 0; k < W1; ++k) rbad = rbad || !isfinite(w1(k));
+  const double rscale = ldexp(1.0, 8 * (S - 1) - Fr);
+  const double b1r = row_ok ? param_value(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row) : 0.0;
+  double w2r[OZ_MAXO], b2[OZ_MAXO];
+#pragma unroll
+  for (int o = 0; o < OZ_MAXO; ++o) {
+    w2r[o] = (o < O && row_ok) ? param_value(A.par, N.d, agent_local, agent, N.w_off[2] + (long long)(r0 + row) * O + o)
+                               : 0.0;
+    b2[o] = o < O ? param_value(A.par, N.d, agent_local, agent, N.b_off[2] + o) : 0.0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if constexpr (C > 1) cluster_sync_all();
+
+  // ---- lane state
+  const int j = group * OZ_N + tid;
+  const bool is_env = tid < OZ_N;
+  const bool valid = is_env && j < A.e;
+  const int per = A.count / A.e, rem = A.count % A.e;
+  const int eps_this = valid ? per + (j < rem ? 1 : 0) : 0;
+  const int slot0 = valid ? j * per + min(j, rem) : 0;
+  LaneEnv s{};
+  double ep_ret = 0.0, wc = 0.0, wmean[4] = {0, 0, 0, 0}, wm2[4] = {0, 0, 0, 0};
+  int ep_len = 0, eps_done = 0;
+  long long steps = 0;
+  uint32_t myfault = 0, myfault_layer = 0;
+  if (valid) {
+    const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
+    env_reset(E, fold_in(lane_key, 0), s);  // proj/src/rollout.cpp:104
+  }
+  NormParams nrm;
+  nrm.active = 0;
+  if (A.norm != nullptr) nrm = *A.norm;
+  double* x0 = reinterpret_cast<double*>(smem + P.off_x0);    // [4][16]
+  double* sce = reinterpret_cast<double*>(smem + P.off_sce);  // [16] 2^-G_e
+  double* red = reinterpret_cast<double*>(smem + P.off_red);  // [4 quadrants][O][16]
+  double* h0s = reinterpret_cast<double*>(smem + P.off_h0s);  // [W1p][16] fp64 layer-1 input (slow_cta only)
+  double* pout_base = reinterpret_cast<double*>(smem + P.off_pout);
+  uint32_t* mask = reinterpret_cast<uint32_t*>(smem + P.off_mask);
+  const int OE = O * OZ_N, OE1 = (O + 1) * OZ_N;
+  double sin_th = 0.0;
+  // observation -> (RunningStats) -> normalisation (the fp64 team's operations,
+  // proj/src/rollout.cpp:124-126, proj/src/obs_norm.cpp:7-18, :76-79)
+  auto observe_into_x0 = [&](bool act) {
+    double raw[4];
+    observe(E, s, raw);
+    sin_th = raw[1];
+    if (act && A.track_stats) {
+      if (wc == 0.0) {
+        for (int i = 0; i < E.obs_dim; ++i) {
+          wmean[i] = raw[i];
+          wm2[i] = 0.0;
+        }
+        wc = 1.0;
+      } else {
+        wc = dadd(wc, 1.0);
+        for (int i = 0; i < E.obs_dim; ++i) {
+          const double delta = dsub(raw[i], wmean[i]);
+          wmean[i] = dadd(wmean[i], ddiv(delta, wc));
+          wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
+        }
+      }
+    }
+    for (int i = 0; i < E.obs_dim; ++i) {
+      double v = raw[i];
+      if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
+      x0[i * OZ_N + tid] = act ? v : 0.0;
+    }
+  };
+  if (valid && eps_this > 0 && A.max_iters > 0) observe_into_x0(true);
+  // layer-0 thread map: lane e, 16 consecutive rows = one 16-byte K row of a B core matrix
+  const int le = tid & 15, rg = tid >> 4;
+  const bool l0_active = rg * 16 < W1p;
+  unsigned char* Bme = Bs + (size_t)rg * LBO + (size_t)(le >> 3) * 128 + (le & 7) * 16;
+
+  OZ_MARK(0);  // prologue
+  for (int it = 0;; ++it) {
+    if (tid < MAXL) mask[tid] = 0u;
+    const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
+    if (!__syncthreads_or(active)) break;
+    OZ_MARK(1);  // loop-top barrier
+    double* pout = pout_base + (it & 1) * C * OE1;
+    if (C > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[it & 1], (uint32_t)(C * OE1 * sizeof(double)));
+
+    // ---- layer 0 (fp64): h = relu(W0 x + b0) for lane le, rows 16 rg .. 16 rg + 15,
+    // then h_int = trunc(h 2^G) (G from the lane bound sum_k max|W0[.][k]| |x_k| + max|b0|)
+    // and its S bytes -> the B data blocks (one 16-byte store per slice)
+    {
+      uint32_t bad = 0u;
+      if (l0_active) {
+        double xr[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xr[k] = k < K0 ? x0[k * OZ_N + le] : 0.0;
+        double bnd = mk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < K0) bnd = fma(mk[k], fabs(xr[k]), bnd);
+        bnd = bnd * (1.0 + 0x1.0p-40);  // covers the rounding of the fma chains below
+        const int G = 8 * S - 1 - bound_exp(bnd);
+        const double hscale = ldexp(1.0, G);
+        if (rg == 0) sce[le] = ldexp(1.0, -G);
+        unsigned long long hq[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int r = rg * 16 + u;
+          double z = 0.0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < K0) z = fma(W0[k * W1p + r], xr[k], z);
+          z = z + b0[r];
+          const double h = z > 0.0 ? z : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
+          if (h == INFINITY) bad = 1u << le;
+          if (slow_cta) h0s[r * OZ_N + le] = h;
+          hq[u] = h < INFINITY ? __double2ull_rz(h * hscale) : 0ull;
+        }
+#pragma unroll
+        for (int jj = 0; jj < S; ++jj) {
+          uint32_t wv[4];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            uint32_t word = 0u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) word |= (uint32_t)((hq[4 * w + b] >> (8 * (S - 1 - jj))) & 0xFFull) << (8 * b);
+            wv[w] = word;
+          }
+          *reinterpret_cast<uint4*>(Bme + (size_t)(S - 1 + jj) * 256) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+      }
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      if (lane == 0 && bad) atomicOr(&mask[0], bad);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B visible to the tensor core
+    }
+    __syncthreads();
+    OZ_MARK(2);  // layer 0 + slicing
+    if (warp == 0) {  // layer 1 on tcgen05: S MMAs per k-step into one accumulator
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t bS = smem_u32(Bs);
+      for (int ks = 0; ks < W1p / 32; ++ks) {
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          const uint64_t bd = oz_desc(bS + (uint32_t)(S - 1 - i) * 256 + (uint32_t)ks * 2 * LBO, LBO, 128);
+          oz_mma_ts_elect(tmem, tmem + colA + (uint32_t)(i * (W1p / 4) + ks * 8), bd, oz_idesc(OZ_M, OZ_N * S, i == 0),
+                          (ks | i) ? 1u : 0u);
+        }
+      }
+      oz_commit_elect(mbar);
+    }
+    mbar_wait_parity_cta(mbar, (uint32_t)(it & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    OZ_MARK(3);  // MMA
+    // ---- epilogue: row `row`, lanes 8 half .. 8 half + 7; output layer fused
+    {
+      uint32_t d[S][8];
+      const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * 8);
+#pragma unroll
+      for (int t = 0; t < S; ++t) oz_ld8(tl + (uint32_t)(t * OZ_N), d[t]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      double h[8];
+      uint32_t bad = 0u;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = half * 8 + q;
+        double acc = (double)(int)d[0][q];
+#pragma unroll
+        for (int t = 1; t < S; ++t) acc = fma(acc, 256.0, (double)(int)d[t][q]);
+        double z = (acc * rscale) * sce[e];
+        if (rbad) {  // non-finite weight in this row: fp64 dot product (IEEE propagation)
+          z = 0.0;
+          for (int k = 0; k < W1; ++k) z = fma(w1(k), h0s[k * OZ_N + e], z);
+        }
+        z = z + b1r;
+        h[q] = z > 0.0 ? z : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
+        if (h[q] == INFINITY) bad |= 1u << e;
+      }
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      if (lane == 0 && bad) atomicOr(&mask[1], bad);
+      // per output o: v[q] = w2[row][o] h[q], summed over the warp's 32 rows by
+      // a reduce-scatter (lane bits 4, 3, 2 select the lane q it ends on)
+      const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, bb2 = (lane >> 2) & 1;
+#pragma unroll
+      for (int o = 0; o < OZ_MAXO; ++o) {
+        if (o >= O) break;
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = w2r[o] * h[q];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double send = b4 ? v[i] : v[i + 4];
+          const double keep = b4 ? v[i + 4] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double send = b3 ? v[i] : v[i + 2];
+          const double keep = b3 ? v[i + 2] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const double send = bb2 ? v[0] : v[1];
+          const double keep = bb2 ? v[1] : v[0];
+          v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        if ((lane & 3) == 0) red[(quad * O + o) * OZ_N + half * 8 + b4 * 4 + b3 * 2 + bb2] = v[0];
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    OZ_MARK(4);  // epilogue
+    // this CTA's partial outputs (fixed quadrant order) + each lane's first
+    // non-finite layer -> every CTA of the cluster
+    for (int oe = tid; oe < OE1; oe += OZ_THREADS) {
+      double v;
+      if (oe < OE) {
+        v = ((red[oe] + red[OE + oe]) + red[2 * OE + oe]) + red[3 * OE + oe];
+      } else {
+        const int e = oe - OE;
+        int bl = 3;
+        for (int l = 1; l >= 0; --l)
+          if ((mask[l] >> e) & 1u) bl = l;
+        v = (double)bl;
+      }
+      if constexpr (C > 1) {
+        const uint32_t la = smem_u32(pout + crank * OE1 + oe), lb = smem_u32(&xbar[it & 1]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) st_async(map_cluster(la, (uint32_t)c), v, map_cluster(lb, (uint32_t)c));
+      } else {
+        pout[oe] = v;
+      }
+    }
+    if constexpr (C > 1) {
+      if (tid < OZ_N) mbar_wait_parity(&xbar[it & 1], (uint32_t)((it >> 1) & 1));
+    } else {
+      __syncthreads();
+    }
+    OZ_MARK(5);  // cluster exchange
+    // ---- head + env step (proj/src/rollout.cpp:57-90, :131-153), next observation
+    if (active) {
+      double z[OZ_MAXO];
+      bool nonfinite_out = false;
+      int bad_layer = 3;
+      for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pout[c * OE1 + OE + tid]);
+      for (int o = 0; o < O; ++o) {
+        double v = pout[o * OZ_N + tid];
+        for (int c = 1; c < C; ++c) v += pout[c * OE1 + o * OZ_N + tid];
+        v = v + b2[o];
+        z[o] = v;
+        if (!isfinite(v)) nonfinite_out = true;
+      }
+      if (bad_layer == 3 && nonfinite_out) bad_layer = 2;
+      if (bad_layer < 3) {  // NetFault: the lowest layer with a non-finite activation
+        myfault = FAULT_NET;
+        myfault_layer = (uint32_t)bad_layer;
+      } else {
+        double action;
+        if (N.head == HEAD_CATEGORICAL) {
+          int arg = 0;
+          for (int o = 1; o < O; ++o)
+            if (z[o] > z[arg]) arg = o;  // maxCoeff: first maximum
+          action = (double)arg;
+        } else if (N.head == HEAD_TANH) {
+          action = N.tanh_scale * tanh(z[0]);
+        } else {
+          action = z[0];
+        }
+        double reward = 0.0;
+        bool term = false, trunc = false;
+        const uint32_t f = env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr);
+        if (f) {
+          myfault = f;
+        } else {
+          ep_ret = dadd(ep_ret, reward);  // proj/src/rollout.cpp:143
+          ep_len += 1;
+          steps += 1;
+          if (term || trunc) {
+            if (crank == 0) {
+              const long long sl = (long long)agent_local * A.count + slot0 + eps_done;
+              A.ep_returns[sl] = ep_ret;
+              if (A.ep_lengths) A.ep_lengths[sl] = ep_len;
+            }
+            ep_ret = 0.0;
+            ep_len = 0;
+            eps_done += 1;
+            if (eps_done < eps_this) env_reset(E, s.rng, s);  // auto-reset, env.cpp:163-167
+          }
+        }
+      }
+      const bool next = myfault == 0 && eps_done < eps_this && it + 1 < A.max_iters;
+      observe_into_x0(next);
+    }
+    OZ_MARK(6);  // head + env + observe
+  }
+#ifdef EVB_TC_PROFILE
+  if (tid == 0) {
+    for (int i = 0; i < 7; ++i) atomicAdd(&g_oz_prof[i], prof[i]);
+    atomicAdd(&g_oz_prof[8], 1ull);
+  }
+#endif
+
+  if (valid && crank == 0) {
+    const long long ln = (long long)agent_local * A.e + j;
+    if (A.lane_steps) A.lane_steps[ln] = steps;
+    if (A.track_stats && A.lane_stats) {
+      double* st = A.lane_stats + ln * 9;
+      st[0] = wc;
+      for (int i = 0; i < 4; ++i) {
+        st[1 + i] = wmean[i];
+        st[5 + i] = wm2[i];
+      }
+    }
+    if (myfault) record_fault(A.fault, (uint64_t)((long long)agent * A.e + j), myfault, myfault_layer);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(OZ_TMEM_COLS));
+  }
+  if constexpr (C > 1) cluster_sync_all();
+}
+
+static int al(int x, int a) { return (x + a - 1) / a * a; }
+
+// S = 6 byte slices (the accuracy default); EVORL_OZ_SLICES=5 selects 5 (for
+// measurements: ~1e-9 instead of ~1e-13 relative policy error)
+static int oz_slices() {
+  const char* v = getenv("EVORL_OZ_SLICES");
+  return (v && v[0] == '5') ? 5 : 6;
+}
+
+bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
+  if (net.nlayers != 3 || obs_dim > 4 || e < 5) return false;  // 16-lane teams, obs -> W1 -> W2 -> O
+  const int W1 = net.dims[1], W2 = net.dims[2], O = net.dims[3];
+  if (net.dims[0] > 4 || O > OZ_MAXO) return false;
+  const int S = oz_slices();
+  const int W1p = (W1 + 31) / 32 * 32;
+  if (S * (W1p / 4) + OZ_N * S > OZ_TMEM_COLS) return false;  // A slices + accumulator in TMEM
+  int C = 1;
+  while (C * OZ_M < W2) C *= 2;
+  if (C > 8) return false;
+  OzPlan p{};
+  p.C = C;
+  p.S = S;
+  p.W1 = W1;
+  p.W1p = W1p;
+  p.W2 = W2;
+  int off = 0;
+  p.off_B = off;
+  off = al(off + OZ_N * (2 * S - 1) * W1p, 1024);
+  p.off_W0 = off;
+  off = al(off + 4 * W1p * 8, 16);
+  p.off_b0 = off;
+  off = al(off + W1p * 8, 16);
+  p.off_mk = off;
+  off = al(off + 5 * 8, 16);
+  p.off_x0 = off;
+  off = al(off + 4 * OZ_N * 8, 16);
+  p.off_sce = off;
+  off = al(off + OZ_N * 8, 16);
+  p.off_red = off;
+  off = al(off + 4 * O * OZ_N * 8, 16);
+  p.off_pout = off;
+  off = al(off + 2 * C * (O + 1) * OZ_N * 8, 16);
+  p.off_mask = off;
+  off = al(off + MAXL * 4, 16);
+  p.off_bar = off;
+  off = al(off + 8 * 3, 16);  // mbar, xbar[2]
+  p.off_tslot = off;
+  off = al(off + 16, 16);
+  p.off_rmax = off;
+  off = al(off + 2 * OZ_M * 8, 16);
+  p.off_h0s = off;
+  off = al(off + W1p * OZ_N * 8, 16);
+  p.used = off;
+  p.bytes = std::max(off, OZ_MIN_SMEM);
+  if (p.bytes > 227 * 1024) return false;
+  static_assert(sizeof(OzPlan) <= sizeof(TcPlanOut), "plan storage");
+  std::memcpy(out, &p, sizeof p);
+  return true;
+}
+
+template <int S, int C>
+static cudaError_t launch_oz_c(const RolloutArgs& a, const OzPlan& p, cudaStream_t stream) {
+  auto kern = rollout_oz_kernel<S, C>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(a.n_agents * a.groups * C));
+  cfg.blockDim = dim3(OZ_THREADS);
+  cfg.dynamicSmemBytes = (size_t)p.bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a, p);
+}
+
+template <int S>
+static cudaError_t launch_oz_s(const RolloutArgs& a, const OzPlan& p, cudaStream_t stream) {
+  switch (p.C) {
+    case 1: return launch_oz_c<S, 1>(a, p, stream);
+    case 2: return launch_oz_c<S, 2>(a, p, stream);
+    case 4: return launch_oz_c<S, 4>(a, p, stream);
+    case 8: return launch_oz_c<S, 8>(a, p, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_rollout_oz(const RolloutArgs& a, const TcPlanOut& po, cudaStream_t stream) {
+  if (a.n_agents <= 0) return cudaSuccess;
+  OzPlan p;
+  std::memcpy(&p, &po, sizeof p);
+  return p.S == 5 ? launch_oz_s<5>(a, p, stream) : launch_oz_s<6>(a, p, stream);
+}
+
+#ifdef EVB_TC_PROFILE
+extern "C" int evorl_debug_oz_profile(unsigned long long* out16) {
+  if (cudaMemcpyFromSymbol(out16, g_oz_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 6;
+  static const unsigned long long zero[16] = {};
+  return cudaMemcpyToSymbol(g_oz_prof, zero, sizeof zero) == cudaSuccess ? 0 : 6;
+}
+#endif
+
+}  // namespace evorl_b200

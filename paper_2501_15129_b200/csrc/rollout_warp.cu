@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(256) rollout_warp_kernel(const __grid_constant
 static int a16(int x) { return (x + 15) & ~15; }
 
 bool plan_rollout_warp(const NetDesc& net, int obs_dim, int e, int precision, WarpPlanOut* out) {
-  const int ts = precision == 0 ? 8 : 4;
+  const int ts = (precision == 0 || precision == 3) ? 8 : 4;
   const int L = net.nlayers;
   if (e > 2 || net.dims[L] > 8 || obs_dim > 4) return false;
   WarpPlan p{};
@@ -267,7 +267,7 @@ cudaError_t launch_rollout_warp(const RolloutArgs& a, const WarpPlanOut& po, int
   if (lanes <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)((lanes + p.wpb - 1) / p.wpb);
   const size_t smem = (size_t)p.wpb * p.slot_bytes;
-  if (precision == 0) {
+  if (precision == 0 || precision == 3) {  // EVORL_PREC_OZ: small policies run the fp64 warp team
     static bool set = false;
     if (!set) {
       cudaFuncSetAttribute(rollout_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -2,7 +2,7 @@
 parity path at full BASELINE config-3 size (OpenES pop 4096 x 16 envs, 2x256,
 Pendulum H=200): same state, one generation each, several generations.
 
-  python tools/tc_rank_agreement.py [gens]
+  python tools/tc_rank_agreement.py [gens] [precision ...]   (default: f32 tc oz)
 """
 import os
 import sys
@@ -15,10 +15,11 @@ import paper_2501_15129_b200 as evb  # noqa: E402
 
 def main():
     gens = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    precs = sys.argv[2:] or ["f32", "tc", "oz"]
     kw = dict(algo="openes", env="pendulum", fixed_horizon=True, pop=4096, fitness_episodes=16,
               hidden=(256, 256), max_episode_steps=200)
     ref = evb.EsWorkflow(evb.EsConfig(precision="f64", **kw)).init((1, 2))
-    for prec in ("f32", "tc"):
+    for prec in precs:
         g = evb.EsWorkflow(evb.EsConfig(precision=prec, **kw)).init((1, 2))
         r = evb.EsWorkflow(evb.EsConfig(precision="f64", **kw)).init((1, 2))
         for gen in range(gens):
