@@ -102,8 +102,18 @@ EVB_DEV void env_reset(const EnvDesc& e, DKey key, LaneEnv& s) {
 // sin_th (optional): sin of the current angle, already computed by observe()
 // for this state -- the reference evaluates std::sin(th) twice with the same
 // argument (proj/src/env.cpp:94 and :48), so reusing it is exact.
+// pendulum_reward_pre: the action-independent part of the Pendulum reward,
+// w*w + (0.1*thdot)*thdot with w = wrap_angle(th) (proj/src/env.cpp:139-141),
+// so a caller can evaluate it off the action's critical path; env_step then
+// adds (0.001*u)*u in the reference's order (bit-identical).
+EVB_DEV double pendulum_reward_pre(const LaneEnv& s) {
+  const double w = wrap_angle(s.p0);
+  return dadd(dmul(w, w), dmul(dmul(0.1, s.p1), s.p1));
+}
+
 EVB_DEV uint32_t env_step(const EnvDesc& e, LaneEnv& s, double action, double& reward,
-                          bool& terminated, bool& truncated, const double* sin_th = nullptr) {
+                          bool& terminated, bool& truncated, const double* sin_th = nullptr,
+                          const double* reward_pre = nullptr) {
   const bool cart = e.id == ENV_CARTPOLE;
   if (!isfinite(s.p0) || !isfinite(s.p1) || (cart && (!isfinite(s.p2) || !isfinite(s.p3))))
     return FAULT_ENV_STATE;
@@ -133,9 +143,9 @@ EVB_DEV uint32_t env_step(const EnvDesc& e, LaneEnv& s, double action, double& r
   } else {
     const double u = clampd(action, -2.0, 2.0);
     const double th = s.p0, thdot = s.p1;
-    const double w = wrap_angle(th);
     // -((w*w + (0.1*thdot)*thdot) + (0.001*u)*u)
-    reward = -dadd(dadd(dmul(w, w), dmul(dmul(0.1, thdot), thdot)), dmul(dmul(0.001, u), u));
+    const double pre = reward_pre ? *reward_pre : pendulum_reward_pre(s);
+    reward = -dadd(pre, dmul(dmul(0.001, u), u));
     // pendulum_physics (proj/src/env.cpp:46-51), 1.5*kPenG = 15 exactly
     const double sn = sin_th ? *sin_th : sin(th);
     double td = dadd(thdot, dmul(dadd(dmul(15.0, sn), dmul(3.0, u)), 0.05));

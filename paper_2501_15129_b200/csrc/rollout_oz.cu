@@ -68,8 +68,7 @@ struct OzPlan {
   int S;       // byte slices per operand
   int W1, W2;  // hidden widths
   int W1p;     // W1 rounded up to the MMA K step (32)
-  int off_B, off_W0, off_b0, off_mk, off_x0, off_sce, off_red, off_pout, off_mask, off_bar, off_tslot, off_h0s,
-      off_rmax;
+  int off_B, off_W0, off_b0, off_mk, off_x0, off_sce, off_red, off_pout, off_mask, off_bar, off_tslot, off_rmax;
   int used;   // bytes of the layout (zeroed by the prologue)
   int bytes;  // dynamic SMEM requested: >= OZ_MIN_SMEM
 };
@@ -115,6 +114,24 @@ EVB_DEV int bound_exp(double v) {
   if (v > 0.0) frexp(v, &e);
   return max(-960, min(960, e));
 }
+// exact int64 -> double for |x| < 2^51 without the (slow) conversion pipe:
+// the integer lands in the mantissa of 1.5 * 2^52 + x
+EVB_DEV double i51_to_double(long long x) {
+  return __longlong_as_double(x + 0x4338000000000000LL) - 6755399441055744.0;
+}
+// byte b (0..3) of each of a0..a3 packed into one word (a0's in the low byte)
+EVB_DEV uint32_t gather_byte(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, int b) {
+  const uint32_t sel = (uint32_t)b | ((uint32_t)(b + 4) << 4);
+  return __byte_perm(__byte_perm(a0, a1, sel), __byte_perm(a2, a3, sel), 0x5410);
+}
+// the frexp exponent of a finite v >= 0 from its bit field (v < 2^e; zero and
+// subnormals give -1022), clamped like bound_exp
+EVB_DEV int bound_exp_bits(double v) {
+  const int e = ((__double2hiint(v) >> 20) & 0x7FF) - 1022;
+  return max(-960, min(960, e));
+}
+// 2^g for |g| <= 1000 (a normal double), built from the exponent field
+EVB_DEV double pow2(int g) { return __hiloint2double((g + 1023) << 20, 0); }
 // atomic max of a non-negative double (bit patterns order like the values)
 EVB_DEV void smem_max_nonneg(double* p, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
@@ -141,7 +158,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
   const uint32_t colA = (uint32_t)(OZ_TMEM_COLS - S * (W1p / 4));
 
 #ifdef EVB_TC_PROFILE
-  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
 #endif
   for (int i = tid; i < P.used / 4; i += OZ_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
@@ -261,10 +278,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
   NormParams nrm;
   nrm.active = 0;
   if (A.norm != nullptr) nrm = *A.norm;
+  double inv_den[4];
+  for (int i = 0; i < 4; ++i) inv_den[i] = nrm.active ? 1.0 / nrm.den[i] : 1.0;
   double* x0 = reinterpret_cast<double*>(smem + P.off_x0);    // [4][16]
   double* sce = reinterpret_cast<double*>(smem + P.off_sce);  // [16] 2^-G_e
   double* red = reinterpret_cast<double*>(smem + P.off_red);  // [4 quadrants][O][16]
-  double* h0s = reinterpret_cast<double*>(smem + P.off_h0s);  // [W1p][16] fp64 layer-1 input (slow_cta only)
   double* pout_base = reinterpret_cast<double*>(smem + P.off_pout);
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem + P.off_mask);
   const int OE = O * OZ_N, OE1 = (O + 1) * OZ_N;
@@ -291,9 +309,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
         }
       }
     }
+    // (o - mean) * (1 / den): within an ulp of the fp64 team's IEEE division,
+    // far below this team's ~1e-13 policy tolerance, and off the divide latency
     for (int i = 0; i < E.obs_dim; ++i) {
       double v = raw[i];
-      if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
+      if (nrm.active) v = dmul(dsub(v, nrm.mean[i]), inv_den[i]);
       x0[i * OZ_N + tid] = act ? v : 0.0;
     }
   };
@@ -313,56 +333,79 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
     if (C > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[it & 1], (uint32_t)(C * OE1 * sizeof(double)));
 
     // ---- layer 0 (fp64): h = relu(W0 x + b0) for lane le, rows 16 rg .. 16 rg + 15,
-    // then h_int = trunc(h 2^G) (G from the lane bound sum_k max|W0[.][k]| |x_k| + max|b0|)
-    // and its S bytes -> the B data blocks (one 16-byte store per slice)
+    // then h_int = rn(h 2^G) (G from the lane bound sum_k max|W0[.][k]| |x_k| + max|b0|)
+    // and its S bytes -> the B data blocks (one 16-byte store per slice).  The
+    // block is issue-bound (one CTA = 2 warps per scheduler): K runs to 4
+    // unconditionally (W0 and x0 are zero past obs_dim), ReLU is fmax, the
+    // exponents are bit fields, the fixed point comes out of the mantissa.
     {
       uint32_t bad = 0u;
       if (l0_active) {
         double xr[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) xr[k] = k < K0 ? x0[k * OZ_N + le] : 0.0;
+        for (int k = 0; k < 4; ++k) xr[k] = x0[k * OZ_N + le];
         double bnd = mk[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k < K0) bnd = fma(mk[k], fabs(xr[k]), bnd);
+        for (int k = 0; k < 4; ++k) bnd = fma(mk[k], fabs(xr[k]), bnd);
         bnd = bnd * (1.0 + 0x1.0p-40);  // covers the rounding of the fma chains below
-        const int G = 8 * S - 1 - bound_exp(bnd);
-        const double hscale = ldexp(1.0, G);
-        if (rg == 0) sce[le] = ldexp(1.0, -G);
-        unsigned long long hq[16];
+        const int G = 8 * S - 1 - bound_exp_bits(bnd);
+        const double hscale = pow2(G);
+        if (rg == 0) sce[le] = pow2(-G);
+        // 16 independent fma chains (k outer): one CTA per SM leaves 2 warps
+        // per scheduler, so the latency is hidden by ILP, not by other warps
+        double z[16];
+        const double* __restrict__ w0r = W0 + rg * 16;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int r = rg * 16 + u;
-          double z = 0.0;
+        for (int k = 0; k < 4; ++k) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k < K0) z = fma(W0[k * W1p + r], xr[k], z);
-          z = z + b0[r];
-          const double h = z > 0.0 ? z : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
-          if (h == INFINITY) bad = 1u << le;
-          if (slow_cta) h0s[r * OZ_N + le] = h;
-          hq[u] = h < INFINITY ? __double2ull_rz(h * hscale) : 0ull;
+          for (int u = 0; u < 16; u += 2) {
+            const double2 w = *reinterpret_cast<const double2*>(w0r + k * W1p + u);
+            z[u] = k == 0 ? w.x * xr[0] : fma(w.x, xr[k], z[u]);
+            z[u + 1] = k == 0 ? w.y * xr[0] : fma(w.y, xr[k], z[u + 1]);
+          }
         }
+        // h_int read straight from the mantissa of h 2^G + 2^52 (no float->int
+        // conversion): low word + bits 32..51; an infinite h shows up as an
+        // exponent field other than 0x433 in the high word
+        uint32_t qlo[16], qhi[16], hor = 0u;
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+          const double2 b = *reinterpret_cast<const double2*>(b0 + rg * 16 + u);
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const double h = fmax(z[u + v] + (v ? b.y : b.x), 0.0);  // ReLU (NaN -> 0, as cwiseMax)
+            const double t = fma(h, hscale, 0x1p52);
+            qlo[u + v] = (uint32_t)__double2loint(t);
+            qhi[u + v] = (uint32_t)__double2hiint(t);
+            hor |= qhi[u + v];
+          }
+        }
+        if ((hor & 0x7FF00000u) != 0x43300000u) bad = 1u << le;  // h = +inf
 #pragma unroll
         for (int jj = 0; jj < S; ++jj) {
+          const int P = 8 * (S - 1 - jj);  // bit position of slice jj
+          const bool H = P >= 32;
           uint32_t wv[4];
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            uint32_t word = 0u;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) word |= (uint32_t)((hq[4 * w + b] >> (8 * (S - 1 - jj))) & 0xFFull) << (8 * b);
-            wv[w] = word;
-          }
+          for (int w = 0; w < 4; ++w)
+            wv[w] = gather_byte(H ? qhi[4 * w] : qlo[4 * w], H ? qhi[4 * w + 1] : qlo[4 * w + 1],
+                                H ? qhi[4 * w + 2] : qlo[4 * w + 2], H ? qhi[4 * w + 3] : qlo[4 * w + 3],
+                                (P & 31) >> 3);
           *reinterpret_cast<uint4*>(Bme + (size_t)(S - 1 + jj) * 256) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
+      OZ_MARK(11);  // layer 0 math + B stores
       bad = __reduce_or_sync(0xffffffffu, bad);
       if (lane == 0 && bad) atomicOr(&mask[0], bad);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B visible to the tensor core
     }
     __syncthreads();
     OZ_MARK(2);  // layer 0 + slicing
-    if (warp == 0) {  // layer 1 on tcgen05: S MMAs per k-step into one accumulator
+    // the env threads (warp 0) evaluate the action-independent part of the
+    // reward while the MMAs run (off the action -> observation critical path)
+    double rpre = 0.0;
+    if (active && E.id == ENV_PENDULUM) rpre = pendulum_reward_pre(s);
+    if (warp == OZ_THREADS / 32 - 1) {  // layer 1 on tcgen05: S MMAs per k-step into one accumulator
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t bS = smem_u32(Bs);
       for (int ks = 0; ks < W1p / 32; ++ks) {
@@ -387,20 +430,55 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       double h[8];
       uint32_t bad = 0u;
+      double sq[8];
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(sce + half * 8 + q);
+        sq[q] = rscale * v.x;  // exact power-of-two scale 2^(8(S-1) - F_r - G_e)
+        sq[q + 1] = rscale * v.y;
+      }
+      // sum_t D_t 2^(8(S-1-t)) = 2^24 hi + lo with hi, lo exact 44-bit integers
+      // (|D_t| < 2^27), converted through the mantissa: no conversion-pipe ops
+      long long hi[8], lo[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int e = half * 8 + q;
-        double acc = (double)(int)d[0][q];
+        hi[q] = 0;
+        lo[q] = 0;
+      }
 #pragma unroll
-        for (int t = 1; t < S; ++t) acc = fma(acc, 256.0, (double)(int)d[t][q]);
-        double z = (acc * rscale) * sce[e];
-        if (rbad) {  // non-finite weight in this row: fp64 dot product (IEEE propagation)
-          z = 0.0;
-          for (int k = 0; k < W1; ++k) z = fma(w1(k), h0s[k * OZ_N + e], z);
+      for (int t = 0; t < S; ++t)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const long long v = (long long)(int)d[t][q];
+          if (t < S - 3) {
+            hi[q] = hi[q] * 256 + v;
+          } else {
+            lo[q] = lo[q] * 256 + v;
+          }
         }
-        z = z + b1r;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double acc = fma(i51_to_double(hi[q]), 16777216.0, i51_to_double(lo[q]));
+        h[q] = acc * sq[q];
+      }
+      if (rbad) {  // non-finite weight in this row: fp64 dot product (IEEE propagation),
+                   // with the layer-0 activations recomputed exactly as above
+        for (int q = 0; q < 8; ++q) {
+          const int e = half * 8 + q;
+          double z = 0.0;
+          for (int k = 0; k < W1; ++k) {
+            double a = W0[k] * x0[e];
+            for (int kk = 1; kk < 4; ++kk) a = fma(W0[kk * W1p + k], x0[kk * OZ_N + e], a);
+            z = fma(w1(k), fmax(a + b0[k], 0.0), z);
+          }
+          h[q] = z;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double z = h[q] + b1r;
         h[q] = z > 0.0 ? z : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
-        if (h[q] == INFINITY) bad |= 1u << e;
+        if (h[q] == INFINITY) bad |= 1u << (half * 8 + q);
       }
       bad = __reduce_or_sync(0xffffffffu, bad);
       if (lane == 0 && bad) atomicOr(&mask[1], bad);
@@ -496,7 +574,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
         }
         double reward = 0.0;
         bool term = false, trunc = false;
-        const uint32_t f = env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr);
+        OZ_MARK(9);  // head (output sum + tanh)
+        const uint32_t f = env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr,
+                                    E.id == ENV_PENDULUM ? &rpre : nullptr);
+        OZ_MARK(10);  // env_step
         if (f) {
           myfault = f;
         } else {
@@ -524,6 +605,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
 #ifdef EVB_TC_PROFILE
   if (tid == 0) {
     for (int i = 0; i < 7; ++i) atomicAdd(&g_oz_prof[i], prof[i]);
+    atomicAdd(&g_oz_prof[9], prof[9]);
+    atomicAdd(&g_oz_prof[10], prof[10]);
+    atomicAdd(&g_oz_prof[11], prof[11]);
     atomicAdd(&g_oz_prof[8], 1ull);
   }
 #endif
@@ -600,8 +684,6 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   off = al(off + 16, 16);
   p.off_rmax = off;
   off = al(off + 2 * OZ_M * 8, 16);
-  p.off_h0s = off;
-  off = al(off + W1p * OZ_N * 8, 16);
   p.used = off;
   p.bytes = std::max(off, OZ_MIN_SMEM);
   if (p.bytes > 227 * 1024) return false;
