@@ -416,6 +416,8 @@ static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** 
     s->cand_cap = (int)std::max(1.0, std::min((double)n, std::floor(kCandCap / ((double)d * tsz))));
     if (f64) {
       A(dalloc(&s->d_cand, (size_t)s->cand_cap * d));
+      if (s->plan.oz)
+        A(dalloc(&s->d_tc_blocks, (size_t)s->cand_cap * s->plan.tcp.data[0] * oz_block_bytes(s->plan.tcp)));
     } else {
       A(dalloc(&s->d_cand_f32, (size_t)s->cand_cap * d));
       if (s->plan.tc)
@@ -842,6 +844,12 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
         CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream));
         ac.par.src = SRC_EXPLICIT;
         ac.par.params = s->d_cand;
+        if (s->d_tc_blocks) {  // the oz team's layer-1 weights, pre-split into fixed-point byte slices
+          CK(run_oz_split(s->d_cand, s->net, s->plan.tcp, c1 - c0, s->d_tc_blocks, s->stream));
+          count_launch();
+          ac.tc_blocks = s->d_tc_blocks;
+          ac.tc_block_bytes = oz_block_bytes(s->plan.tcp);
+        }
       }
       count_launch();
       if (c0 == s->a0) CK(cudaEventRecord(s->ev_r0, s->stream));

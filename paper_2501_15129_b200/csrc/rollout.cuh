@@ -199,5 +199,10 @@ cudaError_t launch_rollout_tc(const RolloutArgs& a, const TcPlanOut& plan, cudaS
 // fixed-point int8 tcgen05 MMAs, everything else fp64.
 bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out);
 cudaError_t launch_rollout_oz(const RolloutArgs& a, const TcPlanOut& plan, cudaStream_t stream);
+// bytes of one (agent, CTA) pre-split layer-1 block of an oz plan
+long long oz_block_bytes(const TcPlanOut& plan);
+// the fp64 candidates [n_agents x d] -> pre-split blocks [n_agents][C]
+cudaError_t run_oz_split(const double* cand, const NetDesc& net, const TcPlanOut& plan, int n_agents,
+                         unsigned char* blocks, cudaStream_t stream);
 
 }  // namespace evorl_b200

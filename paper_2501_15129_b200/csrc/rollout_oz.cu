@@ -69,6 +69,7 @@ struct OzPlan {
   int W1, W2;  // hidden widths
   int W1p;     // W1 rounded up to the MMA K step (32)
   int off_B, off_W0, off_b0, off_mk, off_x0, off_sce, off_red, off_pout, off_mask, off_bar, off_tslot, off_rmax;
+  int pipe;   // 1: the pipelined two-group kernel (rollout_ozp_kernel)
   int used;   // bytes of the layout (zeroed by the prologue)
   int bytes;  // dynamic SMEM requested: >= OZ_MIN_SMEM
 };
@@ -100,10 +101,21 @@ EVB_DEV void oz_ld8(uint32_t taddr, uint32_t* r) {
                  "=r"(r[7])
                : "r"(taddr));
 }
+EVB_DEV void oz_ld4(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+EVB_DEV void named_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 EVB_DEV void oz_st8(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
+}
+// one out-of-line copy of the parameter source (prologue / slow path only):
+// keeps the kernels' code small and the compile fast
+__device__ __noinline__ double oz_param(const ParamDesc& P, long long d, int agent_local, int agent, long long p) {
+  return param_value(P, d, agent_local, agent, p);
 }
 // fmax over finite values only (NaN / inf weights are handled by the fp64 row path)
 EVB_DEV double fin_abs(double v) { return isfinite(v) ? fabs(v) : 0.0; }
@@ -190,12 +202,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
   // ---- prologue: layer 0 (fp64, replicated) and its per-column maxima
   for (int i = tid; i < K0 * W1; i += OZ_THREADS) {
     const int k = i / W1, r = i % W1;
-    const double w = param_value(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W1 + r);
+    const double w = oz_param(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W1 + r);
     W0[k * W1p + r] = w;
     smem_max_nonneg(&mk[k], fin_abs(w));  // (SMEM atomics: once per rollout)
   }
   for (int r = tid; r < W1; r += OZ_THREADS) {
-    const double b = param_value(A.par, N.d, agent_local, agent, N.b_off[0] + r);
+    const double b = oz_param(A.par, N.d, agent_local, agent, N.b_off[0] + r);
     b0[r] = b;
     smem_max_nonneg(&mk[4], fin_abs(b));
   }
@@ -203,7 +215,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
   // Warp halves take alternate 32-wide k chunks (one tcgen05.st.x8 per slice).
   const bool row_ok = r0 + row < W2;  // zero rows past W2
   auto w1 = [&](int k) -> double {
-    return (row_ok && k < W1) ? param_value(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + row)
+    return (row_ok && k < W1) ? oz_param(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + row)
                               : 0.0;
   };
   double rm = 0.0;
@@ -247,13 +259,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
   if (slow_cta)
     for (int k = 0; k < W1; ++k) rbad = rbad || !isfinite(w1(k));
   const double rscale = ldexp(1.0, 8 * (S - 1) - Fr);
-  const double b1r = row_ok ? param_value(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row) : 0.0;
+  const double b1r = row_ok ? oz_param(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row) : 0.0;
   double w2r[OZ_MAXO], b2[OZ_MAXO];
 #pragma unroll
   for (int o = 0; o < OZ_MAXO; ++o) {
-    w2r[o] = (o < O && row_ok) ? param_value(A.par, N.d, agent_local, agent, N.w_off[2] + (long long)(r0 + row) * O + o)
+    w2r[o] = (o < O && row_ok) ? oz_param(A.par, N.d, agent_local, agent, N.w_off[2] + (long long)(r0 + row) * O + o)
                                : 0.0;
-    b2[o] = o < O ? param_value(A.par, N.d, agent_local, agent, N.b_off[2] + o) : 0.0;
+    b2[o] = o < O ? oz_param(A.par, N.d, agent_local, agent, N.b_off[2] + o) : 0.0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -634,13 +646,689 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_
   if constexpr (C > 1) cluster_sync_all();
 }
 
+
+// ---------------------------------------------------------------------------
+// Pipelined team (the default oz kernel): the 16 lanes are two groups of 8 whose
+// step chains -- layer 0 -> MMA -> epilogue -> cluster exchange -> env -- run
+// half a period apart, so one group's MMAs (tensor core) and env step (2 env
+// warps, latency-bound fp64 transcendentals) overlap the other group's layer 0
+// and epilogue (8 compute warps).  Warps: 0-7 compute, 8-9 env (group 0 / 1),
+// 10 MMA issue.  Per group g: B_g (zero-padded windows of 8-lane blocks, N = 8 S),
+// accumulator D_g at TMEM columns 8 S g.. (A slices shared).  Handshakes are
+// mbarriers: x0full[g] (env -> compute), bfull[g] (compute -> MMA, 8 warp
+// arrivals), dfull[g] (tcgen05.commit -> compute), xbar[g][parity] (st.async
+// partial outputs -> env).  NetFault bookkeeping uses step stamps (no resets).
+constexpr int OZP_CW = 8;                         // compute warps
+constexpr int OZP_THREADS = 32 * (OZP_CW + 3);    // + 2 env warps + 1 MMA warp
+constexpr int OZP_G = 8;                          // lanes per group
+
+template <int S, int C>
+__global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __grid_constant__ RolloutArgs A,
+                                                                     const __grid_constant__ OzPlan P) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const NetDesc& N = A.net;
+  const EnvDesc& E = A.env;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool compute = warp < OZP_CW;
+  const int quad = warp & 3, half = (warp >> 2) & 1;  // compute warps: TMEM lane quadrant, lane half
+  const int crank = C > 1 ? (int)cluster_ctarank() : 0;
+  const int team = blockIdx.x / C;
+  const int agent_local = team / A.groups;
+  const int group = team % A.groups;
+  const int agent = A.agent_offset + agent_local;
+  const int W1 = P.W1, W1p = P.W1p, W2 = P.W2, O = N.dims[3];
+  const int r0 = crank * OZ_M;
+  const int row = quad * 32 + lane;
+  constexpr int RB = OZP_G * (2 * S - 1);         // rows (N) of one zero-padded B buffer
+  const uint32_t LBO = (uint32_t)(RB / 8) * 128;  // K-direction core-matrix stride
+  const int BBYTES = RB * W1p;                    // one group's B buffer
+  const uint32_t colA = (uint32_t)(OZ_TMEM_COLS - S * (W1p / 4));
+  constexpr int NG = OZP_G * S;                   // MMA N per group
+
+#ifdef EVB_TC_PROFILE
+  unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+#endif
+  for (int i = tid; i < P.used / 4; i += OZP_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.off_bar);
+  uint64_t* x0full = bars;      // [2]
+  uint64_t* bfull = bars + 2;   // [2]
+  uint64_t* dfull = bars + 4;   // [2]
+  uint64_t* xbar = bars + 6;    // [2 groups][2 parities]
+  __syncthreads();
+  if (warp == OZP_CW + 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(OZ_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&x0full[g], 1);
+      mbar_init(&bfull[g], OZP_CW);
+      mbar_init(&dfull[g], 1);
+      mbar_init(&xbar[2 * g], 1);
+      mbar_init(&xbar[2 * g + 1], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  double* W0 = reinterpret_cast<double*>(smem + P.off_W0);
+  double* b0 = reinterpret_cast<double*>(smem + P.off_b0);
+  double* mk = reinterpret_cast<double*>(smem + P.off_mk);
+  double* rmax = reinterpret_cast<double*>(smem + P.off_rmax);
+  // ---- prologue (compute warps): layer 0 to SMEM, layer-1 slices to TMEM
+  const bool row_ok = compute && r0 + row < W2;
+  auto w1 = [&](int k) -> double {
+    return (row_ok && k < W1) ? oz_param(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + row)
+                              : 0.0;
+  };
+  const int K0 = N.dims[0];
+  if (compute) {
+    for (int i = tid; i < K0 * W1; i += 32 * OZP_CW) {
+      const int k = i / W1, r = i % W1;
+      const double w = oz_param(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W1 + r);
+      W0[k * W1p + r] = w;
+      smem_max_nonneg(&mk[k], fin_abs(w));
+    }
+    for (int r = tid; r < W1; r += 32 * OZP_CW) {
+      const double b = oz_param(A.par, N.d, agent_local, agent, N.b_off[0] + r);
+      b0[r] = b;
+      smem_max_nonneg(&mk[4], fin_abs(b));
+    }
+  }
+  // pre-split blocks (materialised ask): the row's exponent and slices are
+  // ready-made -- coalesced 16-byte loads, then tcgen05.st
+  const unsigned char* blk =
+      A.tc_blocks != nullptr ? A.tc_blocks + ((long long)agent_local * C + crank) * A.tc_block_bytes : nullptr;
+  double rm = 0.0;
+  bool rfin = true;
+  int meta = 0;
+  if (compute && blk != nullptr) {
+    meta = reinterpret_cast<const int*>(blk + (size_t)S * W1p * OZ_M)[row];
+    rfin = (meta >> 16) == 0;
+  } else if (compute) {
+    for (int c = half; c < W1p / 32; c += 2)
+      for (int q = 0; q < 32; ++q) {
+        const double w = w1(c * 32 + q);
+        rm = fmax(rm, fin_abs(w));
+        rfin = rfin && isfinite(w);
+      }
+    rmax[half * OZ_M + row] = rm;
+  }
+  const bool slow_cta = __syncthreads_or(!rfin) != 0;
+  int Fr = 0;
+  bool rbad = false;
+  double rscale = 0.0, b1r = 0.0;
+  double w2r[OZ_MAXO], b2[OZ_MAXO];
+#pragma unroll
+  for (int o = 0; o < OZ_MAXO; ++o) {
+    w2r[o] = 0.0;
+    b2[o] = (!compute && o < O) ? oz_param(A.par, N.d, agent_local, agent, N.b_off[2] + o) : 0.0;
+  }
+  if (compute && blk != nullptr) {
+    Fr = (int)(short)(meta & 0xFFFF);
+    for (int c = half; c < W1p / 32; c += 2)
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        const uint4* src = reinterpret_cast<const uint4*>(blk + (((size_t)i * (W1p / 32) + c) * OZ_M + row) * 32);
+        const uint4 a = __ldg(src), b = __ldg(src + 1);
+        const uint32_t packed[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        oz_st8(tmem + ((uint32_t)(quad * 32) << 16) + colA + (uint32_t)(i * (W1p / 4) + c * 8), packed);
+      }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    rbad = !rfin;
+  } else if (compute) {
+    rm = fmax(rmax[row], rmax[OZ_M + row]);
+    Fr = 8 * S - 1 - bound_exp(rm);  // |W_int| < 2^(8S-1)
+    const double wscale = ldexp(1.0, Fr);
+    for (int c = half; c < W1p / 32; c += 2) {
+      long long wi[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const double w = w1(c * 32 + q);
+        wi[q] = isfinite(w) ? __double2ll_rz(w * wscale) : 0ll;
+      }
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        uint32_t packed[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint32_t word = 0u;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) word |= (uint32_t)((wi[4 * u + b] >> (8 * (S - 1 - i))) & 0xFF) << (8 * b);
+          packed[u] = word;
+        }
+        oz_st8(tmem + ((uint32_t)(quad * 32) << 16) + colA + (uint32_t)(i * (W1p / 4) + c * 8), packed);
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    if (slow_cta)
+      for (int k = 0; k < W1; ++k) rbad = rbad || !isfinite(w1(k));
+  }
+  if (compute) {
+    rscale = ldexp(1.0, 8 * (S - 1) - Fr);
+    b1r = row_ok ? oz_param(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row) : 0.0;
+#pragma unroll
+    for (int o = 0; o < OZ_MAXO; ++o)
+      w2r[o] = (o < O && row_ok)
+                   ? oz_param(A.par, N.d, agent_local, agent, N.w_off[2] + (long long)(r0 + row) * O + o)
+                   : 0.0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if constexpr (C > 1) cluster_sync_all();
+
+  double* x0 = reinterpret_cast<double*>(smem + P.off_x0);     // [2][4][8]
+  double* red = reinterpret_cast<double*>(smem + P.off_red);   // [2][4 quadrants][O][8]
+  double* pout = reinterpret_cast<double*>(smem + P.off_pout); // [2 groups][2 parities][C][(O+1) 8]
+  uint32_t* flags = reinterpret_cast<uint32_t*>(smem + P.off_mask);
+  uint32_t* bad0 = flags;       // [2][8] step stamps: lane's layer-0 activation infinite at step t (= t + 1)
+  uint32_t* bad1 = flags + 16;  // [2][8] the same for layer 1
+  uint32_t* alive = flags + 32; // [2] group has an active lane at this step
+  uint32_t* gdone = flags + 34; // [2] group finished (compute -> MMA warp)
+  const int OEg = O * OZP_G, OE1g = (O + 1) * OZP_G;
+  OZ_MARK(0);  // prologue
+
+  if (warp == OZP_CW || warp == OZP_CW + 1) {
+    // ================================================= env warp of group lg
+    const int lg = warp - OZP_CW;
+    const int l = lane;
+    const int j = group * OZ_N + lg * OZP_G + l;  // lane index within the agent
+    const bool valid = l < OZP_G && j < A.e;
+    const int per = A.count / A.e, rem = A.count % A.e;
+    const int eps_this = valid ? per + (j < rem ? 1 : 0) : 0;
+    const int slot0 = valid ? j * per + min(j, rem) : 0;
+    LaneEnv s{};
+    double ep_ret = 0.0, wc = 0.0, wmean[4] = {0, 0, 0, 0}, wm2[4] = {0, 0, 0, 0};
+    int ep_len = 0, eps_done = 0;
+    long long steps = 0;
+    uint32_t myfault = 0, myfault_layer = 0;
+    if (valid) {
+      const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
+      env_reset(E, fold_in(lane_key, 0), s);  // proj/src/rollout.cpp:104
+    }
+    NormParams nrm;
+    nrm.active = 0;
+    if (A.norm != nullptr) nrm = *A.norm;
+    double inv_den[4];
+    for (int i = 0; i < 4; ++i) inv_den[i] = nrm.active ? 1.0 / nrm.den[i] : 1.0;
+    double* xg = x0 + lg * 4 * OZP_G;
+    double sin_th = 0.0;
+    auto observe_into_x0 = [&](bool act) {  // proj/src/rollout.cpp:124-126
+      double raw[4];
+      observe(E, s, raw);
+      sin_th = raw[1];
+      if (act && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
+        if (wc == 0.0) {
+          for (int i = 0; i < E.obs_dim; ++i) {
+            wmean[i] = raw[i];
+            wm2[i] = 0.0;
+          }
+          wc = 1.0;
+        } else {
+          wc = dadd(wc, 1.0);
+          for (int i = 0; i < E.obs_dim; ++i) {
+            const double delta = dsub(raw[i], wmean[i]);
+            wmean[i] = dadd(wmean[i], ddiv(delta, wc));
+            wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
+          }
+        }
+      }
+      for (int i = 0; i < E.obs_dim; ++i) {  // (o - mean) * (1 / den), as the plain oz team
+        double v = raw[i];
+        if (nrm.active) v = dmul(dsub(v, nrm.mean[i]), inv_den[i]);
+        if (l < OZP_G) xg[i * OZP_G + l] = act ? v : 0.0;
+      }
+    };
+    bool act = valid && eps_this > 0 && A.max_iters > 0;
+    if (act) observe_into_x0(true);
+    for (int it = 0;; ++it) {
+      const bool any = __any_sync(0xffffffffu, act);
+      __syncwarp();  // every lane's x0 stores before lane 0's (release) arrival
+      if (lane == 0) {
+        alive[lg] = any ? 1u : 0u;
+        mbar_arrive_local(&x0full[lg]);  // x0 (and the alive flag) of step it
+      }
+      if (!any) break;
+      // the action-independent part of the reward, while this step's layers run
+      double rpre = 0.0;
+      if (act && E.id == ENV_PENDULUM) rpre = pendulum_reward_pre(s);
+      uint64_t* xb = &xbar[2 * lg + (it & 1)];
+      if (C > 1 && lane == 0) mbar_arrive_expect_tx(xb, (uint32_t)(C * OE1g * sizeof(double)));
+      OZ_MARK(7);  // env warp: own work (reward pre-term, arming)
+      if constexpr (C > 1) {
+        mbar_wait_parity(xb, (uint32_t)((it >> 1) & 1));
+      } else {
+        mbar_wait_parity_cta(xb, (uint32_t)((it >> 1) & 1));
+      }
+      OZ_MARK(6);  // env warp: waiting for the partial outputs
+      const double* pg = pout + (size_t)(lg * 2 + (it & 1)) * C * OE1g;
+      if (act) {
+        double z[OZ_MAXO];
+        bool nonfinite_out = false;
+        int bad_layer = 3;
+        for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pg[c * OE1g + OEg + l]);
+        for (int o = 0; o < O; ++o) {
+          double v = pg[o * OZP_G + l];
+          for (int c = 1; c < C; ++c) v += pg[c * OE1g + o * OZP_G + l];
+          v = v + b2[o];
+          z[o] = v;
+          if (!isfinite(v)) nonfinite_out = true;
+        }
+        if (bad_layer == 3 && nonfinite_out) bad_layer = 2;
+        if (bad_layer < 3) {  // NetFault: the lowest layer with a non-finite activation
+          myfault = FAULT_NET;
+          myfault_layer = (uint32_t)bad_layer;
+        } else {
+          double action;
+          if (N.head == HEAD_CATEGORICAL) {
+            int arg = 0;
+            for (int o = 1; o < O; ++o)
+              if (z[o] > z[arg]) arg = o;  // maxCoeff: first maximum
+            action = (double)arg;
+          } else if (N.head == HEAD_TANH) {
+            action = N.tanh_scale * tanh(z[0]);
+          } else {
+            action = z[0];
+          }
+          double reward = 0.0;
+          bool term = false, trunc = false;
+          const uint32_t f = env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr,
+                                      E.id == ENV_PENDULUM ? &rpre : nullptr);
+          if (f) {
+            myfault = f;
+          } else {
+            ep_ret = dadd(ep_ret, reward);  // proj/src/rollout.cpp:143
+            ep_len += 1;
+            steps += 1;
+            if (term || trunc) {
+              if (crank == 0) {
+                const long long sl = (long long)agent_local * A.count + slot0 + eps_done;
+                A.ep_returns[sl] = ep_ret;
+                if (A.ep_lengths) A.ep_lengths[sl] = ep_len;
+              }
+              ep_ret = 0.0;
+              ep_len = 0;
+              eps_done += 1;
+              if (eps_done < eps_this) env_reset(E, s.rng, s);  // auto-reset, env.cpp:163-167
+            }
+          }
+        }
+        const bool next = myfault == 0 && eps_done < eps_this && it + 1 < A.max_iters;
+        observe_into_x0(next);
+        act = next;
+      }
+      __syncwarp();
+      OZ_MARK(7);  // env warp: head + env + observe
+    }
+    if (valid && crank == 0) {
+      const long long ln = (long long)agent_local * A.e + j;
+      if (A.lane_steps) A.lane_steps[ln] = steps;
+      if (A.track_stats && A.lane_stats) {
+        double* st = A.lane_stats + ln * 9;
+        st[0] = wc;
+        for (int i = 0; i < 4; ++i) {
+          st[1 + i] = wmean[i];
+          st[5 + i] = wm2[i];
+        }
+      }
+      if (myfault) record_fault(A.fault, (uint64_t)((long long)agent * A.e + j), myfault, myfault_layer);
+    }
+  } else if (warp == OZP_CW + 2) {
+    // ================================================= MMA issue warp
+    bool live[2] = {true, true};
+    const uint32_t bS = smem_u32(smem + P.off_B);
+    for (int it = 0; live[0] || live[1]; ++it) {
+      for (int g = 0; g < 2; ++g) {
+        if (!live[g]) continue;
+        OZ_MARK(10);  // MMA warp: issue
+        mbar_wait_parity_cta(&bfull[g], (uint32_t)(it & 1));
+        OZ_MARK(9);  // MMA warp: waiting for B
+        if (gdone[g]) {
+          live[g] = false;
+          continue;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t bg = bS + (uint32_t)(g * BBYTES);
+        for (int ks = 0; ks < W1p / 32; ++ks) {
+#pragma unroll
+          for (int i = 0; i < S; ++i) {
+            const uint64_t bd = oz_desc(bg + (uint32_t)(S - 1 - i) * 128 + (uint32_t)ks * 2 * LBO, LBO, 128);
+            oz_mma_ts_elect(tmem + (uint32_t)(g * NG), tmem + colA + (uint32_t)(i * (W1p / 4) + ks * 8), bd,
+                            oz_idesc(OZ_M, NG, i == 0), (ks | i) ? 1u : 0u);
+          }
+        }
+        oz_commit_elect(&dfull[g]);
+      }
+    }
+  } else {
+    // ================================================= compute warps (0-7)
+    bool live[2] = {true, true};
+    // layer-0 thread map: lane le of the group, 8 consecutive k rows (half a
+    // 16-byte K row of a B core matrix)
+    const int le = tid & 7, rg = tid >> 3;  // rg: 32 row groups of 8
+    const bool l0_active = rg * 8 < W1p;
+    for (int it = 0; live[0] || live[1]; ++it) {
+      for (int g = 0; g < 2; ++g) {
+        if (!live[g]) continue;
+        OZ_MARK(5);  // compute: publish (+ named barrier) / group switch
+        mbar_wait_parity_cta(&x0full[g], (uint32_t)(it & 1));
+        OZ_MARK(1);  // compute: waiting for x0
+        if (!alive[g]) {
+          live[g] = false;
+          if (tid == 0) gdone[g] = 1u;
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(&bfull[g]);
+          continue;
+        }
+        // ---- layer 0 of group g (fp64) -> fixed point -> S bytes -> B_g
+        {
+          const double* xg = x0 + g * 4 * OZP_G;
+          if (l0_active) {
+            double xr[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) xr[k] = xg[k * OZP_G + le];
+            double bnd = mk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bnd = fma(mk[k], fabs(xr[k]), bnd);
+            bnd = bnd * (1.0 + 0x1.0p-40);
+            const int G = 8 * S - 1 - bound_exp_bits(bnd);
+            const double hscale = pow2(G);
+            double z[8];
+            const double* __restrict__ w0r = W0 + rg * 8;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+#pragma unroll
+              for (int u = 0; u < 8; u += 2) {
+                const double2 w = *reinterpret_cast<const double2*>(w0r + k * W1p + u);
+                z[u] = k == 0 ? w.x * xr[0] : fma(w.x, xr[k], z[u]);
+                z[u + 1] = k == 0 ? w.y * xr[0] : fma(w.y, xr[k], z[u + 1]);
+              }
+            }
+            uint32_t qlo[8], qhi[8], hor = 0u;
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              const double2 b = *reinterpret_cast<const double2*>(b0 + rg * 8 + u);
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const double h = fmax(z[u + v] + (v ? b.y : b.x), 0.0);  // ReLU (NaN -> 0, as cwiseMax)
+                const double t = fma(h, hscale, 0x1p52);
+                qlo[u + v] = (uint32_t)__double2loint(t);
+                qhi[u + v] = (uint32_t)__double2hiint(t);
+                hor |= qhi[u + v];
+              }
+            }
+            if ((hor & 0x7FF00000u) != 0x43300000u) bad0[g * OZP_G + le] = (uint32_t)it + 1u;  // h = +inf
+            unsigned char* Bme = smem + P.off_B + g * BBYTES + (size_t)(rg >> 1) * LBO + le * 16 + (rg & 1) * 8;
+#pragma unroll
+            for (int jj = 0; jj < S; ++jj) {
+              const int Pb = 8 * (S - 1 - jj);
+              const bool H = Pb >= 32;
+              uint32_t wv[2];
+#pragma unroll
+              for (int w = 0; w < 2; ++w)
+                wv[w] = gather_byte(H ? qhi[4 * w] : qlo[4 * w], H ? qhi[4 * w + 1] : qlo[4 * w + 1],
+                                    H ? qhi[4 * w + 2] : qlo[4 * w + 2], H ? qhi[4 * w + 3] : qlo[4 * w + 3],
+                                    (Pb & 31) >> 3);
+              *reinterpret_cast<uint2*>(Bme + (size_t)(S - 1 + jj) * 128) = make_uint2(wv[0], wv[1]);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B_g visible to the tensor core
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(&bfull[g]);
+        }
+        // ---- epilogue of group g: row `row`, lanes 4 half .. 4 half + 3
+        OZ_MARK(2);  // compute: layer 0
+        mbar_wait_parity_cta(&dfull[g], (uint32_t)(it & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        OZ_MARK(3);  // compute: waiting for the MMAs
+        {
+          uint32_t d[S][4];
+          const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(g * NG + half * 4);
+#pragma unroll
+          for (int t = 0; t < S; ++t) oz_ld4(tl + (uint32_t)(t * OZP_G), d[t]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          // each lane's scale 2^-G, recomputed from x0 exactly as layer 0 did
+          // (no cross-thread handoff between the layer-0 and epilogue threads)
+          double h[4], sq[4];
+          {
+            const double* xg = x0 + g * 4 * OZP_G;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int e = half * 4 + q;
+              double bnd = mk[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) bnd = fma(mk[k], fabs(xg[k * OZP_G + e]), bnd);
+              bnd = bnd * (1.0 + 0x1.0p-40);
+              sq[q] = rscale * pow2(-(8 * S - 1 - bound_exp_bits(bnd)));
+            }
+          }
+          long long hi[4], lo[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) hi[q] = lo[q] = 0;
+#pragma unroll
+          for (int t = 0; t < S; ++t)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const long long v = (long long)(int)d[t][q];
+              if (t < S - 3) {
+                hi[q] = hi[q] * 256 + v;
+              } else {
+                lo[q] = lo[q] * 256 + v;
+              }
+            }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) h[q] = fma(i51_to_double(hi[q]), 16777216.0, i51_to_double(lo[q])) * sq[q];
+          if (rbad) {  // non-finite weight in this row: fp64 dot product, layer 0 recomputed
+            const double* xg = x0 + g * 4 * OZP_G;
+            for (int q = 0; q < 4; ++q) {
+              const int e = half * 4 + q;
+              double z = 0.0;
+              for (int k = 0; k < W1; ++k) {
+                double a = W0[k] * xg[e];
+                for (int kk = 1; kk < 4; ++kk) a = fma(W0[kk * W1p + k], xg[kk * OZP_G + e], a);
+                z = fma(w1(k), fmax(a + b0[k], 0.0), z);
+              }
+              h[q] = z;
+            }
+          }
+          uint32_t bad = 0u;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double zz = h[q] + b1r;
+            h[q] = zz > 0.0 ? zz : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
+            if (h[q] == INFINITY) bad |= 1u << (half * 4 + q);
+          }
+          bad = __reduce_or_sync(0xffffffffu, bad);
+          if (lane < OZP_G && ((bad >> lane) & 1u)) bad1[g * OZP_G + lane] = (uint32_t)it + 1u;
+          // output layer: v[q] = w2[row][o] h[q] summed over the warp's 32 rows by a
+          // reduce-scatter (lane bits 4, 3 select the lane q it ends on)
+          const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
+#pragma unroll
+          for (int o = 0; o < OZ_MAXO; ++o) {
+            if (o >= O) break;
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = w2r[o] * h[q];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const double send = b4 ? v[i] : v[i + 2];
+              const double keep = b4 ? v[i + 2] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+            {
+              const double send = b3 ? v[0] : v[1];
+              const double keep = b3 ? v[1] : v[0];
+              v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 4);
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+            if ((lane & 7) == 0) red[((g * 4 + quad) * O + o) * OZP_G + half * 4 + b4 * 2 + b3] = v[0];
+          }
+        }
+        OZ_MARK(4);  // compute: epilogue
+        named_sync_n(1, 32 * OZP_CW);  // red / stamps of group g complete
+        // partial outputs (fixed quadrant order) + each lane's first non-finite
+        // layer -> every CTA of the cluster
+        if (tid < OE1g) {
+          const int oe = tid;
+          const double* rg4 = red + g * 4 * OEg;
+          double v;
+          if (oe < OEg) {
+            v = ((rg4[oe] + rg4[OEg + oe]) + rg4[2 * OEg + oe]) + rg4[3 * OEg + oe];
+          } else {
+            const int e = oe - OEg;
+            int bl = 3;
+            if (bad1[g * OZP_G + e] == (uint32_t)it + 1u) bl = 1;
+            if (bad0[g * OZP_G + e] == (uint32_t)it + 1u) bl = 0;
+            v = (double)bl;
+          }
+          double* pg = pout + (size_t)(g * 2 + (it & 1)) * C * OE1g;
+          if constexpr (C > 1) {
+            const uint32_t la = smem_u32(pg + crank * OE1g + oe), lb = smem_u32(&xbar[2 * g + (it & 1)]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) st_async(map_cluster(la, (uint32_t)c), v, map_cluster(lb, (uint32_t)c));
+          } else {
+            pg[oe] = v;
+          }
+        }
+        if constexpr (C == 1) {
+          named_sync_n(1, 32 * OZP_CW);
+          if (tid == 0) mbar_arrive_local(&xbar[2 * g + (it & 1)]);
+        }
+      }
+    }
+  }
+#ifdef EVB_TC_PROFILE
+  if (tid == 0) {
+    for (int i = 0; i < 6; ++i) atomicAdd(&g_oz_prof[i], prof[i]);
+    atomicAdd(&g_oz_prof[8], 1ull);
+  }
+  if (tid == 32 * OZP_CW) {
+    atomicAdd(&g_oz_prof[6], prof[6]);
+    atomicAdd(&g_oz_prof[7], prof[7]);
+  }
+  if (tid == 32 * (OZP_CW + 2)) {
+    atomicAdd(&g_oz_prof[9], prof[9]);
+    atomicAdd(&g_oz_prof[10], prof[10]);
+  }
+#endif
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == OZP_CW + 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(OZ_TMEM_COLS));
+  }
+  if constexpr (C > 1) cluster_sync_all();
+}
+
+
+// ---------------------------------------------------------------------------
+// Pre-split layer-1 weights (materialised ask): one parallel pass over every
+// (agent, CTA, row) computes the row's fixed-point exponent and its S byte
+// slices in the layout the team's prologue stores to TMEM, so the prologue is
+// a coalesced 16-byte-load + tcgen05.st loop instead of 2 x 256 parameter
+// fetches and int64 slicing per row.  Block of one (agent, CTA):
+//   [S][W1p/32][128 rows][8 words] slice bytes (word u = k 4u..4u+3 of the
+//   32-wide chunk, low byte first), then [128] int32 meta = (F_r & 0xFFFF) |
+//   (row holds a non-finite weight) << 16.
+long long oz_block_bytes(const TcPlanOut& po) {
+  OzPlan p;
+  std::memcpy(&p, &po, sizeof p);
+  return (long long)p.S * p.W1p * OZ_M + OZ_M * 4;
+}
+
+template <int S>
+__global__ void k_oz_split(const double* __restrict__ cand, long long d, long long w_off1, int W1, int W2, int W1p,
+                           int C, long long total, unsigned char* __restrict__ blocks, long long block_bytes) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int row = (int)(idx % OZ_M);
+  const long long ac = idx / OZ_M;  // agent * C + crank
+  const int crank = (int)(ac % C);
+  const long long agent = ac / C;
+  const int r = crank * OZ_M + row;
+  const double* wr = cand + agent * d + w_off1 + r;  // weight (r, k) at wr[k * W2]
+  const bool ok = r < W2;
+  double rm = 0.0;
+  bool fin = true;
+  for (int k = 0; k < W1 && ok; ++k) {
+    const double w = wr[(long long)k * W2];
+    rm = fmax(rm, fin_abs(w));
+    fin = fin && isfinite(w);
+  }
+  const int Fr = 8 * S - 1 - bound_exp(rm);
+  const double wscale = ldexp(1.0, Fr);
+  unsigned char* blk = blocks + ac * block_bytes;
+  for (int c = 0; c < W1p / 32; ++c) {
+    long long wi[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int k = c * 32 + q;
+      const double w = (ok && k < W1) ? wr[(long long)k * W2] : 0.0;
+      wi[q] = isfinite(w) ? __double2ll_rz(w * wscale) : 0ll;
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      uint32_t packed[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint32_t word = 0u;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) word |= (uint32_t)((wi[4 * u + b] >> (8 * (S - 1 - i))) & 0xFF) << (8 * b);
+        packed[u] = word;
+      }
+      uint4* dst = reinterpret_cast<uint4*>(blk + (((size_t)i * (W1p / 32) + c) * OZ_M + row) * 32);
+      dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    }
+  }
+  reinterpret_cast<int*>(blk + (size_t)S * W1p * OZ_M)[row] = (Fr & 0xFFFF) | ((ok && !fin) ? (1 << 16) : 0);
+}
+
+cudaError_t run_oz_split(const double* cand, const NetDesc& net, const TcPlanOut& po, int n_agents,
+                         unsigned char* blocks, cudaStream_t stream) {
+  OzPlan p;
+  std::memcpy(&p, &po, sizeof p);
+  const long long total = (long long)n_agents * p.C * OZ_M;
+  if (total <= 0) return cudaSuccess;
+  const long long bb = oz_block_bytes(po);
+  const unsigned grid = (unsigned)((total + 127) / 128);
+#ifdef EVB_OZ_S5
+  if (p.S == 5) {
+    k_oz_split<5><<<grid, 128, 0, stream>>>(cand, net.d, net.w_off[1], p.W1, p.W2, p.W1p, p.C, total, blocks, bb);
+    return cudaGetLastError();
+  }
+#endif
+  k_oz_split<6><<<grid, 128, 0, stream>>>(cand, net.d, net.w_off[1], p.W1, p.W2, p.W1p, p.C, total, blocks, bb);
+  return cudaGetLastError();
+}
+
 static int al(int x, int a) { return (x + a - 1) / a * a; }
 
-// S = 6 byte slices (the accuracy default); EVORL_OZ_SLICES=5 selects 5 (for
-// measurements: ~1e-9 instead of ~1e-13 relative policy error)
+// S = 6 byte slices; a build with -DEVB_OZ_S5 also has S = 5 instances,
+// selected by EVORL_OZ_SLICES=5 (measurements: ~1e-9 instead of ~1e-13 relative
+// policy error, 40 instead of 48 MMAs per step)
 static int oz_slices() {
+#ifdef EVB_OZ_S5
   const char* v = getenv("EVORL_OZ_SLICES");
-  return (v && v[0] == '5') ? 5 : 6;
+  if (v && v[0] == '5') return 5;
+#endif
+  return 6;
+}
+
+// the pipelined two-group kernel is the default; EVORL_OZ_PIPE=0 selects the
+// single-chain kernel (kept for comparison and as a second implementation)
+static int oz_pipe() {
+  const char* v = getenv("EVORL_OZ_PIPE");
+  return (v && v[0] == '0') ? 0 : 1;
 }
 
 bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
@@ -659,7 +1347,38 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.W1 = W1;
   p.W1p = W1p;
   p.W2 = W2;
+  p.pipe = oz_pipe();
   int off = 0;
+  if (p.pipe) {  // rollout_ozp_kernel layout: per-group B buffers, x0, red, pout
+    p.off_B = off;
+    off = al(off + 2 * OZP_G * (2 * S - 1) * W1p, 1024);
+    p.off_W0 = off;
+    off = al(off + 4 * W1p * 8, 16);
+    p.off_b0 = off;
+    off = al(off + W1p * 8, 16);
+    p.off_mk = off;
+    off = al(off + 5 * 8, 16);
+    p.off_x0 = off;
+    off = al(off + 2 * 4 * OZP_G * 8, 16);
+    p.off_sce = off;
+    p.off_red = off;
+    off = al(off + 2 * 4 * O * OZP_G * 8, 16);
+    p.off_pout = off;
+    off = al(off + 2 * 2 * C * (O + 1) * OZP_G * 8, 16);
+    p.off_mask = off;
+    off = al(off + 36 * 4, 16);  // stamps bad0[2][8], bad1[2][8], alive[2], gdone[2]
+    p.off_bar = off;
+    off = al(off + 8 * 10, 16);  // x0full[2], bfull[2], dfull[2], xbar[2][2]
+    p.off_tslot = off;
+    off = al(off + 16, 16);
+    p.off_rmax = off;
+    off = al(off + 2 * OZ_M * 8, 16);
+    p.used = off;
+    p.bytes = std::max(off, OZ_MIN_SMEM);
+    if (p.bytes > 227 * 1024) return false;
+    std::memcpy(out, &p, sizeof p);
+    return true;
+  }
   p.off_B = off;
   off = al(off + OZ_N * (2 * S - 1) * W1p, 1024);
   p.off_W0 = off;
@@ -694,16 +1413,16 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
 
 template <int S, int C>
 static cudaError_t launch_oz_c(const RolloutArgs& a, const OzPlan& p, cudaStream_t stream) {
-  auto kern = rollout_oz_kernel<S, C>;
-  static bool set = false;
-  if (!set) {
+  auto kern = p.pipe ? rollout_ozp_kernel<S, C> : rollout_oz_kernel<S, C>;
+  static bool set[2] = {false, false};
+  if (!set[p.pipe]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    set = true;
+    set[p.pipe] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(a.n_agents * a.groups * C));
-  cfg.blockDim = dim3(OZ_THREADS);
+  cfg.blockDim = dim3(p.pipe ? OZP_THREADS : OZ_THREADS);
   cfg.dynamicSmemBytes = (size_t)p.bytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -731,7 +1450,10 @@ cudaError_t launch_rollout_oz(const RolloutArgs& a, const TcPlanOut& po, cudaStr
   if (a.n_agents <= 0) return cudaSuccess;
   OzPlan p;
   std::memcpy(&p, &po, sizeof p);
-  return p.S == 5 ? launch_oz_s<5>(a, p, stream) : launch_oz_s<6>(a, p, stream);
+#ifdef EVB_OZ_S5
+  if (p.S == 5) return launch_oz_s<5>(a, p, stream);
+#endif
+  return p.S == 6 ? launch_oz_s<6>(a, p, stream) : cudaErrorInvalidValue;
 }
 
 #ifdef EVB_TC_PROFILE
