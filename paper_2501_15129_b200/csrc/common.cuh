@@ -169,25 +169,39 @@ EVB_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
 EVB_DEV void mbar_arrive_local(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Wait (acquire, CTA scope) for the phase with the given parity.
-EVB_DEV void mbar_wait_parity_cta(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
+// Wait (acquire, CTA / cluster scope) for the phase with the given parity.
+// The spin loop is C++ around a single try_wait: a branch hidden inside an asm
+// block is invisible to the compiler, which then assumes the warp reconverged
+// after it -- lanes leaving the spin at different times stay diverged into the
+// following warp-synchronous code (a block-wide BAR.RED reached by half a warp
+// was an illegal instruction on B200).
+EVB_DEV bool mbar_try_wait_parity_cta(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n\tWAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAITC_%=;\n\t}" ::"r"(a),
-      "r"(parity)
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
 }
-// Wait (acquire, cluster scope) for the phase with the given parity.
-EVB_DEV void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
+EVB_DEV bool mbar_try_wait_parity_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+EVB_DEV void mbar_wait_parity_cta(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_parity_cta(bar, parity)) {
+  }
+}
+EVB_DEV void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_parity_cluster(bar, parity)) {
+  }
 }
 
 // ------------------------------------------------------------------- errors

@@ -488,7 +488,11 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
   for (int it = 0;; ++it) {
     if (tid < MAXL) mask[(it & 1) * MAXL + tid] = 0u;  // last used two steps ago
     const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
-    if (!__syncthreads_or(active)) break;  // also orders the x0 writes before layer 0
+    // warp-level vote first: __any_sync waits for all 32 lanes, so the warp
+    // reaches the block-wide reduction barrier converged (the env lanes run
+    // extra code; a partially arrived warp at BAR.RED is an illegal instruction)
+    const bool wact = __any_sync(0xffffffffu, active);
+    if (!__syncthreads_or(wact)) break;  // also orders the x0 writes before layer 0
     RK_MARK(0);  // loop-top barrier
     uint32_t* cur_mask = mask + (it & 1) * MAXL;
     if (C > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[it & 1], (uint32_t)(C * OE1 * sizeof(T)));

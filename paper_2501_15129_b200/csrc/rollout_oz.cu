@@ -18,21 +18,21 @@
 //     S = 6 keeps ~47 bits of every operand: the policy output differs from
 //     fp64 arithmetic by ~1e-13 relative (fitness differences at the level of
 //     the fp64 path's own libm/ordering differences from the reference CPU).
-//   * One accumulator for all t: the B operand lives in SMEM as S data blocks
-//     behind S-1 zero blocks of 16 lanes, [0 .. 0 | B_0 .. B_(S-1)], and MMA i
-//     (A_i from TMEM) reads the window that starts at block S-1-i, so column
-//     block c of D receives A_i B_(c-i) (zero for c < i): D[:, 16t..16t+15] = D_t.
-//     Per k-step of 32: S TS MMAs of M = 128, N = 16 S, K = 32 (S = 6: 48 MMAs
-//     of ~50 cycles per env step, measured by tools/umma_i8_bench.cu at the
-//     int8 peak rate).
+//   * One accumulator per lane group for all t: the B operand lives in SMEM as
+//     S data blocks behind S-1 zero blocks of 8 lanes, [0 .. 0 | B_0 .. B_(S-1)],
+//     and MMA i (A_i from TMEM) reads the window that starts at block S-1-i, so
+//     column block c of D receives A_i B_(c-i) (zero for c < i): D[:, 8t..8t+7]
+//     = D_t.  Per k-step of 32: S TS MMAs of M = 128, N = 8 S, K = 32
+//     (tools/umma_i8_bench.cu checks the scheme and times it).
 //   * TMEM (512 columns, one team CTA per SM): A slices at columns 512 - S W1p/4
-//     (written once by tcgen05.st), D at columns 0 .. 16 S.
-//   * Per env step (one CTA = 128 weight rows; C = W2/128 CTAs per agent):
-//     layer 0 (fp64, replicated) -> per-lane bound, fixed point, bytes -> B
-//     (STS.128 per slice) | MMAs (one elected thread) | epilogue: tcgen05.ld of
-//     D_0..D_(S-1), fp64 combine, bias, ReLU, output-layer partial (warp
-//     reduce-scatter) | st.async partial outputs to every CTA of the cluster |
-//     16 env threads: head, fp64 env step, observe.
+//     (written once by tcgen05.st from pre-split blocks), D_g at columns 8 S g.
+//   * Per env step (one CTA = 128 weight rows; C = W2/128 CTAs per agent) the
+//     16 lanes are two groups of 8 whose chains -- layer 0 (fp64, replicated)
+//     -> per-lane bound, fixed point, bytes -> B_g | MMAs (MMA warp) | epilogue:
+//     tcgen05.ld of D_0..D_(S-1), exact integer combine, fp64 scale, bias, ReLU,
+//     output-layer partial (warp reduce-scatter) | st.async partial outputs to
+//     every CTA of the cluster | env warp: head, fp64 env step, observe -- run
+//     half a period apart (rollout_ozp_kernel below).
 //   * Rows holding a non-finite weight (a diverged mean) are computed by an
 //     fp64 dot product instead (IEEE propagation and NetFault as the fp64 team).
 #include <algorithm>
@@ -42,7 +42,6 @@
 
 namespace evorl_b200 {
 
-constexpr int OZ_THREADS = 256;
 constexpr int OZ_M = 128;  // weight rows per CTA (UMMA M)
 constexpr int OZ_N = 16;   // lanes per team
 constexpr int OZ_MAXO = 8;
@@ -69,7 +68,7 @@ struct OzPlan {
   int W1, W2;  // hidden widths
   int W1p;     // W1 rounded up to the MMA K step (32)
   int off_B, off_W0, off_b0, off_mk, off_x0, off_sce, off_red, off_pout, off_mask, off_bar, off_tslot, off_rmax;
-  int pipe;   // 1: the pipelined two-group kernel (rollout_ozp_kernel)
+  int pipe;   // layout version (1: the two-group pipelined kernel)
   int used;   // bytes of the layout (zeroed by the prologue)
   int bytes;  // dynamic SMEM requested: >= OZ_MIN_SMEM
 };
@@ -112,10 +111,12 @@ EVB_DEV void oz_st8(uint32_t taddr, const uint32_t* r) {
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
-// one out-of-line copy of the parameter source (prologue / slow path only):
-// keeps the kernels' code small and the compile fast
-__device__ __noinline__ double oz_param(const ParamDesc& P, long long d, int agent_local, int agent, long long p) {
-  return param_value(P, d, agent_local, agent, p);
+// The oz teams always read materialised candidates (SRC_EXPLICIT: the
+// workflow's fp64 ask, evaluate's centre, batched_rollout's params; checked by
+// launch_rollout_oz), so a parameter is one load -- no inlined noise
+// regeneration in the prologue (kernel size, compile time).
+EVB_DEV double oz_param(const ParamDesc& P, long long d, int agent_local, long long p) {
+  return P.params[(long long)agent_local * d + p];
 }
 // fmax over finite values only (NaN / inf weights are handled by the fp64 row path)
 EVB_DEV double fin_abs(double v) { return isfinite(v) ? fabs(v) : 0.0; }
@@ -148,504 +149,6 @@ EVB_DEV double pow2(int g) { return __hiloint2double((g + 1023) << 20, 0); }
 EVB_DEV void smem_max_nonneg(double* p, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
 }
-
-template <int S, int C>
-__global__ void __launch_bounds__(OZ_THREADS, 1) rollout_oz_kernel(const __grid_constant__ RolloutArgs A,
-                                                                   const __grid_constant__ OzPlan P) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  const NetDesc& N = A.net;
-  const EnvDesc& E = A.env;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant, lane half (epilogue)
-  const int crank = C > 1 ? (int)cluster_ctarank() : 0;
-  const int team = blockIdx.x / C;
-  const int agent_local = team / A.groups;
-  const int group = team % A.groups;
-  const int agent = A.agent_offset + agent_local;
-  const int W1 = P.W1, W1p = P.W1p, W2 = P.W2, O = N.dims[3], K0 = N.dims[0];
-  const int r0 = crank * OZ_M;  // this CTA's rows of layer 1
-  const int row = quad * 32 + lane;
-  constexpr int RB = OZ_N * (2 * S - 1);         // rows (N) of the zero-padded B buffer
-  const uint32_t LBO = (uint32_t)(RB / 8) * 128;  // K-direction core-matrix stride
-  const uint32_t colA = (uint32_t)(OZ_TMEM_COLS - S * (W1p / 4));
-
-#ifdef EVB_TC_PROFILE
-  unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  long long tprev = clock64();
-#endif
-  for (int i = tid; i < P.used / 4; i += OZ_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.off_tslot);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
-  uint64_t* xbar = mbar + 1;  // [2]: partial outputs of every cluster CTA landed (by step parity)
-  __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "n"(OZ_TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    mbar_init(mbar, 1);
-    mbar_init(&xbar[0], 1);
-    mbar_init(&xbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tslot;
-
-  double* W0 = reinterpret_cast<double*>(smem + P.off_W0);  // [k][W1p], zero past W1
-  double* b0 = reinterpret_cast<double*>(smem + P.off_b0);  // W1p
-  double* mk = reinterpret_cast<double*>(smem + P.off_mk);  // [0..3] max_r |W0[r][k]|, [4] max_r |b0[r]|
-  double* rmax = reinterpret_cast<double*>(smem + P.off_rmax);  // [2][128] row max |W1| per k half
-  unsigned char* Bs = smem + P.off_B;
-  // ---- prologue: layer 0 (fp64, replicated) and its per-column maxima
-  for (int i = tid; i < K0 * W1; i += OZ_THREADS) {
-    const int k = i / W1, r = i % W1;
-    const double w = oz_param(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W1 + r);
-    W0[k * W1p + r] = w;
-    smem_max_nonneg(&mk[k], fin_abs(w));  // (SMEM atomics: once per rollout)
-  }
-  for (int r = tid; r < W1; r += OZ_THREADS) {
-    const double b = oz_param(A.par, N.d, agent_local, agent, N.b_off[0] + r);
-    b0[r] = b;
-    smem_max_nonneg(&mk[4], fin_abs(b));
-  }
-  // ---- layer-1 weights of row `row`: per-row fixed point, S byte slices -> TMEM.
-  // Warp halves take alternate 32-wide k chunks (one tcgen05.st.x8 per slice).
-  const bool row_ok = r0 + row < W2;  // zero rows past W2
-  auto w1 = [&](int k) -> double {
-    return (row_ok && k < W1) ? oz_param(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + row)
-                              : 0.0;
-  };
-  double rm = 0.0;
-  bool rfin = true;
-  for (int c = half; c < W1p / 32; c += 2)
-    for (int q = 0; q < 32; ++q) {
-      const double w = w1(c * 32 + q);
-      rm = fmax(rm, fin_abs(w));
-      rfin = rfin && isfinite(w);
-    }
-  rmax[half * OZ_M + row] = rm;
-  // any non-finite weight in this CTA's slice: rows with one take the fp64 path
-  // (and the CTA keeps an fp64 copy of the layer-1 input for them)
-  const bool slow_cta = __syncthreads_or(!rfin) != 0;
-  rm = fmax(rmax[row], rmax[OZ_M + row]);
-  const int Fr = 8 * S - 1 - bound_exp(rm);  // |W_int| < 2^(8S-1)
-  const double wscale = ldexp(1.0, Fr);
-  for (int c = half; c < W1p / 32; c += 2) {
-    long long wi[32];
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const double w = w1(c * 32 + q);
-      wi[q] = isfinite(w) ? __double2ll_rz(w * wscale) : 0ll;
-    }
-#pragma unroll
-    for (int i = 0; i < S; ++i) {
-      uint32_t packed[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        uint32_t word = 0u;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) word |= (uint32_t)((wi[4 * u + b] >> (8 * (S - 1 - i))) & 0xFF) << (8 * b);
-        packed[u] = word;
-      }
-      oz_st8(tmem + ((uint32_t)(quad * 32) << 16) + colA + (uint32_t)(i * (W1p / 4) + c * 8), packed);
-    }
-  }
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  // per-thread epilogue constants: this row's scale 2^(8(S-1) - F_r), bias, output weights
-  bool rbad = false;  // this row holds a non-finite weight (fp64 path)
-  if (slow_cta)
-    for (int k = 0; k < W1; ++k) rbad = rbad || !isfinite(w1(k));
-  const double rscale = ldexp(1.0, 8 * (S - 1) - Fr);
-  const double b1r = row_ok ? oz_param(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row) : 0.0;
-  double w2r[OZ_MAXO], b2[OZ_MAXO];
-#pragma unroll
-  for (int o = 0; o < OZ_MAXO; ++o) {
-    w2r[o] = (o < O && row_ok) ? oz_param(A.par, N.d, agent_local, agent, N.w_off[2] + (long long)(r0 + row) * O + o)
-                               : 0.0;
-    b2[o] = o < O ? oz_param(A.par, N.d, agent_local, agent, N.b_off[2] + o) : 0.0;
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if constexpr (C > 1) cluster_sync_all();
-
-  // ---- lane state
-  const int j = group * OZ_N + tid;
-  const bool is_env = tid < OZ_N;
-  const bool valid = is_env && j < A.e;
-  const int per = A.count / A.e, rem = A.count % A.e;
-  const int eps_this = valid ? per + (j < rem ? 1 : 0) : 0;
-  const int slot0 = valid ? j * per + min(j, rem) : 0;
-  LaneEnv s{};
-  double ep_ret = 0.0, wc = 0.0, wmean[4] = {0, 0, 0, 0}, wm2[4] = {0, 0, 0, 0};
-  int ep_len = 0, eps_done = 0;
-  long long steps = 0;
-  uint32_t myfault = 0, myfault_layer = 0;
-  if (valid) {
-    const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
-    env_reset(E, fold_in(lane_key, 0), s);  // proj/src/rollout.cpp:104
-  }
-  NormParams nrm;
-  nrm.active = 0;
-  if (A.norm != nullptr) nrm = *A.norm;
-  double inv_den[4];
-  for (int i = 0; i < 4; ++i) inv_den[i] = nrm.active ? 1.0 / nrm.den[i] : 1.0;
-  double* x0 = reinterpret_cast<double*>(smem + P.off_x0);    // [4][16]
-  double* sce = reinterpret_cast<double*>(smem + P.off_sce);  // [16] 2^-G_e
-  double* red = reinterpret_cast<double*>(smem + P.off_red);  // [4 quadrants][O][16]
-  double* pout_base = reinterpret_cast<double*>(smem + P.off_pout);
-  uint32_t* mask = reinterpret_cast<uint32_t*>(smem + P.off_mask);
-  const int OE = O * OZ_N, OE1 = (O + 1) * OZ_N;
-  double sin_th = 0.0;
-  // observation -> (RunningStats) -> normalisation (the fp64 team's operations,
-  // proj/src/rollout.cpp:124-126, proj/src/obs_norm.cpp:7-18, :76-79)
-  auto observe_into_x0 = [&](bool act) {
-    double raw[4];
-    observe(E, s, raw);
-    sin_th = raw[1];
-    if (act && A.track_stats) {
-      if (wc == 0.0) {
-        for (int i = 0; i < E.obs_dim; ++i) {
-          wmean[i] = raw[i];
-          wm2[i] = 0.0;
-        }
-        wc = 1.0;
-      } else {
-        wc = dadd(wc, 1.0);
-        for (int i = 0; i < E.obs_dim; ++i) {
-          const double delta = dsub(raw[i], wmean[i]);
-          wmean[i] = dadd(wmean[i], ddiv(delta, wc));
-          wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
-        }
-      }
-    }
-    // (o - mean) * (1 / den): within an ulp of the fp64 team's IEEE division,
-    // far below this team's ~1e-13 policy tolerance, and off the divide latency
-    for (int i = 0; i < E.obs_dim; ++i) {
-      double v = raw[i];
-      if (nrm.active) v = dmul(dsub(v, nrm.mean[i]), inv_den[i]);
-      x0[i * OZ_N + tid] = act ? v : 0.0;
-    }
-  };
-  if (valid && eps_this > 0 && A.max_iters > 0) observe_into_x0(true);
-  // layer-0 thread map: lane e, 16 consecutive rows = one 16-byte K row of a B core matrix
-  const int le = tid & 15, rg = tid >> 4;
-  const bool l0_active = rg * 16 < W1p;
-  unsigned char* Bme = Bs + (size_t)rg * LBO + (size_t)(le >> 3) * 128 + (le & 7) * 16;
-
-  OZ_MARK(0);  // prologue
-  for (int it = 0;; ++it) {
-    if (tid < MAXL) mask[tid] = 0u;
-    const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
-    if (!__syncthreads_or(active)) break;
-    OZ_MARK(1);  // loop-top barrier
-    double* pout = pout_base + (it & 1) * C * OE1;
-    if (C > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[it & 1], (uint32_t)(C * OE1 * sizeof(double)));
-
-    // ---- layer 0 (fp64): h = relu(W0 x + b0) for lane le, rows 16 rg .. 16 rg + 15,
-    // then h_int = rn(h 2^G) (G from the lane bound sum_k max|W0[.][k]| |x_k| + max|b0|)
-    // and its S bytes -> the B data blocks (one 16-byte store per slice).  The
-    // block is issue-bound (one CTA = 2 warps per scheduler): K runs to 4
-    // unconditionally (W0 and x0 are zero past obs_dim), ReLU is fmax, the
-    // exponents are bit fields, the fixed point comes out of the mantissa.
-    {
-      uint32_t bad = 0u;
-      if (l0_active) {
-        double xr[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) xr[k] = x0[k * OZ_N + le];
-        double bnd = mk[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) bnd = fma(mk[k], fabs(xr[k]), bnd);
-        bnd = bnd * (1.0 + 0x1.0p-40);  // covers the rounding of the fma chains below
-        const int G = 8 * S - 1 - bound_exp_bits(bnd);
-        const double hscale = pow2(G);
-        if (rg == 0) sce[le] = pow2(-G);
-        // 16 independent fma chains (k outer): one CTA per SM leaves 2 warps
-        // per scheduler, so the latency is hidden by ILP, not by other warps
-        double z[16];
-        const double* __restrict__ w0r = W0 + rg * 16;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-#pragma unroll
-          for (int u = 0; u < 16; u += 2) {
-            const double2 w = *reinterpret_cast<const double2*>(w0r + k * W1p + u);
-            z[u] = k == 0 ? w.x * xr[0] : fma(w.x, xr[k], z[u]);
-            z[u + 1] = k == 0 ? w.y * xr[0] : fma(w.y, xr[k], z[u + 1]);
-          }
-        }
-        // h_int read straight from the mantissa of h 2^G + 2^52 (no float->int
-        // conversion): low word + bits 32..51; an infinite h shows up as an
-        // exponent field other than 0x433 in the high word
-        uint32_t qlo[16], qhi[16], hor = 0u;
-#pragma unroll
-        for (int u = 0; u < 16; u += 2) {
-          const double2 b = *reinterpret_cast<const double2*>(b0 + rg * 16 + u);
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const double h = fmax(z[u + v] + (v ? b.y : b.x), 0.0);  // ReLU (NaN -> 0, as cwiseMax)
-            const double t = fma(h, hscale, 0x1p52);
-            qlo[u + v] = (uint32_t)__double2loint(t);
-            qhi[u + v] = (uint32_t)__double2hiint(t);
-            hor |= qhi[u + v];
-          }
-        }
-        if ((hor & 0x7FF00000u) != 0x43300000u) bad = 1u << le;  // h = +inf
-#pragma unroll
-        for (int jj = 0; jj < S; ++jj) {
-          const int P = 8 * (S - 1 - jj);  // bit position of slice jj
-          const bool H = P >= 32;
-          uint32_t wv[4];
-#pragma unroll
-          for (int w = 0; w < 4; ++w)
-            wv[w] = gather_byte(H ? qhi[4 * w] : qlo[4 * w], H ? qhi[4 * w + 1] : qlo[4 * w + 1],
-                                H ? qhi[4 * w + 2] : qlo[4 * w + 2], H ? qhi[4 * w + 3] : qlo[4 * w + 3],
-                                (P & 31) >> 3);
-          *reinterpret_cast<uint4*>(Bme + (size_t)(S - 1 + jj) * 256) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-        }
-      }
-      OZ_MARK(11);  // layer 0 math + B stores
-      bad = __reduce_or_sync(0xffffffffu, bad);
-      if (lane == 0 && bad) atomicOr(&mask[0], bad);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B visible to the tensor core
-    }
-    __syncthreads();
-    OZ_MARK(2);  // layer 0 + slicing
-    // the env threads (warp 0) evaluate the action-independent part of the
-    // reward while the MMAs run (off the action -> observation critical path)
-    double rpre = 0.0;
-    if (active && E.id == ENV_PENDULUM) rpre = pendulum_reward_pre(s);
-    if (warp == OZ_THREADS / 32 - 1) {  // layer 1 on tcgen05: S MMAs per k-step into one accumulator
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t bS = smem_u32(Bs);
-      for (int ks = 0; ks < W1p / 32; ++ks) {
-#pragma unroll
-        for (int i = 0; i < S; ++i) {
-          const uint64_t bd = oz_desc(bS + (uint32_t)(S - 1 - i) * 256 + (uint32_t)ks * 2 * LBO, LBO, 128);
-          oz_mma_ts_elect(tmem, tmem + colA + (uint32_t)(i * (W1p / 4) + ks * 8), bd, oz_idesc(OZ_M, OZ_N * S, i == 0),
-                          (ks | i) ? 1u : 0u);
-        }
-      }
-      oz_commit_elect(mbar);
-    }
-    mbar_wait_parity_cta(mbar, (uint32_t)(it & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    OZ_MARK(3);  // MMA
-    // ---- epilogue: row `row`, lanes 8 half .. 8 half + 7; output layer fused
-    {
-      uint32_t d[S][8];
-      const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * 8);
-#pragma unroll
-      for (int t = 0; t < S; ++t) oz_ld8(tl + (uint32_t)(t * OZ_N), d[t]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      double h[8];
-      uint32_t bad = 0u;
-      double sq[8];
-#pragma unroll
-      for (int q = 0; q < 8; q += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(sce + half * 8 + q);
-        sq[q] = rscale * v.x;  // exact power-of-two scale 2^(8(S-1) - F_r - G_e)
-        sq[q + 1] = rscale * v.y;
-      }
-      // sum_t D_t 2^(8(S-1-t)) = 2^24 hi + lo with hi, lo exact 44-bit integers
-      // (|D_t| < 2^27), converted through the mantissa: no conversion-pipe ops
-      long long hi[8], lo[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        hi[q] = 0;
-        lo[q] = 0;
-      }
-#pragma unroll
-      for (int t = 0; t < S; ++t)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const long long v = (long long)(int)d[t][q];
-          if (t < S - 3) {
-            hi[q] = hi[q] * 256 + v;
-          } else {
-            lo[q] = lo[q] * 256 + v;
-          }
-        }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double acc = fma(i51_to_double(hi[q]), 16777216.0, i51_to_double(lo[q]));
-        h[q] = acc * sq[q];
-      }
-      if (rbad) {  // non-finite weight in this row: fp64 dot product (IEEE propagation),
-                   // with the layer-0 activations recomputed exactly as above
-        for (int q = 0; q < 8; ++q) {
-          const int e = half * 8 + q;
-          double z = 0.0;
-          for (int k = 0; k < W1; ++k) {
-            double a = W0[k] * x0[e];
-            for (int kk = 1; kk < 4; ++kk) a = fma(W0[kk * W1p + k], x0[kk * OZ_N + e], a);
-            z = fma(w1(k), fmax(a + b0[k], 0.0), z);
-          }
-          h[q] = z;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double z = h[q] + b1r;
-        h[q] = z > 0.0 ? z : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
-        if (h[q] == INFINITY) bad |= 1u << (half * 8 + q);
-      }
-      bad = __reduce_or_sync(0xffffffffu, bad);
-      if (lane == 0 && bad) atomicOr(&mask[1], bad);
-      // per output o: v[q] = w2[row][o] h[q], summed over the warp's 32 rows by
-      // a reduce-scatter (lane bits 4, 3, 2 select the lane q it ends on)
-      const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, bb2 = (lane >> 2) & 1;
-#pragma unroll
-      for (int o = 0; o < OZ_MAXO; ++o) {
-        if (o >= O) break;
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = w2r[o] * h[q];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double send = b4 ? v[i] : v[i + 4];
-          const double keep = b4 ? v[i + 4] : v[i];
-          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const double send = b3 ? v[i] : v[i + 2];
-          const double keep = b3 ? v[i + 2] : v[i];
-          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-        {
-          const double send = bb2 ? v[0] : v[1];
-          const double keep = bb2 ? v[1] : v[0];
-          v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-        }
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-        if ((lane & 3) == 0) red[(quad * O + o) * OZ_N + half * 8 + b4 * 4 + b3 * 2 + bb2] = v[0];
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    OZ_MARK(4);  // epilogue
-    // this CTA's partial outputs (fixed quadrant order) + each lane's first
-    // non-finite layer -> every CTA of the cluster
-    for (int oe = tid; oe < OE1; oe += OZ_THREADS) {
-      double v;
-      if (oe < OE) {
-        v = ((red[oe] + red[OE + oe]) + red[2 * OE + oe]) + red[3 * OE + oe];
-      } else {
-        const int e = oe - OE;
-        int bl = 3;
-        for (int l = 1; l >= 0; --l)
-          if ((mask[l] >> e) & 1u) bl = l;
-        v = (double)bl;
-      }
-      if constexpr (C > 1) {
-        const uint32_t la = smem_u32(pout + crank * OE1 + oe), lb = smem_u32(&xbar[it & 1]);
-#pragma unroll
-        for (int c = 0; c < C; ++c) st_async(map_cluster(la, (uint32_t)c), v, map_cluster(lb, (uint32_t)c));
-      } else {
-        pout[oe] = v;
-      }
-    }
-    if constexpr (C > 1) {
-      if (tid < OZ_N) mbar_wait_parity(&xbar[it & 1], (uint32_t)((it >> 1) & 1));
-    } else {
-      __syncthreads();
-    }
-    OZ_MARK(5);  // cluster exchange
-    // ---- head + env step (proj/src/rollout.cpp:57-90, :131-153), next observation
-    if (active) {
-      double z[OZ_MAXO];
-      bool nonfinite_out = false;
-      int bad_layer = 3;
-      for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pout[c * OE1 + OE + tid]);
-      for (int o = 0; o < O; ++o) {
-        double v = pout[o * OZ_N + tid];
-        for (int c = 1; c < C; ++c) v += pout[c * OE1 + o * OZ_N + tid];
-        v = v + b2[o];
-        z[o] = v;
-        if (!isfinite(v)) nonfinite_out = true;
-      }
-      if (bad_layer == 3 && nonfinite_out) bad_layer = 2;
-      if (bad_layer < 3) {  // NetFault: the lowest layer with a non-finite activation
-        myfault = FAULT_NET;
-        myfault_layer = (uint32_t)bad_layer;
-      } else {
-        double action;
-        if (N.head == HEAD_CATEGORICAL) {
-          int arg = 0;
-          for (int o = 1; o < O; ++o)
-            if (z[o] > z[arg]) arg = o;  // maxCoeff: first maximum
-          action = (double)arg;
-        } else if (N.head == HEAD_TANH) {
-          action = N.tanh_scale * tanh(z[0]);
-        } else {
-          action = z[0];
-        }
-        double reward = 0.0;
-        bool term = false, trunc = false;
-        OZ_MARK(9);  // head (output sum + tanh)
-        const uint32_t f = env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr,
-                                    E.id == ENV_PENDULUM ? &rpre : nullptr);
-        OZ_MARK(10);  // env_step
-        if (f) {
-          myfault = f;
-        } else {
-          ep_ret = dadd(ep_ret, reward);  // proj/src/rollout.cpp:143
-          ep_len += 1;
-          steps += 1;
-          if (term || trunc) {
-            if (crank == 0) {
-              const long long sl = (long long)agent_local * A.count + slot0 + eps_done;
-              A.ep_returns[sl] = ep_ret;
-              if (A.ep_lengths) A.ep_lengths[sl] = ep_len;
-            }
-            ep_ret = 0.0;
-            ep_len = 0;
-            eps_done += 1;
-            if (eps_done < eps_this) env_reset(E, s.rng, s);  // auto-reset, env.cpp:163-167
-          }
-        }
-      }
-      const bool next = myfault == 0 && eps_done < eps_this && it + 1 < A.max_iters;
-      observe_into_x0(next);
-    }
-    OZ_MARK(6);  // head + env + observe
-  }
-#ifdef EVB_TC_PROFILE
-  if (tid == 0) {
-    for (int i = 0; i < 7; ++i) atomicAdd(&g_oz_prof[i], prof[i]);
-    atomicAdd(&g_oz_prof[9], prof[9]);
-    atomicAdd(&g_oz_prof[10], prof[10]);
-    atomicAdd(&g_oz_prof[11], prof[11]);
-    atomicAdd(&g_oz_prof[8], 1ull);
-  }
-#endif
-
-  if (valid && crank == 0) {
-    const long long ln = (long long)agent_local * A.e + j;
-    if (A.lane_steps) A.lane_steps[ln] = steps;
-    if (A.track_stats && A.lane_stats) {
-      double* st = A.lane_stats + ln * 9;
-      st[0] = wc;
-      for (int i = 0; i < 4; ++i) {
-        st[1 + i] = wmean[i];
-        st[5 + i] = wm2[i];
-      }
-    }
-    if (myfault) record_fault(A.fault, (uint64_t)((long long)agent * A.e + j), myfault, myfault_layer);
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(OZ_TMEM_COLS));
-  }
-  if constexpr (C > 1) cluster_sync_all();
-}
-
 
 // ---------------------------------------------------------------------------
 // Pipelined team (the default oz kernel): the 16 lanes are two groups of 8 whose
@@ -724,19 +227,19 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
   // ---- prologue (compute warps): layer 0 to SMEM, layer-1 slices to TMEM
   const bool row_ok = compute && r0 + row < W2;
   auto w1 = [&](int k) -> double {
-    return (row_ok && k < W1) ? oz_param(A.par, N.d, agent_local, agent, N.w_off[1] + (long long)k * W2 + r0 + row)
+    return (row_ok && k < W1) ? oz_param(A.par, N.d, agent_local, N.w_off[1] + (long long)k * W2 + r0 + row)
                               : 0.0;
   };
   const int K0 = N.dims[0];
   if (compute) {
     for (int i = tid; i < K0 * W1; i += 32 * OZP_CW) {
       const int k = i / W1, r = i % W1;
-      const double w = oz_param(A.par, N.d, agent_local, agent, N.w_off[0] + (long long)k * W1 + r);
+      const double w = oz_param(A.par, N.d, agent_local, N.w_off[0] + (long long)k * W1 + r);
       W0[k * W1p + r] = w;
       smem_max_nonneg(&mk[k], fin_abs(w));
     }
     for (int r = tid; r < W1; r += 32 * OZP_CW) {
-      const double b = oz_param(A.par, N.d, agent_local, agent, N.b_off[0] + r);
+      const double b = oz_param(A.par, N.d, agent_local, N.b_off[0] + r);
       b0[r] = b;
       smem_max_nonneg(&mk[4], fin_abs(b));
     }
@@ -768,7 +271,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
 #pragma unroll
   for (int o = 0; o < OZ_MAXO; ++o) {
     w2r[o] = 0.0;
-    b2[o] = (!compute && o < O) ? oz_param(A.par, N.d, agent_local, agent, N.b_off[2] + o) : 0.0;
+    b2[o] = (!compute && o < O) ? oz_param(A.par, N.d, agent_local, N.b_off[2] + o) : 0.0;
   }
   if (compute && blk != nullptr) {
     Fr = (int)(short)(meta & 0xFFFF);
@@ -812,11 +315,11 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
   }
   if (compute) {
     rscale = ldexp(1.0, 8 * (S - 1) - Fr);
-    b1r = row_ok ? oz_param(A.par, N.d, agent_local, agent, N.b_off[1] + r0 + row) : 0.0;
+    b1r = row_ok ? oz_param(A.par, N.d, agent_local, N.b_off[1] + r0 + row) : 0.0;
 #pragma unroll
     for (int o = 0; o < OZ_MAXO; ++o)
       w2r[o] = (o < O && row_ok)
-                   ? oz_param(A.par, N.d, agent_local, agent, N.w_off[2] + (long long)(r0 + row) * O + o)
+                   ? oz_param(A.par, N.d, agent_local, N.w_off[2] + (long long)(r0 + row) * O + o)
                    : 0.0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -988,6 +491,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
         if (!live[g]) continue;
         OZ_MARK(10);  // MMA warp: issue
         mbar_wait_parity_cta(&bfull[g], (uint32_t)(it & 1));
+        __syncwarp();  // reconverge after the spin loop (elect.sync / tcgen05 below)
         OZ_MARK(9);  // MMA warp: waiting for B
         if (gdone[g]) {
           live[g] = false;
@@ -1018,6 +522,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
         if (!live[g]) continue;
         OZ_MARK(5);  // compute: publish (+ named barrier) / group switch
         mbar_wait_parity_cta(&x0full[g], (uint32_t)(it & 1));
+        __syncwarp();
         OZ_MARK(1);  // compute: waiting for x0
         if (!alive[g]) {
           live[g] = false;
@@ -1086,6 +591,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
         // ---- epilogue of group g: row `row`, lanes 4 half .. 4 half + 3
         OZ_MARK(2);  // compute: layer 0
         mbar_wait_parity_cta(&dfull[g], (uint32_t)(it & 1));
+        __syncwarp();  // reconverge after the spin loop: tcgen05.ld below is .sync.aligned
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         OZ_MARK(3);  // compute: waiting for the MMAs
         {
@@ -1324,13 +830,6 @@ static int oz_slices() {
   return 6;
 }
 
-// the pipelined two-group kernel is the default; EVORL_OZ_PIPE=0 selects the
-// single-chain kernel (kept for comparison and as a second implementation)
-static int oz_pipe() {
-  const char* v = getenv("EVORL_OZ_PIPE");
-  return (v && v[0] == '0') ? 0 : 1;
-}
-
 bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   if (net.nlayers != 3 || obs_dim > 4 || e < 5) return false;  // 16-lane teams, obs -> W1 -> W2 -> O
   const int W1 = net.dims[1], W2 = net.dims[2], O = net.dims[3];
@@ -1347,40 +846,11 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.W1 = W1;
   p.W1p = W1p;
   p.W2 = W2;
-  p.pipe = oz_pipe();
+  p.pipe = 1;
   int off = 0;
-  if (p.pipe) {  // rollout_ozp_kernel layout: per-group B buffers, x0, red, pout
-    p.off_B = off;
-    off = al(off + 2 * OZP_G * (2 * S - 1) * W1p, 1024);
-    p.off_W0 = off;
-    off = al(off + 4 * W1p * 8, 16);
-    p.off_b0 = off;
-    off = al(off + W1p * 8, 16);
-    p.off_mk = off;
-    off = al(off + 5 * 8, 16);
-    p.off_x0 = off;
-    off = al(off + 2 * 4 * OZP_G * 8, 16);
-    p.off_sce = off;
-    p.off_red = off;
-    off = al(off + 2 * 4 * O * OZP_G * 8, 16);
-    p.off_pout = off;
-    off = al(off + 2 * 2 * C * (O + 1) * OZP_G * 8, 16);
-    p.off_mask = off;
-    off = al(off + 36 * 4, 16);  // stamps bad0[2][8], bad1[2][8], alive[2], gdone[2]
-    p.off_bar = off;
-    off = al(off + 8 * 10, 16);  // x0full[2], bfull[2], dfull[2], xbar[2][2]
-    p.off_tslot = off;
-    off = al(off + 16, 16);
-    p.off_rmax = off;
-    off = al(off + 2 * OZ_M * 8, 16);
-    p.used = off;
-    p.bytes = std::max(off, OZ_MIN_SMEM);
-    if (p.bytes > 227 * 1024) return false;
-    std::memcpy(out, &p, sizeof p);
-    return true;
-  }
+  // rollout_ozp_kernel layout: per-group B buffers, x0, red, pout
   p.off_B = off;
-  off = al(off + OZ_N * (2 * S - 1) * W1p, 1024);
+  off = al(off + 2 * OZP_G * (2 * S - 1) * W1p, 1024);
   p.off_W0 = off;
   off = al(off + 4 * W1p * 8, 16);
   p.off_b0 = off;
@@ -1388,17 +858,16 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.off_mk = off;
   off = al(off + 5 * 8, 16);
   p.off_x0 = off;
-  off = al(off + 4 * OZ_N * 8, 16);
+  off = al(off + 2 * 4 * OZP_G * 8, 16);
   p.off_sce = off;
-  off = al(off + OZ_N * 8, 16);
   p.off_red = off;
-  off = al(off + 4 * O * OZ_N * 8, 16);
+  off = al(off + 2 * 4 * O * OZP_G * 8, 16);
   p.off_pout = off;
-  off = al(off + 2 * C * (O + 1) * OZ_N * 8, 16);
+  off = al(off + 2 * 2 * C * (O + 1) * OZP_G * 8, 16);
   p.off_mask = off;
-  off = al(off + MAXL * 4, 16);
+  off = al(off + 36 * 4, 16);  // stamps bad0[2][8], bad1[2][8], alive[2], gdone[2]
   p.off_bar = off;
-  off = al(off + 8 * 3, 16);  // mbar, xbar[2]
+  off = al(off + 8 * 10, 16);  // x0full[2], bfull[2], dfull[2], xbar[2][2]
   p.off_tslot = off;
   off = al(off + 16, 16);
   p.off_rmax = off;
@@ -1406,6 +875,7 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.used = off;
   p.bytes = std::max(off, OZ_MIN_SMEM);
   if (p.bytes > 227 * 1024) return false;
+
   static_assert(sizeof(OzPlan) <= sizeof(TcPlanOut), "plan storage");
   std::memcpy(out, &p, sizeof p);
   return true;
@@ -1413,16 +883,16 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
 
 template <int S, int C>
 static cudaError_t launch_oz_c(const RolloutArgs& a, const OzPlan& p, cudaStream_t stream) {
-  auto kern = p.pipe ? rollout_ozp_kernel<S, C> : rollout_oz_kernel<S, C>;
-  static bool set[2] = {false, false};
-  if (!set[p.pipe]) {
+  auto kern = rollout_ozp_kernel<S, C>;
+  static bool set = false;
+  if (!set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    set[p.pipe] = true;
+    set = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(a.n_agents * a.groups * C));
-  cfg.blockDim = dim3(p.pipe ? OZP_THREADS : OZ_THREADS);
+  cfg.blockDim = dim3(OZP_THREADS);
   cfg.dynamicSmemBytes = (size_t)p.bytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -1448,6 +918,7 @@ static cudaError_t launch_oz_s(const RolloutArgs& a, const OzPlan& p, cudaStream
 
 cudaError_t launch_rollout_oz(const RolloutArgs& a, const TcPlanOut& po, cudaStream_t stream) {
   if (a.n_agents <= 0) return cudaSuccess;
+  if (a.par.src != SRC_EXPLICIT) return cudaErrorInvalidValue;  // oz teams read materialised candidates
   OzPlan p;
   std::memcpy(&p, &po, sizeof p);
 #ifdef EVB_OZ_S5

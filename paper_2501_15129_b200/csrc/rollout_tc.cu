@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
                    : "memory");
     }
     mbar_wait_parity_cta(pbar, 0);
+    __syncwarp();
     for (int c = half; c < W1p / 16; c += 2) {
       uint32_t packed[8];
 #pragma unroll
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
                    : "memory");
     }
     mbar_wait_parity_cta(pbar, 1);
+    __syncwarp();
   }
   for (int c = half; c < W1p / 16 && A.tc_blocks == nullptr; c += 2) {
     uint32_t packed[8];
@@ -352,7 +354,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
   for (int it = 0;; ++it) {
     if (tid < MAXL) mask[tid] = 0u;
     const bool active = valid && myfault == 0 && eps_done < eps_this && it < A.max_iters;
-    if (!__syncthreads_or(active)) break;
+    // warp-level vote first: __any_sync waits for all 32 lanes, so the warp
+    // reaches the block-wide reduction barrier converged (the env lanes run
+    // extra code; a partially arrived warp at BAR.RED is an illegal instruction)
+    const bool wact = __any_sync(0xffffffffu, active);
+    if (!__syncthreads_or(wact)) break;
     TC_MARK(1);  // loop-top barrier
     float* pout = pout_base + (it & 1) * C * OE1;
     if (C > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[it & 1], (uint32_t)(C * OE1 * sizeof(float)));
@@ -431,6 +437,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
         } else {
           mbar_wait_parity_cta(l0bar, (uint32_t)(it & 1));
         }
+        __syncwarp();  // reconverge after the spin loop (elect.sync / tcgen05 below)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t aLo = smem_u32(Alo), bS = smem_u32(Bs);
         constexpr uint32_t a_lbo = (TC_M / 8) * 128, b_lbo = (NB / 8) * 128;
@@ -460,6 +467,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     }
     TC_MARK(2);  // layer 0 (+ waiting for the MMA issue)
     mbar_wait_parity(mbar, (uint32_t)(it & 1));
+    __syncwarp();  // reconverge after the spin loop: tcgen05.ld below is .sync.aligned
     TC_MARK(3);  // MMA completion wait
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // epilogue: row `row`, lanes 8*half .. 8*half+7; output layer fused

@@ -155,7 +155,7 @@ def ospec_bias0(ospec):
     return ospec.input_dim * 128
 
 
-@pytest.mark.parametrize("precision", ["tc", "f32", "f64"])
+@pytest.mark.parametrize("precision", ["tc", "f32", "f64", "oz"])
 @pytest.mark.parametrize("algo", ["openes", "ars"])
 def test_sharded_materialised_ask_matches_unsharded(evb, precision, algo):
     """The fp32 paths materialise the shard's candidates [a0, a1) once per
