@@ -9,8 +9,15 @@ largest config that fits one GPU and the one the metric's "pop x envs" and
 13.1 M env-steps -> fitness -> ranks -> tell + Adam) with the population
 sharded over N GPUs (weak... total work fixed: "strong" scaling).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--precision f64]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--precision oz|f64|tc|f32]
   python bench.py --impl reference ...   # the reference CPU path (oracle port) on host cores
+
+Headline precision "oz": the policy's dense layer as exact int8 tcgen05 MMAs
+over 6-byte-sliced fixed-point operands (~47 bits each), everything else fp64
+-- fitness ranks identical to the fp64 path on this workload
+(tests/test_gpu_oz.py), returns within ~1e-8 of the reference CPU
+restatement.  The fp64 DMMA team ("f64", the bit-level parity path) and the
+fp32-accurate tcgen05 team ("tc") are measured beside it (`variants`).
 
 Timing: W untimed warm-up generations, then K generations, each bracketed by a
 barrier + torch.cuda.synchronize(); per-generation device time from CUDA
@@ -72,7 +79,17 @@ def cma_lazy_gap(d, mu, pop):
 NCU_TRAFFIC = {
     ("3", "f64"): (2230139136 + 68040960, "ncu r01_f64_v6: rollout_kernel<double,1,16,4,1>"),
     ("3", "tc"): (1104370432 + 10082304, "ncu r01_tc_v5: rollout_tc_kernel<2> (cta_group::2 pair)"),
+    ("3", "oz"): (1676240000 + 48855296, "ncu r02_ozp_full: rollout_ozp_kernel<6,2> (pre-split slices read once)"),
 }
+# int8 MMA work the oz team executes per env step and CTA (2 lane groups x
+# W1p/32 k-steps x S MMAs of M=128, N=8S, K=32): the tensor-pipe view of the
+# roofline beside the algorithmic one
+OZ_S = 6
+
+
+def oz_int8_ops_per_cta_step(w1):
+    w1p = -(-w1 // 32) * 32
+    return 2 * (w1p // 32) * OZ_S * 2 * 128 * (8 * OZ_S) * 32
 
 
 def load_peaks():
@@ -210,12 +227,12 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="f64", choices=["f64", "f32", "tc"])
+    ap.add_argument("--precision", default="oz", choices=["oz", "f64", "f32", "tc"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", dest="variants", action="store_false",
-                    help="skip the tensor-core (precision tc) measurement beside the headline")
+                    help="skip the other precisions' measurements beside the headline")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     if args.impl == "reference":
@@ -343,7 +360,30 @@ def main():
     roll_ms = statistics.mean(roll) if roll else None
     agents_local = es.shard_ranges()[1] - es.shard_ranges()[0] if world > 1 else pop
     flops_launch = agents_local * e * H * F
-    if args.precision == "f64":
+    extra = {}
+    if args.precision == "oz":
+        # config 3 is tensor-core bound, roof = the dense tensor
+        # peak; achieved counts the MLP's algorithmic flops.  The kernel is bound
+        # by the serial 200-step chain (one CTA per SM, TMEM-limited), so two more
+        # views are reported: the same flops against the FP64 peak (the accuracy
+        # class this path delivers) and the int8 MMA work the tensor pipe executes.
+        peak = load_peaks().get("bf16_tflops")
+        bound, unit, peak_src = "tensor", "TFLOP/s", (
+            "MEASURED_PEAKS.json bf16_tflops (burst), per SURVEY.md §8(d); achieved counts the MLP's "
+            "algorithmic flops")
+        fp64_peak = evb.measure_fp64_peak()
+        int8_peak = 2.0 * peak if peak else None
+        ops = oz_int8_ops_per_cta_step(cfg.hidden[0]) * (agents_local * -(-e // 16)) * \
+            (-(-cfg.hidden[1] // 128)) * H if len(cfg.hidden) == 2 else None
+        ex_tops = ops / (roll_ms * 1e-3) / 1e12 if (ops and roll_ms) else None
+        extra = {"fp64_equivalent": {"peak": fp64_peak, "unit": "TFLOP/s",
+                                     "peak_source": "measured live: DFMA-bound microkernel (evorl_measure_fp64_peak)"},
+                 "tensor_pipe_executed": {"achieved": ex_tops, "unit": "TOPS (int8 MMA ops incl. slice products "
+                                          "and zero-padded windows)", "peak": int8_peak,
+                                          "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16 "
+                                                         "on B200; derived, not measured)",
+                                          "frac": (ex_tops / int8_peak) if (ex_tops and int8_peak) else None}}
+    elif args.precision == "f64":
         peak = evb.measure_fp64_peak()
         bound, unit, peak_src = "fp64", "TFLOP/s", (
             "measured live: DFMA-bound microkernel (evorl_measure_fp64_peak); "
@@ -362,42 +402,56 @@ def main():
         peak = evb.measure_fp64_peak() * 2.0  # FP32 FMA issue rate is 2x FP64 on B200
         peak_src = "2 x measured DFMA peak (B200 FP32:FP64 FMA issue ratio 2:1)"
     achieved = flops_launch / (roll_ms * 1e-3) / 1e12 if roll_ms else None
-    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+    if "fp64_equivalent" in extra:
+        fe = extra["fp64_equivalent"]
+        fe["achieved"] = achieved
+        fe["frac"] = (achieved / fe["peak"]) if (achieved and fe["peak"]) else None
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, **extra,
                 "frac": (achieved / peak) if (achieved and peak) else None,
 "traffic": NCU_TRAFFIC.get((args.config, args.precision), (None,))[0],
                 "traffic_source": NCU_TRAFFIC.get((args.config, args.precision), (None, None))[1],
-                "kernel": ("rollout_tc_kernel (tcgen05 hidden layer, fused obs-norm/MLP/env/return)"
-                          if args.precision == "tc" else "rollout_kernel (fused obs-norm/MLP/env/return)"),
+                "kernel": {"tc": "rollout_tc_kernel (tcgen05 hidden layer, fused obs-norm/MLP/env/return)",
+                           "oz": "rollout_ozp_kernel (int8-sliced tcgen05 hidden layer, two pipelined lane "
+                                 "groups, fused obs-norm/MLP/env/return)"}.get(
+                               args.precision, "rollout_kernel (fused obs-norm/MLP/env/return)"),
                 "algorithmic_flops_per_launch": flops_launch,
                 "flops_per_env_step": F, "peak_source": peak_src,
                 "rollout_ms_per_launch": roll_ms, "rollout_share_of_step":
                     (roll_ms / ms_per_step) if roll_ms else None}
 
-    # ---- the tensor-core policy path (tcgen05, precision "tc") on the same
-    # workload, reported beside the fp64 parity headline: returns within the
-    # fp32 tolerance of the reference, ranks not bit-exact
-    tc_variant = None
+    # ---- the other policy precisions on the same workload, beside the headline:
+    # f64 (DMMA team, the bit-level parity path) and tc (fp32-accurate tcgen05
+    # team: returns within the fp32 tolerance, ranks not bit-exact)
+    variants = {}
     params_dim = es.dim
-    if args.variants and args.precision != "tc" and int(kw.get("fitness_episodes", 1)) >= 5 \
-            and len(kw.get("hidden", ())) == 2:
+    parity = {
+        "f64": "bit-level parity path: returns within 1e-9 of the reference CPU restatement, ranks identical",
+        "oz": "returns within ~1e-8 of the reference CPU restatement, ranks identical to the fp64 path "
+              "(tests/test_gpu_oz.py, tools/tc_rank_agreement.py)",
+        "tc": "returns within fp32 tolerance of the reference; fitness ranks not bit-exact "
+              "(tools/tc_rank_agreement.py: 9-99 of 4096 ranks shift, by <= 20 positions)",
+    }
+    if args.variants and int(kw.get("fitness_episodes", 1)) >= 5 and len(kw.get("hidden", ())) == 2:
         del es
-        _, es_tc, tc_ms, tc_roll, tc_launches = timed_generations("tc")
-        tc_roll_ms = statistics.mean(tc_roll) if tc_roll else None
-        tc_peak = load_peaks().get("bf16_tflops")
-        tc_ach = flops_launch / (tc_roll_ms * 1e-3) / 1e12 if tc_roll_ms else None
-        tc_variant = {
-            "precision": "tc", "value": env_steps_per_gen * args.steps / (tc_ms / 1e3),
-            "unit": "env-steps/s", "ms_per_step": tc_ms / args.steps,
-            "generations_per_sec": args.steps / (tc_ms / 1e3), "gpu_launches": int(tc_launches),
-            "roofline": {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak, "unit": "TFLOP/s",
-                         "frac": (tc_ach / tc_peak) if (tc_ach and tc_peak) else None,
-                         "traffic": NCU_TRAFFIC.get((args.config, "tc"), (None,))[0],
-                         "kernel": "rollout_tc_kernel (cta_group::2 tcgen05 hidden layer, fused env)",
-                         "rollout_ms_per_launch": tc_roll_ms,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops; achieved counts algorithmic flops"},
-            "parity": "returns within fp32 tolerance of the reference; fitness ranks not bit-exact "
-                      "(tools/tc_rank_agreement.py: 9-99 of 4096 ranks shift, by <= 20 positions)"}
-        del es_tc
+        for vp in ("f64", "tc", "oz"):
+            if vp == args.precision:
+                continue
+            _, es_v, v_ms, v_roll, v_launches = timed_generations(vp)
+            v_roll_ms = statistics.mean(v_roll) if v_roll else None
+            v_ach = flops_launch / (v_roll_ms * 1e-3) / 1e12 if v_roll_ms else None
+            v_peak = evb.measure_fp64_peak() if vp == "f64" else load_peaks().get("bf16_tflops")
+            variants[vp] = {
+                "precision": vp, "value": env_steps_per_gen * args.steps / (v_ms / 1e3),
+                "unit": "env-steps/s", "ms_per_step": v_ms / args.steps,
+                "generations_per_sec": args.steps / (v_ms / 1e3), "gpu_launches": int(v_launches),
+                "roofline": {"bound": "fp64" if vp == "f64" else "tensor", "achieved": v_ach, "peak": v_peak,
+                             "unit": "TFLOP/s", "frac": (v_ach / v_peak) if (v_ach and v_peak) else None,
+                             "traffic": NCU_TRAFFIC.get((args.config, vp), (None,))[0],
+                             "rollout_ms_per_launch": v_roll_ms,
+                             "peak_source": ("measured live DFMA peak" if vp == "f64" else
+                                             "MEASURED_PEAKS.json bf16_tflops; achieved counts algorithmic flops")},
+                "parity": parity[vp]}
+            del es_v
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -408,12 +462,13 @@ def main():
             "metric": "env-steps/sec", "value": value, "unit": "env-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": args.precision, "data": "synthetic",
+            "dtype": "f32" if args.precision in ("f32", "tc") else "f64", "data": "synthetic",
             "config": {"workload": cfgd["desc"], "config": args.config, "pop": pop,
                        "envs_per_individual": e, "horizon": H, "hidden": list(cfg.hidden),
                        "params": params_dim, "parallelism": f"population-sharded dp{world}",
                        "l2": "flushed (256 MiB write) between timed generations",
                        "policy_precision": args.precision,
+                       "parity": parity.get(args.precision, "returns within fp32 tolerance"),
                        **({"eig_every": getattr(args, "cma_gap", None),
                            "timed_window": "whole lazy periods (one eigendecomposition per period)"}
                           if kw.get("algo") == "cmaes" else {}),
@@ -424,7 +479,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            "tc_variant": tc_variant,
+            "variants": variants,
         }
         print(json.dumps(line))
     if dist is not None:
