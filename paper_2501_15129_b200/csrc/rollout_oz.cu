@@ -18,12 +18,13 @@
 //     S = 6 keeps ~47 bits of every operand: the policy output differs from
 //     fp64 arithmetic by ~1e-13 relative (fitness differences at the level of
 //     the fp64 path's own libm/ordering differences from the reference CPU).
-//   * One accumulator per lane group for all t: the B operand lives in SMEM as
-//     S data blocks behind S-1 zero blocks of 8 lanes, [0 .. 0 | B_0 .. B_(S-1)],
-//     and MMA i (A_i from TMEM) reads the window that starts at block S-1-i, so
-//     column block c of D receives A_i B_(c-i) (zero for c < i): D[:, 8t..8t+7]
-//     = D_t.  Per k-step of 32: S TS MMAs of M = 128, N = 8 S, K = 32
-//     (tools/umma_i8_bench.cu checks the scheme and times it).
+//   * One accumulator per lane group for all t: the B operand is the S slice
+//     blocks of 8 lanes [B_0 .. B_(S-1)] in SMEM, and MMA i (A_i from TMEM)
+//     writes D from column block i on with N = 8 (S - i) rounded up to 16, so
+//     column block c of D receives A_i B_(c-i): D[:, 8t..8t+7] = D_t (the
+//     rounding spills into block S, never read).  Per k-step of 32: S TS MMAs
+//     of M = 128, K = 32, N = 48, 48, 32, 32, 16, 16 (tools/umma_i8_bench.cu
+//     checks the scheme and times it: 48 MMAs in ~920 cycles).
 //   * TMEM (512 columns, one team CTA per SM): A slices at columns 512 - S W1p/4
 //     (written once by tcgen05.st from pre-split blocks), D_g at columns 8 S g.
 //   * Per env step (one CTA = 128 weight rows; C = W2/128 CTAs per agent) the
@@ -87,6 +88,23 @@ EVB_DEV void oz_mma_ts_elect(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uin
       "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
       "r"(atmem), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// single-thread forms (the caller elects the issuing lane once per group-step)
+EVB_DEV bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}"
+               : "=r"(p));
+  return p != 0;
+}
+EVB_DEV void oz_mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"((uint32_t)acc));
+}
+EVB_DEV void oz_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
 }
 EVB_DEV void oz_commit_elect(uint64_t* bar) {
   asm volatile(
@@ -182,11 +200,11 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
   const int W1 = P.W1, W1p = P.W1p, W2 = P.W2, O = N.dims[3];
   const int r0 = crank * OZ_M;
   const int row = quad * 32 + lane;
-  constexpr int RB = OZP_G * (2 * S - 1);         // rows (N) of one zero-padded B buffer
+  constexpr int RB = OZP_G * (S + 1);             // rows (N) of one B buffer: S data blocks + a spill block
   const uint32_t LBO = (uint32_t)(RB / 8) * 128;  // K-direction core-matrix stride
   const int BBYTES = RB * W1p;                    // one group's B buffer
   const uint32_t colA = (uint32_t)(OZ_TMEM_COLS - S * (W1p / 4));
-  constexpr int NG = OZP_G * S;                   // MMA N per group
+  constexpr int NG = OZP_G * (S + 1);             // accumulator columns per group (D_0..D_(S-1) + spill)
 
 #ifdef EVB_TC_PROFILE
   unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -498,16 +516,25 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
           continue;
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t bg = bS + (uint32_t)(g * BBYTES);
-        for (int ks = 0; ks < W1p / 32; ++ks) {
+        // one elected lane issues the whole group-step: descriptors advance by
+        // constant strides (the B start address field by 2 LBO >> 4 per k-step,
+        // the A TMEM column by 8), so each MMA is an add or two plus the issue
+        if (elect_one()) {
+          const uint64_t bd0 = oz_desc(bS + (uint32_t)(g * BBYTES), LBO, 128);
+          const uint32_t dg = tmem + (uint32_t)(g * NG);
+          const uint32_t aS = (uint32_t)(W1p / 4);
+          const int KS = W1p / 32;
+          for (int ks = 0; ks < KS; ++ks) {
+            const uint64_t bd = bd0 + (uint64_t)((uint32_t)ks * ((2 * LBO) >> 4));
+            const uint32_t a0 = tmem + colA + (uint32_t)ks * 8;
 #pragma unroll
-          for (int i = 0; i < S; ++i) {
-            const uint64_t bd = oz_desc(bg + (uint32_t)(S - 1 - i) * 128 + (uint32_t)ks * 2 * LBO, LBO, 128);
-            oz_mma_ts_elect(tmem + (uint32_t)(g * NG), tmem + colA + (uint32_t)(i * (W1p / 4) + ks * 8), bd,
-                            oz_idesc(OZ_M, NG, i == 0), (ks | i) ? 1u : 0u);
+            for (int i = 0; i < S; ++i)  // D blocks i .. += A_i [B_0 B_1 ..]; N = 8 (S - i) rounded up to 16
+              oz_mma_ts(dg + (uint32_t)(OZP_G * i), a0 + (uint32_t)i * aS, bd,
+                        oz_idesc(OZ_M, (OZP_G * (S - i) + 15) / 16 * 16, i == 0), (ks | i) != 0);
           }
+          oz_commit(&dfull[g]);
         }
-        oz_commit_elect(&dfull[g]);
+        __syncwarp();
       }
     }
   } else {
@@ -580,7 +607,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
                 wv[w] = gather_byte(H ? qhi[4 * w] : qlo[4 * w], H ? qhi[4 * w + 1] : qlo[4 * w + 1],
                                     H ? qhi[4 * w + 2] : qlo[4 * w + 2], H ? qhi[4 * w + 3] : qlo[4 * w + 3],
                                     (Pb & 31) >> 3);
-              *reinterpret_cast<uint2*>(Bme + (size_t)(S - 1 + jj) * 128) = make_uint2(wv[0], wv[1]);
+              *reinterpret_cast<uint2*>(Bme + (size_t)jj * 128) = make_uint2(wv[0], wv[1]);
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B_g visible to the tensor core
@@ -836,7 +863,7 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   if (net.dims[0] > 4 || O > OZ_MAXO) return false;
   const int S = oz_slices();
   const int W1p = (W1 + 31) / 32 * 32;
-  if (S * (W1p / 4) + OZ_N * S > OZ_TMEM_COLS) return false;  // A slices + accumulator in TMEM
+  if (S * (W1p / 4) + 2 * OZP_G * (S + 1) > OZ_TMEM_COLS) return false;  // A slices + 2 accumulators in TMEM
   int C = 1;
   while (C * OZ_M < W2) C *= 2;
   if (C > 8) return false;
@@ -850,7 +877,7 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   int off = 0;
   // rollout_ozp_kernel layout: per-group B buffers, x0, red, pout
   p.off_B = off;
-  off = al(off + 2 * OZP_G * (2 * S - 1) * W1p, 1024);
+  off = al(off + 2 * OZP_G * (S + 1) * W1p, 1024);
   p.off_W0 = off;
   off = al(off + 4 * W1p * 8, 16);
   p.off_b0 = off;

@@ -185,10 +185,152 @@ int run(int reps) {
   return bad != 0;
 }
 
+
+// Exact-N variant for 8-lane groups (the pipelined team): MMA i writes D
+// columns [8i, 8i + N_i) with N_i = 8(S-i) rounded up to 16 and reads the data
+// blocks B_0.. from block 0 (no zero blocks); the rounding spills into column
+// block S (ignored).  Checks D_t = sum_{i+j=t} A_i B_j for t < S and times it.
+template <int S>
+__global__ void bench_exact(const uint8_t* A, const uint8_t* B, int* out, long long* cyc, int reps) {
+  constexpr int G = 8;                 // lanes per group
+  constexpr int R = G * (S + 1);       // data blocks + one spill block
+  constexpr uint32_t LBO = (R / 8) * 128;
+  __shared__ __align__(1024) uint8_t Bs[R * K];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid & 31;
+  for (int i = tid; i < R * K / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(Bs)[i] = 0u;
+  __syncthreads();
+  for (int i = tid; i < S * G * K; i += blockDim.x) {
+    const int j = i / (G * K), e = (i / K) % G, k = i % K;
+    Bs[boff(j * G + e, k, R)] = B[(j * NL + e) * K + k];
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  const uint32_t colA = 512 - 64 * S;
+  if (warp < 4) {
+    const int row = warp * 32 + lane;
+    for (int i = 0; i < S; ++i)
+      for (int c0 = 0; c0 < 64; c0 += 8) {
+        uint32_t v[8];
+        for (int q = 0; q < 8; ++q) v[q] = *reinterpret_cast<const uint32_t*>(A + ((size_t)i * M + row) * K + (c0 + q) * 4);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                         tmem + ((uint32_t)(warp * 32) << 16) + colA + 64 * i + c0),
+                     "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                     : "memory");
+      }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0) {
+    uint32_t phase = 0;
+    long long best = 1ll << 60;
+    for (int rep = 0; rep < reps; ++rep) {
+      const long long t0 = clock64();
+      for (int ks = 0; ks < K / 32; ++ks)
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          const int n = ((8 * (S - i)) + 15) / 16 * 16;
+          const uint64_t bd = desc(su32(Bs) + ks * 2 * LBO, LBO, 128);
+          mma_ts(tmem + 8 * i, tmem + colA + 64 * i + ks * 8, bd, idesc_i8(M, n, i == 0),
+                 (ks > 0 || i > 0) ? 1u : 0u);
+        }
+      asm volatile(
+          "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&bar))
+          : "memory");
+      const long long t1 = clock64();
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      const long long t2 = clock64();
+      if (t2 - t0 < best) {
+        best = t2 - t0;
+        if (lane == 0) {
+          cyc[0] = t1 - t0;
+          cyc[1] = t2 - t0;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp < 4) {
+    const int row = warp * 32 + lane;
+    for (int c0 = 0; c0 < G * S; c0 += 8) {
+      uint32_t v[8];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                   : "r"(tmem + ((uint32_t)(warp * 32) << 16) + c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int q = 0; q < 8; ++q) out[row * (G * S) + c0 + q] = (int)v[q];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int S>
+int run_exact(int reps) {
+  constexpr int G = 8, N = G * S;
+  std::vector<uint8_t> A((size_t)S * M * K), B((size_t)S * NL * K);
+  srand(77 + S);
+  for (auto& x : A) x = (uint8_t)(rand() & 0xFF);
+  for (auto& x : B) x = (uint8_t)(rand() & 0xFF);
+  uint8_t *dA, *dB;
+  int* dO;
+  long long* dc;
+  cudaMalloc(&dA, A.size());
+  cudaMalloc(&dB, B.size());
+  cudaMalloc(&dO, sizeof(int) * M * N);
+  cudaMalloc(&dc, 16);
+  cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
+  bench_exact<S><<<1, 128>>>(dA, dB, dO, dc, reps);
+  std::vector<int> O((size_t)M * N);
+  long long cyc[2];
+  cudaError_t e = cudaMemcpy(O.data(), dO, sizeof(int) * M * N, cudaMemcpyDeviceToHost);
+  cudaMemcpy(cyc, dc, 16, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    printf("exact S=%d: %s\n", S, cudaGetErrorString(e));
+    return 1;
+  }
+  long long bad = 0;
+  for (int r = 0; r < M; ++r)
+    for (int t = 0; t < S; ++t)
+      for (int l = 0; l < G; ++l) {
+        long long acc = 0;
+        for (int i = 0; i <= t; ++i)
+          for (int k = 0; k < K; ++k) {
+            const int a = i == 0 ? (int)(int8_t)A[((size_t)i * M + r) * K + k] : (int)A[((size_t)i * M + r) * K + k];
+            acc += (long long)a * (int)B[((size_t)(t - i) * NL + l) * K + k];
+          }
+        if (acc != (long long)O[r * N + t * G + l]) {
+          if (bad < 5) printf("  mismatch r=%d t=%d lane=%d: got %d want %lld\n", r, t, l, O[r * N + t * G + l], acc);
+          ++bad;
+        }
+      }
+  printf("exact-N S=%d (8-lane group): %d MMAs issue %lld cyc, complete %lld cyc -> %.1f cyc/MMA; mismatches %lld\n", S,
+         8 * S, cyc[0], cyc[1], (double)cyc[1] / (8 * S), bad);
+  return bad != 0;
+}
+
 int main() {
   int rc = 0;
   rc |= run<4>(8);
   rc |= run<5>(8);
   rc |= run<6>(8);
+  rc |= run_exact<6>(8);
   return rc;
 }
