@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
   constexpr int NG = OZP_G * (S + 1);             // accumulator columns per group (D_0..D_(S-1) + spill)
 
 #ifdef EVB_TC_PROFILE
-  unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long prof[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
 #endif
   for (int i = tid; i < P.used / 4; i += OZP_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
   uint32_t* bad1 = flags + 16;  // [2][8] the same for layer 1
   uint32_t* alive = flags + 32; // [2] group has an active lane at this step
   uint32_t* gdone = flags + 34; // [2] group finished (compute -> MMA warp)
+  int* gexp = reinterpret_cast<int*>(flags + 36);  // [2][8] lane exponent G of layer 0's fixed point (env -> compute)
   const int OEg = O * OZP_G, OE1g = (O + 1) * OZP_G;
   OZ_MARK(0);  // prologue
 
@@ -400,11 +401,18 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
           }
         }
       }
-      for (int i = 0; i < E.obs_dim; ++i) {  // (o - mean) * (1 / den), as the plain oz team
+      // (o - mean) * (1 / den): within an ulp of the fp64 team's IEEE division,
+      // far below this team's ~1e-13 policy tolerance, and off the divide latency
+      double bnd = mk[4];  // the lane's fixed-point exponent G for layer 0's output:
+      for (int i = 0; i < E.obs_dim; ++i) {  // bound = max|b0| + sum_k max|W0[.][k]| |x_k|
         double v = raw[i];
         if (nrm.active) v = dmul(dsub(v, nrm.mean[i]), inv_den[i]);
-        if (l < OZP_G) xg[i * OZP_G + l] = act ? v : 0.0;
+        v = act ? v : 0.0;
+        bnd = fma(mk[i], fabs(v), bnd);
+        if (l < OZP_G) xg[i * OZP_G + l] = v;
       }
+      bnd = bnd * (1.0 + 0x1.0p-40);  // covers the rounding of layer 0's fma chains
+      if (l < OZP_G) gexp[lg * OZP_G + l] = 8 * S - 1 - bound_exp_bits(bnd);
     };
     bool act = valid && eps_this > 0 && A.max_iters > 0;
     if (act) observe_into_x0(true);
@@ -459,8 +467,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
           }
           double reward = 0.0;
           bool term = false, trunc = false;
+          OZ_MARK(11);  // env warp: head (output sum + tanh)
           const uint32_t f = env_step(E, s, action, reward, term, trunc, E.id == ENV_PENDULUM ? &sin_th : nullptr,
                                       E.id == ENV_PENDULUM ? &rpre : nullptr);
+          OZ_MARK(12);  // env warp: env_step
           if (f) {
             myfault = f;
           } else {
@@ -481,11 +491,12 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
           }
         }
         const bool next = myfault == 0 && eps_done < eps_this && it + 1 < A.max_iters;
+        OZ_MARK(13);  // env warp: bookkeeping
         observe_into_x0(next);
         act = next;
       }
       __syncwarp();
-      OZ_MARK(7);  // env warp: head + env + observe
+      OZ_MARK(14);  // env warp: observe
     }
     if (valid && crank == 0) {
       const long long ln = (long long)agent_local * A.e + j;
@@ -565,30 +576,32 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
             double xr[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) xr[k] = xg[k * OZP_G + le];
-            double bnd = mk[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) bnd = fma(mk[k], fabs(xr[k]), bnd);
-            bnd = bnd * (1.0 + 0x1.0p-40);
-            const int G = 8 * S - 1 - bound_exp_bits(bnd);
-            const double hscale = pow2(G);
+            const double hscale = pow2(gexp[g * OZP_G + le]);  // 2^G, G from the env warp
+            // z = W0 x + b0 as one fma chain from the bias (k = 0..3; W0 and x
+            // are zero past obs_dim)
             double z[8];
             const double* __restrict__ w0r = W0 + rg * 8;
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              const double2 b = *reinterpret_cast<const double2*>(b0 + rg * 8 + u);
+              z[u] = b.x;
+              z[u + 1] = b.y;
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
 #pragma unroll
               for (int u = 0; u < 8; u += 2) {
                 const double2 w = *reinterpret_cast<const double2*>(w0r + k * W1p + u);
-                z[u] = k == 0 ? w.x * xr[0] : fma(w.x, xr[k], z[u]);
-                z[u + 1] = k == 0 ? w.y * xr[0] : fma(w.y, xr[k], z[u + 1]);
+                z[u] = fma(w.x, xr[k], z[u]);
+                z[u + 1] = fma(w.y, xr[k], z[u + 1]);
               }
             }
             uint32_t qlo[8], qhi[8], hor = 0u;
 #pragma unroll
             for (int u = 0; u < 8; u += 2) {
-              const double2 b = *reinterpret_cast<const double2*>(b0 + rg * 8 + u);
 #pragma unroll
               for (int v = 0; v < 2; ++v) {
-                const double h = fmax(z[u + v] + (v ? b.y : b.x), 0.0);  // ReLU (NaN -> 0, as cwiseMax)
+                const double h = fmax(z[u + v], 0.0);  // ReLU (NaN -> 0, as cwiseMax)
                 const double t = fma(h, hscale, 0x1p52);
                 qlo[u + v] = (uint32_t)__double2loint(t);
                 qhi[u + v] = (uint32_t)__double2hiint(t);
@@ -630,18 +643,8 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
           // each lane's scale 2^-G, recomputed from x0 exactly as layer 0 did
           // (no cross-thread handoff between the layer-0 and epilogue threads)
           double h[4], sq[4];
-          {
-            const double* xg = x0 + g * 4 * OZP_G;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int e = half * 4 + q;
-              double bnd = mk[4];
-#pragma unroll
-              for (int k = 0; k < 4; ++k) bnd = fma(mk[k], fabs(xg[k * OZP_G + e]), bnd);
-              bnd = bnd * (1.0 + 0x1.0p-40);
-              sq[q] = rscale * pow2(-(8 * S - 1 - bound_exp_bits(bnd)));
-            }
-          }
+          for (int q = 0; q < 4; ++q) sq[q] = rscale * pow2(-gexp[g * OZP_G + half * 4 + q]);  // 2^(8(S-1) - F_r - G)
           long long hi[4], lo[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) hi[q] = lo[q] = 0;
@@ -664,9 +667,9 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
               const int e = half * 4 + q;
               double z = 0.0;
               for (int k = 0; k < W1; ++k) {
-                double a = W0[k] * xg[e];
-                for (int kk = 1; kk < 4; ++kk) a = fma(W0[kk * W1p + k], xg[kk * OZP_G + e], a);
-                z = fma(w1(k), fmax(a + b0[k], 0.0), z);
+                double a = b0[k];
+                for (int kk = 0; kk < 4; ++kk) a = fma(W0[kk * W1p + k], xg[kk * OZP_G + e], a);
+                z = fma(w1(k), fmax(a, 0.0), z);
               }
               h[q] = z;
             }
@@ -747,6 +750,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
   if (tid == 32 * OZP_CW) {
     atomicAdd(&g_oz_prof[6], prof[6]);
     atomicAdd(&g_oz_prof[7], prof[7]);
+    for (int i = 11; i < 15; ++i) atomicAdd(&g_oz_prof[i], prof[i]);
   }
   if (tid == 32 * (OZP_CW + 2)) {
     atomicAdd(&g_oz_prof[9], prof[9]);
@@ -892,7 +896,7 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.off_pout = off;
   off = al(off + 2 * 2 * C * (O + 1) * OZP_G * 8, 16);
   p.off_mask = off;
-  off = al(off + 36 * 4, 16);  // stamps bad0[2][8], bad1[2][8], alive[2], gdone[2]
+  off = al(off + 52 * 4, 16);  // stamps bad0[2][8], bad1[2][8], alive[2], gdone[2], gexp[2][8]
   p.off_bar = off;
   off = al(off + 8 * 10, 16);  // x0full[2], bfull[2], dfull[2], xbar[2][2]
   p.off_tslot = off;

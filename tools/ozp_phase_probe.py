@@ -16,7 +16,8 @@ import paper_2501_15129_b200 as evb  # noqa: E402
 
 ROLES = {"compute warps": {0: "prologue (once)", 1: "wait x0 (env)", 2: "layer 0 + B", 3: "wait MMA",
                            4: "epilogue", 5: "publish + barrier"},
-         "env warp 0": {7: "own work (env, observe, arming)", 6: "wait partial outputs"},
+         "env warp 0": {7: "reward pre-term, arming, loop top", 6: "wait partial outputs", 11: "head (sum + tanh)",
+                        12: "env_step", 13: "bookkeeping", 14: "observe + x0"},
          "MMA warp": {9: "wait B", 10: "issue"}}
 
 
