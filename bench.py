@@ -79,17 +79,18 @@ def cma_lazy_gap(d, mu, pop):
 NCU_TRAFFIC = {
     ("3", "f64"): (2230139136 + 68040960, "ncu r01_f64_v6: rollout_kernel<double,1,16,4,1>"),
     ("3", "tc"): (1104370432 + 10082304, "ncu r01_tc_v5: rollout_tc_kernel<2> (cta_group::2 pair)"),
-    ("3", "oz"): (1676240000 + 48855296, "ncu r02_ozp_full: rollout_ozp_kernel<6,2> (pre-split slices read once)"),
+    ("3", "oz"): (1673598000 + 48497664, "ncu r02_ozp_full_v2: rollout_ozp_kernel<6,2> (pre-split slices read once)"),
 }
 # int8 MMA work the oz team executes per env step and CTA (2 lane groups x
-# W1p/32 k-steps x S MMAs of M=128, N=8S, K=32): the tensor-pipe view of the
-# roofline beside the algorithmic one
+# W1p/32 k-steps x S MMAs of M=128, K=32, N = 8(S-i) rounded up to 16): the
+# tensor-pipe view of the roofline beside the algorithmic one
 OZ_S = 6
 
 
 def oz_int8_ops_per_cta_step(w1):
     w1p = -(-w1 // 32) * 32
-    return 2 * (w1p // 32) * OZ_S * 2 * 128 * (8 * OZ_S) * 32
+    n_sum = sum(-(-(8 * (OZ_S - i)) // 16) * 16 for i in range(OZ_S))
+    return 2 * (w1p // 32) * 2 * 128 * n_sum * 32
 
 
 def load_peaks():
