@@ -6,7 +6,7 @@ timed generation per cell (CUDA events around EsWorkflow.step, L2 not flushed:
 the generation is seconds long), cells whose projected time exceeds the budget
 are skipped and listed.  Writes JSON lines to stdout.
 
-  python tools/scale_sweep.py [--precision tc] [--budget-s 20] [--h 1000]
+  python tools/scale_sweep.py [--precision tc|oz|f64|f32] [--budget-s 20] [--h 1000]
 """
 import argparse
 import json
@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--precision", default="tc", choices=["f64", "f32", "tc"])
+    ap.add_argument("--precision", default="tc", choices=["f64", "f32", "tc", "oz"])
     ap.add_argument("--budget-s", type=float, default=20.0)
     ap.add_argument("--h", type=int, default=1000)
     ap.add_argument("--pops", default="256,1024,4096,16384,65536")
@@ -70,7 +70,7 @@ def main():
                                  "env_steps_per_s": steps / (ms / 1e3),
                                  "policy_tflops": steps * F / (roll_ms / 1e3) / 1e12,
                                  "wall_s": time.time() - t0})
-                    if args.precision == "tc" and peaks.get("bf16_tflops"):
+                    if args.precision in ("tc", "oz") and peaks.get("bf16_tflops"):
                         cell["frac_of_bf16_peak"] = cell["policy_tflops"] / peaks["bf16_tflops"]
                     rate[(w, e)] = steps / (ms / 1e3)
                 except Exception as ex:  # report and continue (e.g. Unsupported)
