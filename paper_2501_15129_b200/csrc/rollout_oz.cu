@@ -10,11 +10,12 @@
 //   * Each weight row r is a signed fixed-point integer W_int = trunc(W 2^F_r)
 //     with |W_int| < 2^(8S-1) (F_r from the row's largest |w|), cut into S
 //     bytes from the top: A_0 = W_int >> 8(S-1) (s8), A_i = byte i (u8).
-//     Each activation column (lane) e is h_int = trunc(h 2^G_e) < 2^(8S-1)
+//     Each activation column (lane) e is h_int = rn(h 2^G_e) <= 2^(8S-1)
 //     (h >= 0 after ReLU; G_e from a per-lane bound), bytes B_j (u8).
 //   * W_int h_int = sum_{i,j} A_i B_j 2^(8(2S-2-i-j)); the terms i + j < S are
 //     kept: D_t = sum_{i+j=t} A_i B_j, t < S, exact in int32 (|D_t| < S 2^24).
-//     z = 2^(8(S-1) - F_r - G_e) sum_t D_t 2^(8(S-1-t)), combined in fp64.
+//     z = 2^(8(S-1) - F_r - G_e) sum_t D_t 2^(8(S-1-t)), combined exactly in two
+//     44-bit integers and converted to fp64 once.
 //     S = 6 keeps ~47 bits of every operand: the policy output differs from
 //     fp64 arithmetic by ~1e-13 relative (fitness differences at the level of
 //     the fp64 path's own libm/ordering differences from the reference CPU).
@@ -26,7 +27,7 @@
 //     of M = 128, K = 32, N = 48, 48, 32, 32, 16, 16 (tools/umma_i8_bench.cu
 //     checks the scheme and times it: 48 MMAs in ~920 cycles).
 //   * TMEM (512 columns, one team CTA per SM): A slices at columns 512 - S W1p/4
-//     (written once by tcgen05.st from pre-split blocks), D_g at columns 8 S g.
+//     (written once by tcgen05.st from pre-split blocks), D_g at columns 8 (S+1) g.
 //   * Per env step (one CTA = 128 weight rows; C = W2/128 CTAs per agent) the
 //     16 lanes are two groups of 8 whose chains -- layer 0 (fp64, replicated)
 //     -> per-lane bound, fixed point, bytes -> B_g | MMAs (MMA warp) | epilogue:
@@ -68,8 +69,7 @@ struct OzPlan {
   int S;       // byte slices per operand
   int W1, W2;  // hidden widths
   int W1p;     // W1 rounded up to the MMA K step (32)
-  int off_B, off_W0, off_b0, off_mk, off_x0, off_sce, off_red, off_pout, off_mask, off_bar, off_tslot, off_rmax;
-  int pipe;   // layout version (1: the two-group pipelined kernel)
+  int off_B, off_W0, off_b0, off_mk, off_x0, off_red, off_pout, off_mask, off_bar, off_tslot, off_rmax;
   int used;   // bytes of the layout (zeroed by the prologue)
   int bytes;  // dynamic SMEM requested: >= OZ_MIN_SMEM
 };
@@ -877,7 +877,6 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   p.W1 = W1;
   p.W1p = W1p;
   p.W2 = W2;
-  p.pipe = 1;
   int off = 0;
   // rollout_ozp_kernel layout: per-group B buffers, x0, red, pout
   p.off_B = off;
@@ -890,7 +889,6 @@ bool plan_rollout_oz(const NetDesc& net, int obs_dim, int e, TcPlanOut* out) {
   off = al(off + 5 * 8, 16);
   p.off_x0 = off;
   off = al(off + 2 * 4 * OZP_G * 8, 16);
-  p.off_sce = off;
   p.off_red = off;
   off = al(off + 2 * 4 * O * OZP_G * 8, 16);
   p.off_pout = off;
