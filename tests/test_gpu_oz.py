@@ -148,3 +148,34 @@ def test_oz_config3_ranks_match_fp64_path(evb):
         assert np.allclose(fg, fr, rtol=RTOL_OZ, atol=0)
         assert np.array_equal(np.argsort(fg, kind="stable"), np.argsort(fr, kind="stable"))
         assert np.array_equal(g.mean(), r.mean())
+
+
+@pytest.mark.parametrize("kw", [
+    # Workflow::evaluate (m = 1 agent, 32 episodes -> two 16-lane teams) at the centre
+    dict(algo="openes", env="pendulum", fixed_horizon=True, pop=16, hidden=[64, 128], max_episode_steps=150,
+         fitness_episodes=8, vbn_samples=300),
+    # the noise-table ask (SRC_OPENES_TABLE materialised, then pre-split)
+    dict(algo="openes", env="pendulum", fixed_horizon=True, pop=16, hidden=[32, 128], max_episode_steps=100,
+         fitness_episodes=8, vbn_samples=300, openes_noise_table=True, openes_noise_table_size=1 << 18),
+    # CMA-ES: candidates from the device ask GEMM, no pre-split blocks (in-kernel slicing)
+    dict(algo="cmaes", env="pendulum", fixed_horizon=True, pop=16, hidden=[16, 128], max_episode_steps=100,
+         fitness_episodes=8, vbn_samples=300, cmaes_elites=8, cmaes_sigma0=0.1, cmaes_max_dim=4096),
+], ids=["evaluate", "noise-table", "cmaes"])
+def test_oz_other_callers_match_fp64(evb, kw):
+    """The oz team behind the workflow's other callers: per-generation fitness
+    within RTOL_OZ of the fp64 team from the same state, ranks identical, and
+    Workflow::evaluate at the centre within RTOL_OZ."""
+    kwc = {k: (tuple(v) if k == "hidden" else v) for k, v in kw.items()}
+    a = evb.EsWorkflow(evb.EsConfig(precision="f64", **kwc)).init((21, 22))
+    b = evb.EsWorkflow(evb.EsConfig(precision="oz", **kwc)).init((21, 22))
+    for _ in range(2):
+        a.step()
+        b.step()
+        fa, fb = a.fitness(), b.fitness()
+        assert np.allclose(fb, fa, rtol=RTOL_OZ, atol=1e-12)
+        assert np.array_equal(np.argsort(fa, kind="stable"), np.argsort(fb, kind="stable"))
+    b.set_mean(a.mean())
+    ma, sa = a.evaluate(32, (5, 6))
+    mb, sb = b.evaluate(32, (5, 6))
+    assert mb == pytest.approx(ma, rel=RTOL_OZ)
+    assert sb == pytest.approx(sa, rel=1e-6, abs=1e-9)
