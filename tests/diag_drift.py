@@ -8,7 +8,7 @@ import oracle_ffi as oracle
 import paper_2501_15129_b200 as evb
 
 def run(kw, gens):
-    okw = dict(kw); okw["hidden"] = list(kw["hidden"]); okw["workers"] = 0
+    okw = {k: v for k, v in kw.items() if k != "precision"}; okw["hidden"] = list(kw["hidden"]); okw["workers"] = 0
     o = oracle.OracleEs(oracle.es_config(**okw)); g = evb.EsWorkflow(evb.EsConfig(**kw))
     k = oracle.key_from_seed(5); o.init(k); g.init(k)
     for gen in range(gens):
@@ -28,3 +28,9 @@ run(dict(algo="openes", env="pendulum", fixed_horizon=True, pop=64, hidden=(64, 
          max_episode_steps=200, vbn_samples=2000), 8)
 run(dict(algo="ars", env="pendulum", fixed_horizon=True, pop=64, hidden=(16,),
          max_episode_steps=100), 8)
+# the oz team (int8-sliced tensor cores) and the fp64 DMMA team on the same
+# 16-env OpenES workflow: per-generation drift from the CPU restatement
+for prec in ("f64", "oz"):
+    print("precision", prec)
+    run(dict(algo="openes", env="pendulum", fixed_horizon=True, pop=256, hidden=(128, 256),
+             max_episode_steps=200, vbn_samples=2000, fitness_episodes=16, precision=prec), 8)
