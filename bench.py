@@ -362,7 +362,12 @@ def main():
     agents_local = es.shard_ranges()[1] - es.shard_ranges()[0] if world > 1 else pop
     flops_launch = agents_local * e * H * F
     extra = {}
-    if args.precision == "oz":
+    # the team that actually runs: oz covers obs -> W1 -> W2 -> O with W1 <= 256 and
+    # >= 5 envs per individual, other shapes run the fp64 teams (bit-identical to f64)
+    eff_prec = args.precision
+    if eff_prec == "oz" and not (len(cfg.hidden) == 2 and e >= 5 and cfg.hidden[0] <= 256):
+        eff_prec = "f64"
+    if eff_prec == "oz":
         # config 3 is tensor-core bound, roof = the dense tensor
         # peak; achieved counts the MLP's algorithmic flops.  The kernel is bound
         # by the serial 200-step chain (one CTA per SM, TMEM-limited), so two more
@@ -384,12 +389,12 @@ def main():
                                           "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16 "
                                                          "on B200; derived, not measured)",
                                           "frac": (ex_tops / int8_peak) if (ex_tops and int8_peak) else None}}
-    elif args.precision == "f64":
+    elif eff_prec == "f64":
         peak = evb.measure_fp64_peak()
         bound, unit, peak_src = "fp64", "TFLOP/s", (
             "measured live: DFMA-bound microkernel (evorl_measure_fp64_peak); "
             "MEASURED_PEAKS.json has no FP64 figure")
-    elif args.precision == "tc":
+    elif eff_prec == "tc":
         # the dense W2 x W1 layer runs on tcgen05 (kind::f16, 3 passes); the
         # roof is the dense 16-bit tensor peak of MEASURED_PEAKS.json (fp16 and
         # bf16 run at the same rate), counting only the useful (1-pass) flops
@@ -409,12 +414,14 @@ def main():
         fe["frac"] = (achieved / fe["peak"]) if (achieved and fe["peak"]) else None
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, **extra,
                 "frac": (achieved / peak) if (achieved and peak) else None,
-"traffic": NCU_TRAFFIC.get((args.config, args.precision), (None,))[0],
-                "traffic_source": NCU_TRAFFIC.get((args.config, args.precision), (None, None))[1],
+                "traffic": NCU_TRAFFIC.get((args.config, eff_prec), (None,))[0],
+                "traffic_source": NCU_TRAFFIC.get((args.config, eff_prec), (None, None))[1],
                 "kernel": {"tc": "rollout_tc_kernel (tcgen05 hidden layer, fused obs-norm/MLP/env/return)",
                            "oz": "rollout_ozp_kernel (int8-sliced tcgen05 hidden layer, two pipelined lane "
                                  "groups, fused obs-norm/MLP/env/return)"}.get(
-                               args.precision, "rollout_kernel (fused obs-norm/MLP/env/return)"),
+                               eff_prec, "fp64 rollout team (cluster DMMA or warp-per-lane; fused "
+                                         "obs-norm/MLP/env/return)"),
+                "team_precision": eff_prec,
                 "algorithmic_flops_per_launch": flops_launch,
                 "flops_per_env_step": F, "peak_source": peak_src,
                 "rollout_ms_per_launch": roll_ms, "rollout_share_of_step":
@@ -469,7 +476,8 @@ def main():
                        "params": params_dim, "parallelism": f"population-sharded dp{world}",
                        "l2": "flushed (256 MiB write) between timed generations",
                        "policy_precision": args.precision,
-                       "parity": parity.get(args.precision, "returns within fp32 tolerance"),
+                       "policy_team": eff_prec,
+                       "parity": parity.get(eff_prec, "returns within fp32 tolerance"),
                        **({"eig_every": getattr(args, "cma_gap", None),
                            "timed_window": "whole lazy periods (one eigendecomposition per period)"}
                           if kw.get("algo") == "cmaes" else {}),
