@@ -190,10 +190,9 @@ int run(int reps) {
 // columns [8i, 8i + N_i) with N_i = 8(S-i) rounded up to 16 and reads the data
 // blocks B_0.. from block 0 (no zero blocks); the rounding spills into column
 // block S (ignored).  Checks D_t = sum_{i+j=t} A_i B_j for t < S and times it.
-template <int S>
+template <int S, int G>
 __global__ void bench_exact(const uint8_t* A, const uint8_t* B, int* out, long long* cyc, int reps) {
-  constexpr int G = 8;                 // lanes per group
-  constexpr int R = G * (S + 1);       // data blocks + one spill block
+  constexpr int R = (G * (S + 1) + 7) / 8 * 8;  // data blocks + spill, whole 8-row core groups
   constexpr uint32_t LBO = (R / 8) * 128;
   __shared__ __align__(1024) uint8_t Bs[R * K];
   __shared__ uint64_t bar;
@@ -240,9 +239,9 @@ __global__ void bench_exact(const uint8_t* A, const uint8_t* B, int* out, long l
       for (int ks = 0; ks < K / 32; ++ks)
 #pragma unroll
         for (int i = 0; i < S; ++i) {
-          const int n = ((8 * (S - i)) + 15) / 16 * 16;
+          const int n = ((G * (S - i)) + 15) / 16 * 16;
           const uint64_t bd = desc(su32(Bs) + ks * 2 * LBO, LBO, 128);
-          mma_ts(tmem + 8 * i, tmem + colA + 64 * i + ks * 8, bd, idesc_i8(M, n, i == 0),
+          mma_ts(tmem + G * i, tmem + colA + 64 * i + ks * 8, bd, idesc_i8(M, n, i == 0),
                  (ks > 0 || i > 0) ? 1u : 0u);
         }
       asm volatile(
@@ -267,13 +266,14 @@ __global__ void bench_exact(const uint8_t* A, const uint8_t* B, int* out, long l
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp < 4) {
     const int row = warp * 32 + lane;
-    for (int c0 = 0; c0 < G * S; c0 += 8) {
+    for (int c0 = 0; c0 < (G * S + 7) / 8 * 8; c0 += 8) {
       uint32_t v[8];
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                    : "r"(tmem + ((uint32_t)(warp * 32) << 16) + c0));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      for (int q = 0; q < 8; ++q) out[row * (G * S) + c0 + q] = (int)v[q];
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q < G * S) out[row * (G * S) + c0 + q] = (int)v[q];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -281,9 +281,9 @@ __global__ void bench_exact(const uint8_t* A, const uint8_t* B, int* out, long l
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int S>
+template <int S, int G>
 int run_exact(int reps) {
-  constexpr int G = 8, N = G * S;
+  constexpr int N = G * S;
   std::vector<uint8_t> A((size_t)S * M * K), B((size_t)S * NL * K);
   srand(77 + S);
   for (auto& x : A) x = (uint8_t)(rand() & 0xFF);
@@ -297,7 +297,7 @@ int run_exact(int reps) {
   cudaMalloc(&dc, 16);
   cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
-  bench_exact<S><<<1, 128>>>(dA, dB, dO, dc, reps);
+  bench_exact<S, G><<<1, 128>>>(dA, dB, dO, dc, reps);
   std::vector<int> O((size_t)M * N);
   long long cyc[2];
   cudaError_t e = cudaMemcpy(O.data(), dO, sizeof(int) * M * N, cudaMemcpyDeviceToHost);
@@ -321,8 +321,8 @@ int run_exact(int reps) {
           ++bad;
         }
       }
-  printf("exact-N S=%d (8-lane group): %d MMAs issue %lld cyc, complete %lld cyc -> %.1f cyc/MMA; mismatches %lld\n", S,
-         8 * S, cyc[0], cyc[1], (double)cyc[1] / (8 * S), bad);
+  printf("exact-N S=%d (%d-lane group): %d MMAs issue %lld cyc, complete %lld cyc -> %.1f cyc/MMA; mismatches %lld\n", S,
+         G, 8 * S, cyc[0], cyc[1], (double)cyc[1] / (8 * S), bad);
   return bad != 0;
 }
 
@@ -331,6 +331,7 @@ int main() {
   rc |= run<4>(8);
   rc |= run<5>(8);
   rc |= run<6>(8);
-  rc |= run_exact<6>(8);
+  rc |= run_exact<6, 8>(8);
+  rc |= run_exact<6, 4>(8);
   return rc;
 }
