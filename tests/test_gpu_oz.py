@@ -45,6 +45,7 @@ SHAPES = [
     ("pendulum", [256, 256], 3, 5, 7, True, 120),
     ("pendulum", [128, 256], 2, 40, 40, True, 80),
     ("cartpole", [64, 128], 6, 16, 16, False, 200),
+    ("pendulum", [128, 1024], 2, 16, 16, True, 60),   # cluster of 8 CTAs
 ]
 
 
