@@ -7,7 +7,7 @@
 // normaliser, layer 0, the output layer and the head stay fp64 on the CUDA
 // cores in the fp64 team's operation order.  What changes is the dense
 // W2 x W1 layer (proj/src/net.cpp:96, z = W h + b):
-//   * Each weight row r is a signed fixed-point integer W_int = trunc(W 2^F_r)
+//   * Each weight row r is a signed fixed-point integer W_int = floor(W 2^F_r)
 //     with |W_int| < 2^(8S-1) (F_r from the row's largest |w|), cut into S
 //     bytes from the top: A_0 = W_int >> 8(S-1) (s8), A_i = byte i (u8).
 //     Each activation column (lane) e is h_int = rn(h 2^G_e) <= 2^(8S-1)
@@ -163,6 +163,36 @@ EVB_DEV int bound_exp_bits(double v) {
 }
 // 2^g for |g| <= 1000 (a normal double), built from the exponent field
 EVB_DEV double pow2(int g) { return __hiloint2double((g + 1023) << 20, 0); }
+// The S bytes of 32 consecutive weights of one row, W_int = floor(w 2^F) in
+// offset binary: t = w 2^F + 2^52 + 2^(8S-1) (rounded toward zero) carries
+// U = W_int + 2^(8S-1) in [0, 2^(8S)) in its mantissa, so the bytes are byte
+// permutes of its two words (no float->int conversion, no 64-bit shifts); the
+// top byte of U minus 128 is the signed A_0 (an XOR with 0x80).  Non-finite
+// weights slice as 0 (their rows take the fp64 path).
+template <int S>
+EVB_DEV void oz_slice32(const double* w, double wscale, uint32_t (&out)[S][8]) {
+  static_assert(S <= 6, "U must fit the 52-bit mantissa with room for the offset");
+  const double off = 0x1p52 + (double)(1ull << (8 * S - 1));
+  uint32_t lo[32], hi[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const double t = __fma_rz(isfinite(w[q]) ? w[q] : 0.0, wscale, off);
+    lo[q] = (uint32_t)__double2loint(t);
+    hi[q] = (uint32_t)__double2hiint(t);
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    const int Pb = 8 * (S - 1 - i);
+    const bool H = Pb >= 32;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t v = gather_byte(H ? hi[4 * u] : lo[4 * u], H ? hi[4 * u + 1] : lo[4 * u + 1],
+                                     H ? hi[4 * u + 2] : lo[4 * u + 2], H ? hi[4 * u + 3] : lo[4 * u + 3],
+                                     (Pb & 31) >> 3);
+      out[i][u] = i == 0 ? v ^ 0x80808080u : v;
+    }
+  }
+}
 // atomic max of a non-negative double (bit patterns order like the values)
 EVB_DEV void smem_max_nonneg(double* p, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
@@ -308,24 +338,14 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
     Fr = 8 * S - 1 - bound_exp(rm);  // |W_int| < 2^(8S-1)
     const double wscale = ldexp(1.0, Fr);
     for (int c = half; c < W1p / 32; c += 2) {
-      long long wi[32];
+      double w[32];
 #pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const double w = w1(c * 32 + q);
-        wi[q] = isfinite(w) ? __double2ll_rz(w * wscale) : 0ll;
-      }
+      for (int q = 0; q < 32; ++q) w[q] = w1(c * 32 + q);
+      uint32_t sl[S][8];
+      oz_slice32<S>(w, wscale, sl);
 #pragma unroll
-      for (int i = 0; i < S; ++i) {
-        uint32_t packed[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          uint32_t word = 0u;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) word |= (uint32_t)((wi[4 * u + b] >> (8 * (S - 1 - i))) & 0xFF) << (8 * b);
-          packed[u] = word;
-        }
-        oz_st8(tmem + ((uint32_t)(quad * 32) << 16) + colA + (uint32_t)(i * (W1p / 4) + c * 8), packed);
-      }
+      for (int i = 0; i < S; ++i)
+        oz_st8(tmem + ((uint32_t)(quad * 32) << 16) + colA + (uint32_t)(i * (W1p / 4) + c * 8), sl[i]);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     if (slow_cta)
@@ -805,26 +825,19 @@ __global__ void k_oz_split(const double* __restrict__ cand, long long d, long lo
   const double wscale = ldexp(1.0, Fr);
   unsigned char* blk = blocks + ac * block_bytes;
   for (int c = 0; c < W1p / 32; ++c) {
-    long long wi[32];
+    double w[32];
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
       const int k = c * 32 + q;
-      const double w = (ok && k < W1) ? wr[(long long)k * W2] : 0.0;
-      wi[q] = isfinite(w) ? __double2ll_rz(w * wscale) : 0ll;
+      w[q] = (ok && k < W1) ? wr[(long long)k * W2] : 0.0;
     }
+    uint32_t sl[S][8];
+    oz_slice32<S>(w, wscale, sl);
 #pragma unroll
     for (int i = 0; i < S; ++i) {
-      uint32_t packed[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        uint32_t word = 0u;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) word |= (uint32_t)((wi[4 * u + b] >> (8 * (S - 1 - i))) & 0xFF) << (8 * b);
-        packed[u] = word;
-      }
       uint4* dst = reinterpret_cast<uint4*>(blk + (((size_t)i * (W1p / 32) + c) * OZ_M + row) * 32);
-      dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      dst[0] = make_uint4(sl[i][0], sl[i][1], sl[i][2], sl[i][3]);
+      dst[1] = make_uint4(sl[i][4], sl[i][5], sl[i][6], sl[i][7]);
     }
   }
   reinterpret_cast<int*>(blk + (size_t)S * W1p * OZ_M)[row] = (Fr & 0xFFFF) | ((ok && !fin) ? (1 << 16) : 0);
