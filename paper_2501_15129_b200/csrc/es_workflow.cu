@@ -191,6 +191,12 @@ struct evorl_es {
   std::vector<long long> h_offsets;
   double* d_tell_part = nullptr;  // OpenES tell: per-row-chunk partial contractions
   long long tell_part_cap = 0;
+  // OpenES: this generation's sampled noise rows (base x d), written by the
+  // ask when one rank materialises every row, read by the tell instead of
+  // regenerating them (valid between phase_rollout and phase_tell)
+  double* d_eps_rows = nullptr;
+  bool eps_rows_valid = false;
+  bool eps_rows_failed = false;
   cudaStream_t stream = nullptr;
   // WorkflowState (proj/include/evorl/workflow.hpp:31-36)
   DKey rng{};
@@ -284,7 +290,7 @@ static void free_all(evorl_es* s) {
                   s->d_ep_returns, s->d_lane_stats, s->d_agent_stats, s->d_lane_steps, s->d_rank,
                   s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
                   s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand,
-                  s->d_cand_f32, s->d_tell_part, s->d_table, s->d_offsets, s->d_tc_blocks};
+                  s->d_cand_f32, s->d_tell_part, s->d_table, s->d_offsets, s->d_tc_blocks, s->d_eps_rows};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
@@ -681,6 +687,26 @@ static int check_ask(const evorl_es* s) {  // the ask-side argument checks
   return EVORL_OK;
 }
 
+// The buffer the ask keeps this generation's OpenES noise rows in, or null
+// (regenerated by the tell): only when this rank materialises every sampled
+// row (unsharded), regenerated-noise mode, under a 4 GiB cap
+// (EVORL_EPS_ROWS_CAP_BYTES overrides it; 0 disables -- used by the tests).
+static double* eps_rows_buffer(evorl_es* s) {
+  if (s->cfg.algo != EVORL_ALGO_OPENES || s->d_table || s->eps_rows_failed) return nullptr;
+  if (s->a0 != 0 || s->a1 != s->cfg.pop) return nullptr;
+  static const double kCap =
+      getenv("EVORL_EPS_ROWS_CAP_BYTES") ? atof(getenv("EVORL_EPS_ROWS_CAP_BYTES")) : 4.0 * (1ull << 30);
+  const long long rows = s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop;
+  const double bytes = (double)rows * (double)s->d * sizeof(double);
+  if (bytes <= 0 || bytes > kCap) return nullptr;
+  if (!s->d_eps_rows && cudaMalloc((void**)&s->d_eps_rows, (size_t)bytes) != cudaSuccess) {
+    cudaGetLastError();  // out of memory: keep regenerating
+    s->d_eps_rows = nullptr;
+    s->eps_rows_failed = true;
+  }
+  return s->d_eps_rows;
+}
+
 static RolloutArgs rollout_args(const evorl_es* s) {
   RolloutArgs a{};
   a.env = s->env;
@@ -793,6 +819,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
   s->ask_key = fold_in(s->step_key, 0);      // proj/src/workflow_es.cpp:94
   s->rollout_key = fold_in(s->step_key, 1);  // proj/src/workflow_es.cpp:125
   if (s->d_table) CK(table_offsets(s, s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop));
+  s->eps_rows_valid = false;
   CK(cudaEventRecord(s->ev_s0, s->stream));
   CK(cudaMemsetAsync(s->d_steps, 0, sizeof(unsigned long long), s->stream));
   CK(cudaMemsetAsync(s->d_fault, 0xFF, sizeof(unsigned long long), s->stream));
@@ -813,7 +840,9 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
   } else if (s->warp_path) {
     // small policy: materialise the shard's candidates (fully parallel ask),
     // then one warp per lane with the weights resident in shared memory
-    CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream));
+    double* er = a.par.src == SRC_OPENES ? eps_rows_buffer(s) : nullptr;
+    CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream, er));
+    s->eps_rows_valid = er != nullptr;
     count_launch();
     a.par.src = SRC_EXPLICIT;
     a.par.params = s->d_cand;
@@ -822,6 +851,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
   } else {
     // team path: materialise the shard's candidates (chunks of cand_cap
     // agents), then roll each chunk out
+    double* er = a.par.src == SRC_OPENES ? eps_rows_buffer(s) : nullptr;
     for (int c0 = s->a0; c0 < s->a1; c0 += s->cand_cap) {
       const int c1 = std::min(s->a1, c0 + s->cand_cap);
       RolloutArgs ac = a;
@@ -831,7 +861,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
       ac.lane_steps = s->d_lane_steps + (long long)c0 * s->e;
       ac.lane_stats = s->d_lane_stats + (long long)c0 * s->e * 9;
       if (s->d_cand_f32) {
-        CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream));
+        CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream, er));
         ac.par.src = SRC_EXPLICIT_F32;
         ac.par.params_f32 = s->d_cand_f32;
         if (s->d_tc_blocks) {  // the tc team's layer-1 weights, pre-split (bulk-copied by its prologue)
@@ -841,7 +871,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
           ac.tc_block_bytes = tc_block_bytes(s->plan.tcp);
         }
       } else {
-        CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream));
+        CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream, er));
         ac.par.src = SRC_EXPLICIT;
         ac.par.params = s->d_cand;
         if (s->d_tc_blocks) {  // the oz team's layer-1 weights, pre-split into fixed-point byte slices
@@ -856,6 +886,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
       CK(launch_rollout(ac, s->cfg.precision, s->stream));
       count_launch();
     }
+    s->eps_rows_valid = er != nullptr && s->a1 > s->a0;
   }
   CK(cudaEventRecord(s->ev_r1, s->stream));
   CK(run_fitness(a.ep_returns, s->count, a.n_agents, s->a0, s->d_fitness, a.lane_steps, s->e, s->d_steps,
@@ -915,6 +946,8 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       t.adam_bc_len = s->adam_bc_len;
       t.table = s->d_table;
       t.offsets = s->d_offsets;
+      t.eps_rows = s->eps_rows_valid ? s->d_eps_rows : nullptr;
+      s->eps_rows_valid = false;
       {
         const long long need = (long long)openes_tell_chunks(t.base, s->d) * (s->p1 - s->p0);
         if (need > s->tell_part_cap) {

@@ -375,6 +375,43 @@ __global__ void __launch_bounds__(TELL_T) k_openes_tell_partial(const OpenEsTell
     if (pbase + v < a.p1) out[v] = acc[v];
 }
 
+// The same contraction with the noise rows kept by the ask
+// (run_materialize's eps_out): one coordinate per thread, so every row is a
+// coalesced read.  Each coordinate accumulates the rows of its chunk in the
+// same order as k_openes_tell_partial, so the partials are bit-identical.
+__global__ void __launch_bounds__(TELL_T) k_openes_tell_rows(const OpenEsTellArgs a, int chunk_rows) {
+  __shared__ double wsh[1024];
+  const long long p = a.p0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int rows = a.mirrored ? a.base : a.n;
+  const int r0 = blockIdx.y * chunk_rows, r1 = min(rows, r0 + chunk_rows);
+  double acc = 0.0;
+  for (int i0 = r0; i0 < r1; i0 += 1024) {
+    const int lim = min(1024, r1 - i0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < lim; q += blockDim.x) {
+      const int i = i0 + q;
+      wsh[q] = a.mirrored ? dsub(a.shaped[i], a.shaped[i + a.base]) : a.shaped[i];
+    }
+    __syncthreads();
+    if (p < a.p1) {
+      const double* col = a.eps_rows + (long long)i0 * a.d + p;
+      int q = 0;
+      for (; q + 4 <= lim; q += 4) {  // four rows' loads in flight
+        const double e0 = __ldcs(col), e1 = __ldcs(col + a.d), e2 = __ldcs(col + 2 * a.d),
+                     e3 = __ldcs(col + 3 * a.d);
+        acc = fma(e0, wsh[q], acc);
+        acc = fma(e1, wsh[q + 1], acc);
+        acc = fma(e2, wsh[q + 2], acc);
+        acc = fma(e3, wsh[q + 3], acc);
+        col += 4 * a.d;
+      }
+      for (; q < lim; ++q, col += a.d) acc = fma(__ldcs(col), wsh[q], acc);
+    }
+  }
+  if (p >= a.p1) return;
+  a.partial[(long long)blockIdx.y * (a.p1 - a.p0) + (p - a.p0)] = acc;
+}
+
 // g_p = sum over chunks (fixed order) / (n sigma), then adam_step.
 __global__ void k_openes_adam(const OpenEsTellArgs a, int chunks) {
   const long long p = a.p0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -421,9 +458,14 @@ cudaError_t run_openes_tell(const OpenEsTellArgs& a, cudaStream_t s) {
   const int rows = a.mirrored ? a.base : a.n;
   const int chunks = openes_tell_chunks(rows, a.d);
   const int chunk_rows = (rows + chunks - 1) / chunks;
-  const long long threads = (span + TELL_V - 1) / TELL_V;
-  dim3 grid((unsigned)((threads + TELL_T - 1) / TELL_T), (unsigned)chunks);
-  k_openes_tell_partial<<<grid, TELL_T, 0, s>>>(a, chunk_rows);
+  if (a.eps_rows && !a.table) {
+    dim3 grid((unsigned)((span + TELL_T - 1) / TELL_T), (unsigned)chunks);
+    k_openes_tell_rows<<<grid, TELL_T, 0, s>>>(a, chunk_rows);
+  } else {
+    const long long threads = (span + TELL_V - 1) / TELL_V;
+    dim3 grid((unsigned)((threads + TELL_T - 1) / TELL_T), (unsigned)chunks);
+    k_openes_tell_partial<<<grid, TELL_T, 0, s>>>(a, chunk_rows);
+  }
   k_openes_adam<<<blocks_for(span, 256), 256, 0, s>>>(a, chunks);
   EVB_CHECK_LAUNCH();
 }

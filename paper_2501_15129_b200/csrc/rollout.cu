@@ -90,13 +90,24 @@ __global__ void k_materialize_f32(const ParamDesc P, long long d, int a0, int a1
 // (t odd) half of Box-Muller block t >> 1; thread b computes block b once and
 // writes both entries to every agent using them (row, and row + base when
 // mirrored, negated) -- the same value param_value regenerates.
+// eps_out (optional): the noise entries themselves, eps_out[t], kept for the
+// tell of the same generation (run_openes_tell reads them instead of
+// regenerating the Box-Muller pairs).
 template <typename T>
 __global__ void k_materialize_openes(const ParamDesc P, long long d, int a0, int a1, long long t0, long long t1,
-                                     T* out) {
+                                     T* out, double* eps_out) {
   const long long b = (t0 >> 1) + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (2 * b >= t1) return;
   double c, sn;
   normal_pair(P.ask_key, (uint64_t)b, c, sn);
+  if (eps_out) {
+    if (2 * b >= t0 && 2 * b + 1 < t1)
+      reinterpret_cast<double2*>(eps_out)[b] = make_double2(c, sn);
+    else if (2 * b >= t0)
+      eps_out[2 * b] = c;
+    else
+      eps_out[2 * b + 1] = sn;
+  }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const long long t = 2 * b + h;
@@ -138,7 +149,8 @@ static void openes_rows(const ParamDesc& par, int a0, int a1, long long& r0, lon
 }
 
 template <typename T>
-static cudaError_t materialize(const ParamDesc& par, long long d, int a0, int a1, T* out, cudaStream_t stream) {
+static cudaError_t materialize(const ParamDesc& par, long long d, int a0, int a1, T* out, cudaStream_t stream,
+                               double* eps_out = nullptr) {
   const long long n = (long long)(a1 - a0) * d;
   if (n <= 0) return cudaSuccess;
   if (par.src == SRC_OPENES) {
@@ -146,7 +158,8 @@ static cudaError_t materialize(const ParamDesc& par, long long d, int a0, int a1
     openes_rows(par, a0, a1, r0, r1);
     const long long t0 = r0 * d, t1 = r1 * d;
     const long long blocks = ((t1 + 1) >> 1) - (t0 >> 1);
-    k_materialize_openes<T><<<(unsigned)((blocks + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1, out);
+    k_materialize_openes<T><<<(unsigned)((blocks + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1, out,
+                                                                                     eps_out);
     return cudaGetLastError();
   }
   if constexpr (sizeof(T) == 4) {
@@ -158,12 +171,14 @@ static cudaError_t materialize(const ParamDesc& par, long long d, int a0, int a1
 }
 
 cudaError_t run_materialize_f32(const ParamDesc& par, long long d, int a0, int a1, float* out,
-                                cudaStream_t stream) {
-  return materialize(par, d, a0, a1, out, stream);
+                                cudaStream_t stream, double* eps_out) {
+  if (eps_out && par.src != SRC_OPENES) return cudaErrorInvalidValue;
+  return materialize(par, d, a0, a1, out, stream, eps_out);
 }
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
-                            cudaStream_t stream) {
-  return materialize(par, d, a0, a1, out, stream);
+                            cudaStream_t stream, double* eps_out) {
+  if (eps_out && par.src != SRC_OPENES) return cudaErrorInvalidValue;
+  return materialize(par, d, a0, a1, out, stream, eps_out);
 }
 
 template <typename T, int N>

@@ -175,14 +175,16 @@ bool plan_rollout_warp(const NetDesc& net, int obs_dim, int e, int precision, Wa
 cudaError_t launch_rollout_warp(const RolloutArgs& a, const WarpPlanOut& plan, int precision,
                                 cudaStream_t stream);
 // Materialise candidates [a0, a1) (row-major, d each) from a ParamDesc.
+// SRC_OPENES only: eps_out (optional) receives the sampled noise entries of
+// the rows these agents use, at their stream index row * d + p.
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
-                            cudaStream_t stream);
+                            cudaStream_t stream, double* eps_out = nullptr);
 
 // Materialise candidates [a0, a1) as fp32 (the value the fp32 policy paths
 // round each fp64 candidate parameter to).  OpenES: one Box-Muller pair per
 // thread, shared by the mirrored agents.
 cudaError_t run_materialize_f32(const ParamDesc& par, long long d, int a0, int a1, float* out,
-                                cudaStream_t stream);
+                                cudaStream_t stream, double* eps_out = nullptr);
 
 // Tensor-core rollout (rollout_tc.cu, precision EVORL_PREC_TC): obs -> W1 -> W2 -> O
 // policies with W2 a multiple of 128; the W2 x W1 layer runs on tcgen05.

@@ -480,6 +480,34 @@ def test_chunked_materialised_ask_is_identical(evb):
     assert np.array_equal(outs[0], outs[1])
 
 
+def test_tell_from_kept_noise_rows_is_identical(evb):
+    """The OpenES tell reads the noise rows the ask kept (one rank
+    materialising every row) instead of regenerating them: the updated mean is
+    bit-identical to the regenerating tell (EVORL_EPS_ROWS_CAP_BYTES=0 in a
+    child process) on the warp, fp64-team, tc-team and oz-team paths,
+    mirrored or not, and with a chunked materialised ask."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, paper_2501_15129_b200 as evb\n"
+            "for hidden, prec, mir in [((8,), 'f64', True), ((32, 32), 'f64', False), ((32, 32), 'f64', True),\n"
+            "                          ((128, 128), 'tc', True), ((256, 256), 'oz', True), ((256, 256), 'oz', False)]:\n"
+            "    kw = dict(algo='openes', env='pendulum', fixed_horizon=True, pop=26, hidden=hidden,\n"
+            "              max_episode_steps=30, fitness_episodes=8, precision=prec, openes_mirrored=mir)\n"
+            "    g = evb.EsWorkflow(evb.EsConfig(**kw)).init((7, 8))\n"
+            "    for _ in range(3): g.step()\n"
+            "    print('MEAN', g.mean().tobytes().hex())\n")
+    outs = []
+    for env_kv in ({}, {"EVORL_EPS_ROWS_CAP_BYTES": "0"}, {"EVORL_CAND_CAP_BYTES": str(5 * 67073 * 8)}):
+        env = dict(os.environ)
+        env.update(env_kv)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        outs.append([x.split()[1] for x in r.stdout.decode().splitlines() if x.startswith("MEAN ")])
+    assert len(outs[0]) == 6
+    assert outs[0] == outs[1]
+    assert outs[0] == outs[2]  # (the oz rows in 5-agent chunks)
+
+
 @pytest.mark.parametrize("mirrored", [True, False])
 def test_openes_noise_table_generations_match_oracle(oracle, evb, mirrored):
     """OpenES noise-table mode (proj/src/ec.cpp:50-86): the table (normals of
