@@ -397,7 +397,11 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
     NormParams nrm;
     nrm.active = 0;
     if (A.norm != nullptr) nrm = *A.norm;
+    // (every loop over the obs / output dimension is unrolled to its compile-time
+    // bound with a predicate, so these arrays stay in registers: a dynamic
+    // index would put them in local memory on the env chain's critical path)
     double inv_den[4];
+#pragma unroll
     for (int i = 0; i < 4; ++i) inv_den[i] = nrm.active ? 1.0 / nrm.den[i] : 1.0;
     double* xg = x0 + lg * 4 * OZP_G;
     double sin_th = 0.0;
@@ -407,14 +411,18 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
       sin_th = raw[1];
       if (act && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
         if (wc == 0.0) {
-          for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (i >= E.obs_dim) break;
             wmean[i] = raw[i];
             wm2[i] = 0.0;
           }
           wc = 1.0;
         } else {
           wc = dadd(wc, 1.0);
-          for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (i >= E.obs_dim) break;
             const double delta = dsub(raw[i], wmean[i]);
             wmean[i] = dadd(wmean[i], ddiv(delta, wc));
             wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
@@ -424,7 +432,9 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
       // (o - mean) * (1 / den): within an ulp of the fp64 team's IEEE division,
       // far below this team's ~1e-13 policy tolerance, and off the divide latency
       double bnd = mk[4];  // the lane's fixed-point exponent G for layer 0's output:
-      for (int i = 0; i < E.obs_dim; ++i) {  // bound = max|b0| + sum_k max|W0[.][k]| |x_k|
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // bound = max|b0| + sum_k max|W0[.][k]| |x_k|
+        if (i >= E.obs_dim) break;
         double v = raw[i];
         if (nrm.active) v = dmul(dsub(v, nrm.mean[i]), inv_den[i]);
         v = act ? v : 0.0;
@@ -462,8 +472,11 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
         bool nonfinite_out = false;
         int bad_layer = 3;
         for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pg[c * OE1g + OEg + l]);
-        for (int o = 0; o < O; ++o) {
+#pragma unroll
+        for (int o = 0; o < OZ_MAXO; ++o) {
+          if (o >= O) break;
           double v = pg[o * OZP_G + l];
+#pragma unroll
           for (int c = 1; c < C; ++c) v += pg[c * OE1g + o * OZP_G + l];
           v = v + b2[o];
           z[o] = v;
@@ -477,8 +490,13 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
           double action;
           if (N.head == HEAD_CATEGORICAL) {
             int arg = 0;
-            for (int o = 1; o < O; ++o)
-              if (z[o] > z[arg]) arg = o;  // maxCoeff: first maximum
+            double best = z[0];
+#pragma unroll
+            for (int o = 1; o < OZ_MAXO; ++o)
+              if (o < O && z[o] > best) {  // maxCoeff: first maximum
+                best = z[o];
+                arg = o;
+              }
             action = (double)arg;
           } else if (N.head == HEAD_TANH) {
             action = N.tanh_scale * tanh(z[0]);
@@ -533,17 +551,17 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
     }
   } else if (warp == OZP_CW + 2) {
     // ================================================= MMA issue warp
-    bool live[2] = {true, true};
+    uint32_t live = 3u;  // bit g: group g still running (a mask, not an array: registers)
     const uint32_t bS = smem_u32(smem + P.off_B);
-    for (int it = 0; live[0] || live[1]; ++it) {
+    for (int it = 0; live != 0u; ++it) {
       for (int g = 0; g < 2; ++g) {
-        if (!live[g]) continue;
+        if (!((live >> g) & 1u)) continue;
         OZ_MARK(10);  // MMA warp: issue
         mbar_wait_parity_cta(&bfull[g], (uint32_t)(it & 1));
         __syncwarp();  // reconverge after the spin loop (elect.sync / tcgen05 below)
         OZ_MARK(9);  // MMA warp: waiting for B
         if (gdone[g]) {
-          live[g] = false;
+          live &= ~(1u << g);
           continue;
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -570,20 +588,20 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
     }
   } else {
     // ================================================= compute warps (0-7)
-    bool live[2] = {true, true};
+    uint32_t live = 3u;  // bit g: group g still running (a mask, not an array: registers)
     // layer-0 thread map: lane le of the group, 8 consecutive k rows (half a
     // 16-byte K row of a B core matrix)
     const int le = tid & 7, rg = tid >> 3;  // rg: 32 row groups of 8
     const bool l0_active = rg * 8 < W1p;
-    for (int it = 0; live[0] || live[1]; ++it) {
+    for (int it = 0; live != 0u; ++it) {
       for (int g = 0; g < 2; ++g) {
-        if (!live[g]) continue;
+        if (!((live >> g) & 1u)) continue;
         OZ_MARK(5);  // compute: publish (+ named barrier) / group switch
         mbar_wait_parity_cta(&x0full[g], (uint32_t)(it & 1));
         __syncwarp();
         OZ_MARK(1);  // compute: waiting for x0
         if (!alive[g]) {
-          live[g] = false;
+          live &= ~(1u << g);
           if (tid == 0) gdone[g] = 1u;
           __syncwarp();
           if (lane == 0) mbar_arrive_local(&bfull[g]);
