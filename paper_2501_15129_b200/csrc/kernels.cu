@@ -344,24 +344,25 @@ __global__ void __launch_bounds__(TELL_T) k_openes_tell_partial(const OpenEsTell
       for (int q = 0; q < lim; ++q) {
         const double w = wsh[q];
         const uint64_t k0 = (uint64_t)((long long)(i0 + q) * a.d + pbase);
-        // blocks covering normals [k0, k0 + V)
+        // blocks covering normals [k0, k0 + V) (the two alignments spelled out
+        // so every acc index is a compile-time constant: acc stays in registers)
         uint64_t b = k0 >> 1;
-        int v = 0;
+        double c, sn;
         if (k0 & 1) {  // first coordinate is the sin half of block b
-          double c, sn;
-          normal_pair(a.ask_key, b, c, sn);
+          normal_pair(a.ask_key, b++, c, sn);
           acc[0] = fma(sn, w, acc[0]);
-          v = 1;
-          ++b;
-        }
 #pragma unroll
-        for (int vv = 0; vv < TELL_V; vv += 2) {
-          if (vv + v < TELL_V) {
-            double c, sn;
-            normal_pair(a.ask_key, b, c, sn);
-            acc[vv + v] = fma(c, w, acc[vv + v]);
-            if (vv + v + 1 < TELL_V) acc[vv + v + 1] = fma(sn, w, acc[vv + v + 1]);
-            ++b;
+          for (int vv = 1; vv < TELL_V; vv += 2) {
+            normal_pair(a.ask_key, b++, c, sn);
+            acc[vv] = fma(c, w, acc[vv]);
+            if (vv + 1 < TELL_V) acc[vv + 1] = fma(sn, w, acc[vv + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int vv = 0; vv < TELL_V; vv += 2) {
+            normal_pair(a.ask_key, b++, c, sn);
+            acc[vv] = fma(c, w, acc[vv]);
+            acc[vv + 1] = fma(sn, w, acc[vv + 1]);
           }
         }
       }
@@ -659,7 +660,9 @@ EVB_DEV void welford_merge(W9& w, const W9& o, int dim) {
   const double total = dadd(w.c, o.c);
   const double s = ddiv(dmul(w.c, o.c), total);
   const double f = ddiv(o.c, total);
-  for (int i = 0; i < dim; ++i) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // registers, not local memory
+    if (i >= dim) break;
     const double delta = dsub(o.m[i], w.m[i]);
     w.q[i] = dadd(w.q[i], dadd(o.q[i], dmul(dmul(delta, delta), s)));
     w.m[i] = dadd(w.m[i], dmul(delta, f));
@@ -734,13 +737,17 @@ __global__ void k_rs_update(const double* agent_stats, int n_agents, DevNorm* no
     W9 cur{};
     if (nm.count > 0.0) {
       cur.c = nm.count;
-      for (int i = 0; i < dim; ++i) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // registers, not local memory
+        if (i >= dim) break;
         cur.m[i] = nm.mean[i];
         cur.q[i] = dmul(nm.var[i], nm.count);
       }
     }
     welford_merge(cur, batch, dim);
-    for (int i = 0; i < dim; ++i) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // registers, not local memory
+      if (i >= dim) break;
       nm.mean[i] = cur.m[i];
       nm.var[i] = cur.c == 0.0 ? cur.m[i] : ddiv(cur.q[i], cur.c);
     }
@@ -780,14 +787,18 @@ __global__ void k_vbn_fit(EnvDesc env, DKey lane_key, int n, DevNorm* norm, Norm
     double raw[4];
     observe(env, s, raw);
     if (w.c == 0.0) {
-      for (int i = 0; i < dim; ++i) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // registers, not local memory
+        if (i >= dim) break;
         w.m[i] = raw[i];
         w.q[i] = 0.0;
       }
       w.c = 1.0;
     } else {
       w.c = dadd(w.c, 1.0);
-      for (int i = 0; i < dim; ++i) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // registers, not local memory
+        if (i >= dim) break;
         const double delta = dsub(raw[i], w.m[i]);
         w.m[i] = dadd(w.m[i], ddiv(delta, w.c));
         w.q[i] = dadd(w.q[i], dmul(delta, dsub(raw[i], w.m[i])));
@@ -815,7 +826,9 @@ __global__ void k_vbn_fit(EnvDesc env, DKey lane_key, int n, DevNorm* norm, Norm
   DevNorm nm{};
   nm.mode = 1;
   nm.dim = dim;
-  for (int i = 0; i < dim; ++i) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // registers, not local memory
+    if (i >= dim) break;
     nm.mean[i] = w.m[i];
     nm.var[i] = w.c == 0.0 ? w.m[i] : ddiv(w.q[i], w.c);
   }

@@ -446,10 +446,7 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
     const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
     env_reset(E, fold_in(lane_key, 0), s);  // proj/src/rollout.cpp:104
   }
-  NormParams nrm;
-  nrm.active = 0;
-  nrm.dim = 0;
-  if (A.norm != nullptr) nrm = *A.norm;
+  const NormParams nrm = load_norm(A.norm);
 
   T* x0 = reinterpret_cast<T*>(smem + S.off_x0);
   T* part = reinterpret_cast<T*>(smem + S.off_part);
@@ -474,21 +471,27 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
       for (int i = 0; i < 4; ++i) cur_raw[i] = raw[i];
     if (act && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
       if (wc == 0.0) {
-        for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // registers, not local memory
+          if (i >= E.obs_dim) break;
           wmean[i] = raw[i];
           wm2[i] = 0.0;
         }
         wc = 1.0;
       } else {
         wc = dadd(wc, 1.0);
-        for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // registers, not local memory
+          if (i >= E.obs_dim) break;
           const double delta = dsub(raw[i], wmean[i]);
           wmean[i] = dadd(wmean[i], ddiv(delta, wc));
           wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
         }
       }
     }
-    for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // registers, not local memory
+      if (i >= E.obs_dim) break;
       double v = raw[i];
       if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
       x0[i * S.XS + tid] = act ? to_T<T>(v) : T(0);
@@ -668,7 +671,9 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
       bool nonfinite_out = false;
       int bad_layer = L;
       for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pout[c * OE1 + OE + tid]);
-      for (int o = 0; o < O && o < 8; ++o) {
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        if (o >= O) break;
         T v = pout[o * ET + tid];
         for (int c = 1; c < C; ++c) v += pout[c * OE1 + o * ET + tid];
         v = v + bo[o];
@@ -683,8 +688,13 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
         double action;
         if (N.head == HEAD_CATEGORICAL) {
           int arg = 0;
-          for (int o = 1; o < O; ++o)
-            if (z[o] > z[arg]) arg = o;  // maxCoeff: first maximum
+          double best = z[0];
+#pragma unroll
+          for (int o = 1; o < 8; ++o)
+            if (o < O && z[o] > best) {  // maxCoeff: first maximum
+              best = z[o];
+              arg = o;
+            }
           action = (double)arg;
         } else if (N.head == HEAD_TANH) {
           action = N.tanh_scale * tanh(z[0]);
@@ -699,7 +709,9 @@ __global__ void __launch_bounds__(ROLLOUT_THREADS, 1) rollout_kernel(const __gri
           double nxt[4];
           observe(E, s, nxt);  // final_obs: the successor before any auto-reset
           const long long row = ((long long)agent_local * A.e + j) * A.t_cap + steps;
-          for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // registers, not local memory
+            if (i >= E.obs_dim) break;
             A.t_obs[row * E.obs_dim + i] = cur_raw[i];
             A.t_next[row * E.obs_dim + i] = nxt[i];
           }
@@ -1032,10 +1044,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) rollout_pipe_kernel(const __g
       const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
       env_reset(E, fold_in(lane_key, 0), s);  // proj/src/rollout.cpp:104
     }
-    NormParams nrm;
-    nrm.active = 0;
-    nrm.dim = 0;
-    if (A.norm != nullptr) nrm = *A.norm;
+    const NormParams nrm = load_norm(A.norm);
     const double* bo = reinterpret_cast<const double*>(smem + S.off_bout);
     double sin_th = 0.0;
     auto observe_into_x0 = [&](bool act) {
@@ -1044,21 +1053,27 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) rollout_pipe_kernel(const __g
       sin_th = raw[1];
       if (act && A.track_stats) {  // WelfordStats::add, proj/src/obs_norm.cpp:7-18
         if (wc == 0.0) {
-          for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // registers, not local memory
+            if (i >= E.obs_dim) break;
             wmean[i] = raw[i];
             wm2[i] = 0.0;
           }
           wc = 1.0;
         } else {
           wc = dadd(wc, 1.0);
-          for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // registers, not local memory
+            if (i >= E.obs_dim) break;
             const double delta = dsub(raw[i], wmean[i]);
             wmean[i] = dadd(wmean[i], ddiv(delta, wc));
             wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
           }
         }
       }
-      for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // registers, not local memory
+        if (i >= E.obs_dim) break;
         double v = raw[i];
         if (nrm.active) v = ddiv(dsub(v, nrm.mean[i]), nrm.den[i]);
         x0[(gq_me * 4 + i) * PG + e] = act ? v : 0.0;
@@ -1095,7 +1110,9 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) rollout_pipe_kernel(const __g
           bool nonfinite_out = false;
           int bad_layer = L;
           for (int c = 0; c < C; ++c) bad_layer = min(bad_layer, (int)pout[c * OE1 + OE + e]);
-          for (int o = 0; o < O && o < 8; ++o) {
+#pragma unroll
+          for (int o = 0; o < 8; ++o) {
+            if (o >= O) break;
             double v = pout[o * PG + e];
             for (int c = 1; c < C; ++c) v += pout[c * OE1 + o * PG + e];
             z[o] = v + bo[o];
@@ -1109,8 +1126,13 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) rollout_pipe_kernel(const __g
             double action;
             if (N.head == HEAD_CATEGORICAL) {
               int arg = 0;
-              for (int o = 1; o < O; ++o)
-                if (z[o] > z[arg]) arg = o;  // maxCoeff: first maximum
+              double best = z[0];
+#pragma unroll
+              for (int o = 1; o < 8; ++o)
+                if (o < O && z[o] > best) {  // maxCoeff: first maximum
+                  best = z[o];
+                  arg = o;
+                }
               action = (double)arg;
             } else if (N.head == HEAD_TANH) {
               action = N.tanh_scale * tanh(z[0]);

@@ -53,6 +53,17 @@ struct NormParams {
   double den[4];
 };
 
+// The generation's normaliser, or the identity (inactive, den = 1) when there
+// is none -- every field defined, so no uninitialised value reaches the
+// speculated reciprocals of the env code.
+EVB_DEV NormParams load_norm(const NormParams* p) {
+  if (p != nullptr) return *p;
+  NormParams n{};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) n.den[i] = 1.0;
+  return n;
+}
+
 // Candidate parameter p of agent `agent` (global population index).
 EVB_DEV double param_value(const ParamDesc& P, long long d, int agent_local, int agent,
                            long long p) {

@@ -394,9 +394,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
       const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
       env_reset(E, fold_in(lane_key, 0), s);  // proj/src/rollout.cpp:104
     }
-    NormParams nrm;
-    nrm.active = 0;
-    if (A.norm != nullptr) nrm = *A.norm;
+    const NormParams nrm = load_norm(A.norm);
     // (every loop over the obs / output dimension is unrolled to its compile-time
     // bound with a predicate, so these arrays stay in registers: a dynamic
     // index would put them in local memory on the env chain's critical path)

@@ -308,9 +308,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) rollout_tc_kernel(const __grid_
     const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
     env_reset(E, fold_in(lane_key, 0), s);
   }
-  NormParams nrm;
-  nrm.active = 0;
-  if (A.norm != nullptr) nrm = *A.norm;
+  const NormParams nrm = load_norm(A.norm);
   double inv_den[4];
   for (int i = 0; i < 4; ++i) inv_den[i] = nrm.active ? 1.0 / nrm.den[i] : 1.0;
   float* x0 = reinterpret_cast<float*>(smem + P.off_x0);    // [4][16]

@@ -88,28 +88,31 @@ __global__ void __launch_bounds__(256) rollout_warp_kernel(const __grid_constant
   LaneEnv s{};
   const DKey lane_key = fold_in(fold_in(A.rollout_key, (uint64_t)agent), (uint64_t)j);
   env_reset(E, fold_in(lane_key, 0), s);
-  NormParams nrm;
-  nrm.active = 0;
-  if (A.norm != nullptr) nrm = *A.norm;
+  const NormParams nrm = load_norm(A.norm);
   double ep_ret = 0.0, wc = 0.0, wmean[4] = {0, 0, 0, 0}, wm2[4] = {0, 0, 0, 0};
   int ep_len = 0, eps_done = 0;
   long long steps = 0;
   uint32_t fault = 0, fault_layer = 0;
-  T* act[2] = {reinterpret_cast<T*>(slot + P.off_act0), reinterpret_cast<T*>(slot + P.off_act1)};
+  T* const act0 = reinterpret_cast<T*>(slot + P.off_act0);  // ping-pong activations (selected, not
+  T* const act1 = reinterpret_cast<T*>(slot + P.off_act1);  // indexed: no local-memory array)
 
   for (int it = 0; eps_done < eps_this && fault == 0 && it < A.max_iters; ++it) {
     double raw[4];
     observe(E, s, raw);
     if (A.track_stats) {  // WelfordStats::add (proj/src/obs_norm.cpp:7-18)
       if (wc == 0.0) {
-        for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // registers, not local memory
+          if (i >= E.obs_dim) break;
           wmean[i] = raw[i];
           wm2[i] = 0.0;
         }
         wc = 1.0;
       } else {
         wc = dadd(wc, 1.0);
-        for (int i = 0; i < E.obs_dim; ++i) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // registers, not local memory
+          if (i >= E.obs_dim) break;
           const double delta = dsub(raw[i], wmean[i]);
           wmean[i] = dadd(wmean[i], ddiv(delta, wc));
           wm2[i] = dadd(wm2[i], dmul(delta, dsub(raw[i], wmean[i])));
@@ -128,14 +131,14 @@ __global__ void __launch_bounds__(256) rollout_warp_kernel(const __grid_constant
       const int K = N.dims[l], W = N.dims[l + 1], RP = P.rows_p[l];
       const T* Ws = reinterpret_cast<const T*>(slot + P.off_w[l]);
       const T* bs = reinterpret_cast<const T*>(slot + P.off_b[l]);
-      const T* xin = act[(l + 1) & 1];
-      T* hout = act[l & 1];
+      const T* xin = (l & 1) ? act0 : act1;
+      T* hout = (l & 1) ? act1 : act0;
       bool nonfinite = false;
       for (int r0 = 0; r0 < RP; r0 += 128) {  // up to 4 rows per lane per pass
         T acc[4] = {T(0), T(0), T(0), T(0)};
         const int nr = min(4, (RP - r0) / 32);
         for (int k = 0; k < K; ++k) {
-          const T xv = l == 0 ? x0[k] : xin[k];
+          const T xv = l == 0 ? (k == 0 ? x0[0] : k == 1 ? x0[1] : k == 2 ? x0[2] : x0[3]) : xin[k];
           const T* wr = Ws + (size_t)k * RP + r0 + lane;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -161,19 +164,26 @@ __global__ void __launch_bounds__(256) rollout_warp_kernel(const __grid_constant
       const int l = L - 1, K = N.dims[l], RP = P.rows_p[l];
       const T* Ws = reinterpret_cast<const T*>(slot + P.off_w[l]);
       const T* bs = reinterpret_cast<const T*>(slot + P.off_b[l]);
-      const T* xin = act[(l + 1) & 1];
-      for (int o = 0; o < O && o < 8; ++o) {
+      const T* xin = (l & 1) ? act0 : act1;
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        if (o >= O) break;
         T part = T(0);
-        for (int k = lane; k < K; k += 32) part = fma(Ws[(size_t)k * RP + o], L == 1 ? x0[k] : xin[k], part);
-        // linear policy: K = obs_dim <= 4 lives in registers (lane < K only)
+        // linear policy: K = obs_dim <= 4 lives in registers (lane < K only),
+        // selected without a dynamic index (which would put x0 in local memory)
+        for (int k = lane; k < K; k += 32) {
+          const T xk = L == 1 ? (k == 0 ? x0[0] : k == 1 ? x0[1] : k == 2 ? x0[2] : x0[3]) : xin[k];
+          part = fma(Ws[(size_t)k * RP + o], xk, part);
+        }
         const T tot = warp_sum(part);
         z[o] = (double)(tot + bs[o]);
       }
     }
     __syncwarp();
     bool nonfinite_out = false;
-    for (int o = 0; o < O && o < 8; ++o)
-      if (!isfinite(z[o])) nonfinite_out = true;
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+      if (o < O && !isfinite(z[o])) nonfinite_out = true;
     if (bad < 0 && nonfinite_out) bad = L - 1;
     if (bad >= 0) {
       fault = FAULT_NET;
@@ -183,8 +193,13 @@ __global__ void __launch_bounds__(256) rollout_warp_kernel(const __grid_constant
     double action;
     if (N.head == HEAD_CATEGORICAL) {
       int arg = 0;
-      for (int o = 1; o < O; ++o)
-        if (z[o] > z[arg]) arg = o;
+      double best = z[0];
+#pragma unroll
+      for (int o = 1; o < 8; ++o)
+        if (o < O && z[o] > best) {  // maxCoeff: first maximum
+          best = z[o];
+          arg = o;
+        }
       action = (double)arg;
     } else if (N.head == HEAD_TANH) {
       action = N.tanh_scale * tanh(z[0]);
