@@ -79,7 +79,7 @@ def cma_lazy_gap(d, mu, pop):
 NCU_TRAFFIC = {
     ("3", "f64"): (2230139136 + 68040960, "ncu r01_f64_v6: rollout_kernel<double,1,16,4,1>"),
     ("3", "tc"): (1104370432 + 10082304, "ncu r01_tc_v5: rollout_tc_kernel<2> (cta_group::2 pair)"),
-    ("3", "oz"): (1673598000 + 48497664, "ncu r02_ozp_full_v2: rollout_ozp_kernel<6,2> (pre-split slices read once)"),
+    ("3", "oz"): (1672574000 + 6800640, "ncu r02_ozp_full_v10: rollout_ozp_kernel<6,2> (pre-split slices read once)"),
 }
 # int8 MMA work the oz team executes per env step and CTA (2 lane groups x
 # W1p/32 k-steps x S MMAs of M=128, K=32, N = 8(S-i) rounded up to 16): the
