@@ -72,12 +72,21 @@ EVB_DEV double word_to_uniform(uint64_t w) { return (double)(w >> 11) * 0x1.0p-5
 // proj/src/rng.cpp:70-72: lo + (hi - lo) * u
 EVB_DEV double uniform_range(double lo, double hi, double u) { return dadd(lo, dmul(hi - lo, u)); }
 
+// exact u64 -> double for x < 2^52: x lands in the mantissa of 2^52 + x
+EVB_DEV double u52_to_double(uint64_t x) {
+  return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;
+}
+
 // Box-Muller pair of block b (proj/src/rng.cpp:74-87): normal #2b = c, #2b+1 = s.
 EVB_DEV void normal_pair(DKey k, uint64_t b, double& c, double& s) {
   uint64_t w0, w1;
   threefry2x64(k.hi, k.lo, 1, b, w0, w1);
-  const double u1 = (double)((w0 >> 11) + 1) * 0x1.0p-53;
-  const double u2 = (double)(w1 >> 11) * 0x1.0p-53;
+  // u1 = ((w0 >> 11) + 1) 2^-53, u2 = (w1 >> 11) 2^-53, converted exactly
+  // without the conversion pipe: the top 52 bits land in a mantissa, the last
+  // bit and the +1 are exact fp64 adds (every intermediate is an integer < 2^53)
+  const double u1 =
+      dadd(dadd(dmul(u52_to_double(w0 >> 12), 2.0), ((w0 >> 11) & 1) ? 1.0 : 0.0), 1.0) * 0x1.0p-53;
+  const double u2 = dadd(dmul(u52_to_double(w1 >> 12), 2.0), ((w1 >> 11) & 1) ? 1.0 : 0.0) * 0x1.0p-53;
   const double r = sqrt(-2.0 * log(u1));
   const double a = 6.283185307179586 * u2;  // 2.0 * M_PI * u2
   double sa, ca;

@@ -100,6 +100,17 @@ __global__ void k_materialize_openes(const ParamDesc P, long long d, int a0, int
   if (2 * b >= t1) return;
   double c, sn;
   normal_pair(P.ask_key, (uint64_t)b, c, sn);
+  // (row, p) of entry 2b, one division per pair (32-bit when the stream
+  // indices fit: a 64-bit division is a long software sequence)
+  long long row2b, p2b;
+  if (t1 <= 0xFFFFFFFFll && d <= 0xFFFFFFFFll) {
+    const uint32_t q = (uint32_t)(2 * b) / (uint32_t)d;
+    row2b = q;
+    p2b = 2 * b - (long long)q * d;
+  } else {
+    row2b = (2 * b) / d;
+    p2b = 2 * b - row2b * d;
+  }
   if (eps_out) {
     if (2 * b >= t0 && 2 * b + 1 < t1)
       reinterpret_cast<double2*>(eps_out)[b] = make_double2(c, sn);
@@ -112,7 +123,11 @@ __global__ void k_materialize_openes(const ParamDesc P, long long d, int a0, int
   for (int h = 0; h < 2; ++h) {
     const long long t = 2 * b + h;
     if (t < t0 || t >= t1) continue;
-    const long long row = t / d, p = t - row * d;
+    long long row = row2b, p = p2b + h;
+    if (p == d) {  // entry 2b + 1 starts the next row
+      row += 1;
+      p = 0;
+    }
     const double eps = h ? sn : c;
     const int ag[2] = {(int)row, P.mirrored ? (int)row + P.base : -1};
 #pragma unroll
