@@ -58,6 +58,25 @@ CONFIGS = {
 }
 
 
+def workload_config(cfg_name):
+    """The `config` object of the bench line: the workload's identity only, so
+    the GPU arm and the reference arm print the same object for the same run
+    (how each arm executes it goes under `run`)."""
+    cfgd = CONFIGS[cfg_name]
+    obs, out = (3, 1) if cfgd["env"] == "pendulum" else (4, 2)
+    dims = [obs] + list(cfgd["hidden"]) + [out]
+    params = sum(dims[i] * dims[i + 1] + dims[i + 1] for i in range(len(dims) - 1))
+    c = {"workload": cfgd["desc"], "config": cfg_name, "pop": cfgd["pop"],
+         "envs_per_individual": cfgd["fitness_episodes"], "horizon": cfgd["max_episode_steps"],
+         "hidden": list(cfgd["hidden"]), "params": params,
+         "l2": "GPU arm: flushed (256 MiB write) before every timed generation; CPU reference arm: host, "
+               "not applicable"}
+    if cfgd["algo"] == "cmaes":
+        c["eig_every"] = cma_lazy_gap(params, cfgd["cmaes_elites"], cfgd["pop"])
+        c["timed_window"] = "whole lazy periods (one eigendecomposition per period)"
+    return c
+
+
 def mlp_flops_per_step(obs_dim, hidden, out_dim):
     dims = [obs_dim] + list(hidden) + [out_dim]
     return 2 * sum(a * b for a, b in zip(dims[:-1], dims[1:]))
@@ -209,8 +228,8 @@ def run_reference_arm(args, cfgd, cfg_name):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfgd["desc"], "config": cfg_name, "pop_sampled": sp,
-                   "pop": pop, "parallelism": f"{cores} host threads (ThreadPool lane grid)"},
+        "config": workload_config(cfg_name),
+        "run": {"parallelism": f"{cores} host threads (ThreadPool lane grid)", "pop_sampled": sp},
         "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "port",
                          "sample": f"each step = 1 generation of the oracle port at pop {sp} of {pop}"},
         "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
@@ -431,7 +450,7 @@ def main():
     # f64 (DMMA team, the bit-level parity path) and tc (fp32-accurate tcgen05
     # team: returns within the fp32 tolerance, ranks not bit-exact)
     variants = {}
-    params_dim = es.dim
+    assert es.dim == workload_config(args.config)["params"]
     parity = {
         "f64": "bit-level parity path: returns within 1e-9 of the reference CPU restatement, ranks identical",
         "oz": "returns within ~1e-8 of the reference CPU restatement, ranks identical to the fp64 path "
@@ -471,17 +490,12 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if args.precision in ("f32", "tc") else "f64", "data": "synthetic",
-            "config": {"workload": cfgd["desc"], "config": args.config, "pop": pop,
-                       "envs_per_individual": e, "horizon": H, "hidden": list(cfg.hidden),
-                       "params": params_dim, "parallelism": f"population-sharded dp{world}",
-                       "l2": "flushed (256 MiB write) between timed generations",
-                       "policy_precision": args.precision,
-                       "policy_team": eff_prec,
-                       "parity": parity.get(eff_prec, "returns within fp32 tolerance"),
-                       **({"eig_every": getattr(args, "cma_gap", None),
-                           "timed_window": "whole lazy periods (one eigendecomposition per period)"}
-                          if kw.get("algo") == "cmaes" else {}),
-                       "env_dynamics": "f64"},
+            "config": workload_config(args.config),
+            "run": {"parallelism": f"population-sharded dp{world}",
+                    "policy_precision": args.precision,
+                    "policy_team": eff_prec,
+                    "parity": parity.get(eff_prec, "returns within fp32 tolerance"),
+                    "env_dynamics": "f64"},
             "generations_per_sec": args.steps / (max_ms / 1e3),
             "gpu_launches": int(launches),
             "roofline": roofline,
