@@ -104,6 +104,9 @@ NCU_TRAFFIC = {
 # W1p/32 k-steps x S MMAs of M=128, K=32, N = 8(S-i) rounded up to 16): the
 # tensor-pipe view of the roofline beside the algorithmic one
 OZ_S = 6
+# executed warp-instructions per Box-Muller pair of the OpenES ask
+# (smsp__inst_executed / pairs of k_materialize_openes<double>, ncu, config 3)
+ASK_WARP_INSTS_PER_PAIR = 540
 
 
 def oz_int8_ops_per_cta_step(w1):
@@ -312,7 +315,7 @@ def main():
             args.steps = -(-max(args.steps, gap) // gap) * gap
             args.cma_gap = gap
         launches0 = L.evorl_kernel_launches()
-        times, roll = [], []
+        times, roll, ask = [], [], []
         if clk is not None:
             clk.__enter__()
         for _ in range(args.steps):
@@ -326,16 +329,19 @@ def main():
             barrier()
             times.append(e0.elapsed_time(e1))
             roll.append(es.last_timings()[0])   # rollout kernel, events on the library stream
+            ask.append(es.last_ask_ms())        # materialised ask (-1: not one timed launch)
         if clk is not None:
             clk.__exit__(None, None, None)
         launches = L.evorl_kernel_launches() - launches0
         tot = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
         if dist is not None:
             dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        args.ask_ms = statistics.mean(ask) if ask and min(ask) > 0 else None
         return cfg, es, float(tot.item()), roll, launches
 
     clk = ClockSampler(local)
     cfg, es, max_ms, roll, launches = timed_generations(args.precision, clk)
+    ask_ms = args.ask_ms
 
     pop, e, H = cfg.pop, cfg.fitness_episodes, cfg.max_episode_steps
     env_steps_per_gen = pop * e * H
@@ -446,6 +452,22 @@ def main():
                 "rollout_ms_per_launch": roll_ms, "rollout_share_of_step":
                     (roll_ms / ms_per_step) if roll_ms else None}
 
+    # ---- the ask's noise generator (normals/s against the SM
+    # issue rate -- Threefry is INT ALU work and Box-Muller FP64, both issue-bound)
+    rng = None
+    if kw.get("algo") == "openes" and ask_ms and world == 1:
+        rows = pop // 2 if cfg.openes_mirrored else pop
+        normals = rows * es.dim
+        sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+        peak_n = 148 * 4 * sm_mhz * 1e6 * 32 / ASK_WARP_INSTS_PER_PAIR * 2
+        rng = {"normals_per_gen": normals, "ask_ms": ask_ms, "achieved": normals / (ask_ms * 1e-3),
+               "unit": "normals/s", "bound": "SM issue (Threefry INT ALU + Box-Muller FP64)", "peak": peak_n,
+               "frac": normals / (ask_ms * 1e-3) / peak_n,
+               "peak_source": f"148 SMs x 4 warp-instructions/clk x {sm_mhz:.0f} MHz / "
+                              f"{ASK_WARP_INSTS_PER_PAIR} warp-instructions per Box-Muller pair (ncu "
+                              "smsp__inst_executed of k_materialize_openes<double>) x 2 normals per pair",
+               "kernel": "k_materialize_openes<double> (candidates + kept noise rows written)"}
+
     # ---- the other policy precisions on the same workload, beside the headline:
     # f64 (DMMA team, the bit-level parity path) and tc (fp32-accurate tcgen05
     # team: returns within the fp32 tolerance, ranks not bit-exact)
@@ -499,6 +521,7 @@ def main():
             "generations_per_sec": args.steps / (max_ms / 1e3),
             "gpu_launches": int(launches),
             "roofline": roofline,
+            "ask_rng": rng,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),

@@ -319,6 +319,11 @@ void* evorl_es_stream(evorl_es* es);
 /* device time (ms) of the last rollout launch and last full step, from CUDA
  * events on the handle's stream */
 int evorl_es_last_timings(const evorl_es* es, float* rollout_ms, float* step_ms);
+/* device time (ms) of the last generation's materialised ask (the candidate
+ * matrix -- for OpenES the Threefry + Box-Muller noise -- in one launch), or
+ * -1 when the ask was not one timed launch (chunked candidates, CMA-ES, or
+ * before the first step) */
+int evorl_es_last_ask_ms(const evorl_es* es, float* ask_ms);
 
 /* ---------------------------------------------------------- benchmarking
  * Measured FP64 FMA peak of this GPU (TFLOP/s) by a DFMA-bound kernel; used

@@ -225,7 +225,9 @@ struct evorl_es {
   long long p0 = 0, p1 = 0;
   // timing
   cudaEvent_t ev_r0 = nullptr, ev_r1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
-  float last_rollout_ms = 0.f, last_step_ms = 0.f;
+  cudaEvent_t ev_a0 = nullptr, ev_a1 = nullptr;  // around the materialised ask (one chunk)
+  float last_rollout_ms = 0.f, last_step_ms = 0.f, last_ask_ms = -1.f;
+  bool ask_timed = false;
   // per-step keys
   DKey step_key{}, ask_key{}, rollout_key{};
   // CmaState (proj/include/evorl/ec.hpp:107-122): scalars on the host (the
@@ -294,7 +296,7 @@ static void free_all(evorl_es* s) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
-  for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1})
+  for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1, s->ev_a0, s->ev_a1})
     if (ev) cudaEventDestroy(ev);
   void* cm[] = {s->cma.d_w, s->cma.dev.C, s->cma.dev.B, s->cma.dev.D, s->cma.dev.ps, s->cma.dev.pc,
                 s->cma.dev.W, s->cma.dev.V, s->cma.dev.Bt, s->cma.dev.Tt, s->cma.dev.U, s->cma.dev.skipf, s->cma.dev.evals, s->cma.dev.order, s->cma.dev.zD,
@@ -503,6 +505,8 @@ static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** 
   A(cudaEventCreate(&s->ev_r1));
   A(cudaEventCreate(&s->ev_s0));
   A(cudaEventCreate(&s->ev_s1));
+  A(cudaEventCreate(&s->ev_a0));
+  A(cudaEventCreate(&s->ev_a1));
   // Adam bias corrections 1 - beta^t with the host libm pow (the reference's
   // std::pow, proj/src/optim.cpp:12-13), t = 1..65536.
   s->adam_bc_len = 65536;
@@ -820,6 +824,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
   s->rollout_key = fold_in(s->step_key, 1);  // proj/src/workflow_es.cpp:125
   if (s->d_table) CK(table_offsets(s, s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop));
   s->eps_rows_valid = false;
+  s->ask_timed = false;
   CK(cudaEventRecord(s->ev_s0, s->stream));
   CK(cudaMemsetAsync(s->d_steps, 0, sizeof(unsigned long long), s->stream));
   CK(cudaMemsetAsync(s->d_fault, 0xFF, sizeof(unsigned long long), s->stream));
@@ -841,7 +846,10 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
     // small policy: materialise the shard's candidates (fully parallel ask),
     // then one warp per lane with the weights resident in shared memory
     double* er = a.par.src == SRC_OPENES ? eps_rows_buffer(s) : nullptr;
+    CK(cudaEventRecord(s->ev_a0, s->stream));
     CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream, er));
+    CK(cudaEventRecord(s->ev_a1, s->stream));
+    s->ask_timed = true;
     s->eps_rows_valid = er != nullptr;
     count_launch();
     a.par.src = SRC_EXPLICIT;
@@ -860,8 +868,11 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
       ac.ep_returns = s->d_ep_returns + (long long)c0 * s->count;
       ac.lane_steps = s->d_lane_steps + (long long)c0 * s->e;
       ac.lane_stats = s->d_lane_stats + (long long)c0 * s->e * 9;
+      const bool one_chunk = c0 == s->a0 && c1 == s->a1;
+      if (one_chunk) CK(cudaEventRecord(s->ev_a0, s->stream));
       if (s->d_cand_f32) {
         CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream, er));
+        if (one_chunk) CK(cudaEventRecord(s->ev_a1, s->stream));
         ac.par.src = SRC_EXPLICIT_F32;
         ac.par.params_f32 = s->d_cand_f32;
         if (s->d_tc_blocks) {  // the tc team's layer-1 weights, pre-split (bulk-copied by its prologue)
@@ -872,6 +883,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
         }
       } else {
         CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream, er));
+        if (one_chunk) CK(cudaEventRecord(s->ev_a1, s->stream));
         ac.par.src = SRC_EXPLICIT;
         ac.par.params = s->d_cand;
         if (s->d_tc_blocks) {  // the oz team's layer-1 weights, pre-split into fixed-point byte slices
@@ -882,6 +894,7 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
         }
       }
       count_launch();
+      s->ask_timed = one_chunk;
       if (c0 == s->a0) CK(cudaEventRecord(s->ev_r0, s->stream));
       CK(launch_rollout(ac, s->cfg.precision, s->stream));
       count_launch();
@@ -1018,6 +1031,8 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
   }
   cudaEventElapsedTime(&s->last_rollout_ms, s->ev_r0, s->ev_r1);
   cudaEventElapsedTime(&s->last_step_ms, s->ev_s0, s->ev_s1);
+  s->last_ask_ms = -1.f;
+  if (s->ask_timed) cudaEventElapsedTime(&s->last_ask_ms, s->ev_a0, s->ev_a1);
   s->env_steps += (long long)s->h->steps;
   s->episodes += (long long)n * s->count;
   s->iteration += 1;
@@ -1169,6 +1184,11 @@ extern "C" void* evorl_es_stream(evorl_es* s) { return (void*)s->stream; }
 extern "C" int evorl_es_last_timings(const evorl_es* s, float* rollout_ms, float* step_ms) {
   if (rollout_ms) *rollout_ms = s->last_rollout_ms;
   if (step_ms) *step_ms = s->last_step_ms;
+  return EVORL_OK;
+}
+
+extern "C" int evorl_es_last_ask_ms(const evorl_es* s, float* ask_ms) {
+  if (ask_ms) *ask_ms = s->last_ask_ms;
   return EVORL_OK;
 }
 

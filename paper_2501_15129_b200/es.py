@@ -253,6 +253,12 @@ class EsWorkflow:
         check(self.L.evorl_es_last_timings(self.h, C.byref(r), C.byref(s)))
         return r.value, s.value
 
+    def last_ask_ms(self) -> float:
+        """Device ms of the last generation's materialised ask (-1 if not timed)."""
+        a = C.c_float()
+        check(self.L.evorl_es_last_ask_ms(self.h, C.byref(a)))
+        return a.value
+
     # sharded phases (see paper_2501_15129_b200.dist) ----------------------
     def set_shard(self, rank: int, world: int) -> None:
         check(self.L.evorl_es_set_shard(self.h, rank, world))
