@@ -104,9 +104,9 @@ NCU_TRAFFIC = {
 # W1p/32 k-steps x S MMAs of M=128, K=32, N = 8(S-i) rounded up to 16): the
 # tensor-pipe view of the roofline beside the algorithmic one
 OZ_S = 6
-# executed warp-instructions per Box-Muller pair of the OpenES ask
-# (smsp__inst_executed / pairs of k_materialize_openes<double>, ncu, config 3)
-ASK_WARP_INSTS_PER_PAIR = 540
+# executed warp-instructions per Box-Muller pair of the OpenES noise generator
+# (smsp__inst_executed / pairs of k_noise_rows, ncu, config 3)
+NOISE_WARP_INSTS_PER_PAIR = 384
 
 
 def oz_int8_ops_per_cta_step(w1):
@@ -452,21 +452,27 @@ def main():
                 "rollout_ms_per_launch": roll_ms, "rollout_share_of_step":
                     (roll_ms / ms_per_step) if roll_ms else None}
 
-    # ---- the ask's noise generator (normals/s against the SM
-    # issue rate -- Threefry is INT ALU work and Box-Muller FP64, both issue-bound)
+    # ---- the ask: the OpenES noise generator as normals/s
+    # against the SM issue rate (Threefry is INT ALU work, Box-Muller FP64:
+    # both issue-bound), measured at full occupancy; in the generation it runs
+    # beside the previous rollout, and the ask on the path only adds the mean
     rng = None
-    if kw.get("algo") == "openes" and ask_ms and world == 1:
+    if kw.get("algo") == "openes" and world == 1:
         rows = pop // 2 if cfg.openes_mirrored else pop
         normals = rows * es.dim
+        rate = evb.measure_noise_rate(normals)
         sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
-        peak_n = 148 * 4 * sm_mhz * 1e6 * 32 / ASK_WARP_INSTS_PER_PAIR * 2
-        rng = {"normals_per_gen": normals, "ask_ms": ask_ms, "achieved": normals / (ask_ms * 1e-3),
-               "unit": "normals/s", "bound": "SM issue (Threefry INT ALU + Box-Muller FP64)", "peak": peak_n,
-               "frac": normals / (ask_ms * 1e-3) / peak_n,
+        peak_n = 148 * 4 * sm_mhz * 1e6 * 32 / NOISE_WARP_INSTS_PER_PAIR * 2
+        rng = {"normals_per_gen": normals, "achieved": rate, "unit": "normals/s",
+               "bound": "SM issue (Threefry INT ALU + Box-Muller FP64)", "peak": peak_n, "frac": rate / peak_n,
                "peak_source": f"148 SMs x 4 warp-instructions/clk x {sm_mhz:.0f} MHz / "
-                              f"{ASK_WARP_INSTS_PER_PAIR} warp-instructions per Box-Muller pair (ncu "
-                              "smsp__inst_executed of k_materialize_openes<double>) x 2 normals per pair",
-               "kernel": "k_materialize_openes<double> (candidates + kept noise rows written)"}
+                              f"{NOISE_WARP_INSTS_PER_PAIR} warp-instructions per Box-Muller pair (ncu "
+                              "smsp__inst_executed of k_noise_rows) x 2 normals per pair",
+               "kernel": "k_noise_rows (evorl_measure_noise_rate: full occupancy, alone)",
+               "in_generation": "k_noise_rows beside the previous generation's rollout (one block per SM on a "
+                                "low-priority stream), off the critical path",
+               "ask_on_path_ms": ask_ms,
+               "ask_on_path": "k_cand_from_eps: candidates = mean + sigma * kept noise rows (HBM-bound)"}
 
     # ---- the other policy precisions on the same workload, beside the headline:
     # f64 (DMMA team, the bit-level parity path) and tc (fp32-accurate tcgen05

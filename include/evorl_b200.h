@@ -320,15 +320,19 @@ void* evorl_es_stream(evorl_es* es);
  * events on the handle's stream */
 int evorl_es_last_timings(const evorl_es* es, float* rollout_ms, float* step_ms);
 /* device time (ms) of the last generation's materialised ask (the candidate
- * matrix -- for OpenES the Threefry + Box-Muller noise -- in one launch), or
- * -1 when the ask was not one timed launch (chunked candidates, CMA-ES, or
- * before the first step) */
+ * matrix in one launch: for OpenES from the noise rows generated beside the
+ * previous rollout, or with its own Threefry + Box-Muller noise on the first
+ * generation / when that is off), or -1 when the ask was not one timed launch
+ * (chunked candidates, CMA-ES, or before the first step) */
 int evorl_es_last_ask_ms(const evorl_es* es, float* ask_ms);
 
 /* ---------------------------------------------------------- benchmarking
  * Measured FP64 FMA peak of this GPU (TFLOP/s) by a DFMA-bound kernel; used
  * as the roofline denominator of the fp64 rollout. */
 int evorl_measure_fp64_peak(double* tflops);
+/* The OpenES noise generator (counter-addressed Threefry2x64 + Box-Muller)
+ * at full occupancy: device ms to write n normals (second of two runs). */
+int evorl_measure_noise_rate(int64_t n, float* ms);
 /* Measured FP64 tensor-core (mma.sync m8n8k4 DMMA) peak, TFLOP/s. */
 int evorl_measure_dmma_peak(double* tflops);
 

@@ -7,14 +7,14 @@ reference's Workflow / ask-tell / rollout interfaces over that ABI.
 from ._lib import (CheckpointError, ConfigError, DeviceError, EnvFault, EvorlError,
                    InvalidArgument, LengthError, MissingExtension, NetFault, Unsupported)
 from .es import (CmaEs, EsConfig, EsWorkflow, StepMetrics, ars_ask, ars_tell, batched_rollout,
-                 centered_ranks, env_step_batch, gaussian_matrix, measure_fp64_peak, mlp_desc,
-                 openes_ask, openes_tell, param_count, rank_desc, stream_words, sym_eig,
+                 centered_ranks, env_step_batch, gaussian_matrix, measure_fp64_peak, measure_noise_rate,
+                 mlp_desc, openes_ask, openes_tell, param_count, rank_desc, stream_words, sym_eig,
                  threefry2x64)
 
 __all__ = [
     "ConfigError", "DeviceError", "EnvFault", "EvorlError", "InvalidArgument", "LengthError",
     "MissingExtension", "NetFault", "Unsupported", "CheckpointError", "CmaEs", "EsConfig", "EsWorkflow", "StepMetrics",
     "ars_ask", "ars_tell", "batched_rollout", "centered_ranks", "env_step_batch",
-    "gaussian_matrix", "measure_fp64_peak", "mlp_desc", "openes_ask", "openes_tell",
+    "gaussian_matrix", "measure_fp64_peak", "measure_noise_rate", "mlp_desc", "openes_ask", "openes_tell",
     "param_count", "rank_desc", "stream_words", "sym_eig", "threefry2x64",
 ]

@@ -197,6 +197,15 @@ struct evorl_es {
   double* d_eps_rows = nullptr;
   bool eps_rows_valid = false;
   bool eps_rows_failed = false;
+  // ... and the NEXT generation's noise rows, generated beside this rollout on
+  // a low-priority stream (one small block per SM next to the team CTA), so
+  // the next ask only adds the mean (valid while its key is the next ask key)
+  double* d_eps_next = nullptr;
+  bool eps_next_valid = false, eps_next_failed = false;
+  DKey eps_next_key{};
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_noise = nullptr;
+  int n_sms = 0;
   cudaStream_t stream = nullptr;
   // WorkflowState (proj/include/evorl/workflow.hpp:31-36)
   DKey rng{};
@@ -292,11 +301,12 @@ static void free_all(evorl_es* s) {
                   s->d_ep_returns, s->d_lane_stats, s->d_agent_stats, s->d_lane_steps, s->d_rank,
                   s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
                   s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand,
-                  s->d_cand_f32, s->d_tell_part, s->d_table, s->d_offsets, s->d_tc_blocks, s->d_eps_rows};
+                  s->d_cand_f32, s->d_tell_part, s->d_table, s->d_offsets, s->d_tc_blocks, s->d_eps_rows,
+                  s->d_eps_next};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
-  for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1, s->ev_a0, s->ev_a1})
+  for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1, s->ev_a0, s->ev_a1, s->ev_noise})
     if (ev) cudaEventDestroy(ev);
   void* cm[] = {s->cma.d_w, s->cma.dev.C, s->cma.dev.B, s->cma.dev.D, s->cma.dev.ps, s->cma.dev.pc,
                 s->cma.dev.W, s->cma.dev.V, s->cma.dev.Bt, s->cma.dev.Tt, s->cma.dev.U, s->cma.dev.skipf, s->cma.dev.evals, s->cma.dev.order, s->cma.dev.zD,
@@ -304,6 +314,7 @@ static void free_all(evorl_es* s) {
   for (void* p : cm)
     if (p) cudaFree(p);
   if (s->stream) cudaStreamDestroy(s->stream);
+  if (s->side) cudaStreamDestroy(s->side);
 }
 
 static int resolve_norm(const evorl_es_config& c) {  // proj/src/workflow.cpp:131-144
@@ -383,7 +394,13 @@ static int es_create(const evorl_es_config* cfg, long long forced_d, evorl_es** 
       return set_err(EVORL_E_CUDA, "allocation failed: %s", cudaGetErrorString(_e)); \
     }                          \
   } while (0)
-  A(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  {
+    // the generation's stream at the highest priority, so the rollout's team
+    // CTAs are placed before the low-priority noise-ahead blocks (side stream)
+    int least = 0, greatest = 0;
+    A(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    A(cudaStreamCreateWithPriority(&s->stream, cudaStreamNonBlocking, greatest));
+  }
   A(dalloc(&s->d_mean, d));
   A(dalloc(&s->d_m, d));
   A(dalloc(&s->d_v, d));
@@ -538,6 +555,7 @@ extern "C" void evorl_es_destroy(evorl_es* s) {
   if (!s) return;
   cudaSetDevice(s->cfg.device);
   cudaStreamSynchronize(s->stream);
+  if (s->side) cudaStreamSynchronize(s->side);
   free_all(s);
   delete s;
 }
@@ -711,6 +729,29 @@ static double* eps_rows_buffer(evorl_es* s) {
   return s->d_eps_rows;
 }
 
+// The buffer for the next generation's noise rows (same size as
+// eps_rows_buffer's), the low-priority stream and event, or null
+// (EVORL_NO_NOISE_AHEAD=1 disables it -- used by the tests).
+static double* eps_next_buffer(evorl_es* s) {
+  static const bool off = getenv("EVORL_NO_NOISE_AHEAD") && atoi(getenv("EVORL_NO_NOISE_AHEAD")) != 0;
+  if (off || s->eps_next_failed || !s->d_eps_rows) return nullptr;
+  if (!s->d_eps_next) {
+    const long long rows = s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop;
+    int least = 0, greatest = 0;
+    bool ok = cudaMalloc((void**)&s->d_eps_next, sizeof(double) * (size_t)rows * (size_t)s->d) == cudaSuccess;
+    ok = ok && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, least) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&s->ev_noise, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaDeviceGetAttribute(&s->n_sms, cudaDevAttrMultiProcessorCount, s->cfg.device) == cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      s->eps_next_failed = true;
+      return nullptr;
+    }
+  }
+  return s->d_eps_next;
+}
+
 static RolloutArgs rollout_args(const evorl_es* s) {
   RolloutArgs a{};
   a.env = s->env;
@@ -860,6 +901,16 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
     // team path: materialise the shard's candidates (chunks of cand_cap
     // agents), then roll each chunk out
     double* er = a.par.src == SRC_OPENES ? eps_rows_buffer(s) : nullptr;
+    const bool whole = s->cand_cap >= s->a1 - s->a0;  // one materialised chunk
+    bool kept = false;  // this ask's noise rows were generated beside the last rollout
+    if (er && whole && s->eps_next_valid && s->eps_next_key.hi == s->ask_key.hi &&
+        s->eps_next_key.lo == s->ask_key.lo) {
+      CK(cudaStreamWaitEvent(s->stream, s->ev_noise, 0));
+      std::swap(s->d_eps_rows, s->d_eps_next);
+      er = s->d_eps_rows;
+      kept = true;
+    }
+    s->eps_next_valid = false;
     for (int c0 = s->a0; c0 < s->a1; c0 += s->cand_cap) {
       const int c1 = std::min(s->a1, c0 + s->cand_cap);
       RolloutArgs ac = a;
@@ -871,7 +922,11 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
       const bool one_chunk = c0 == s->a0 && c1 == s->a1;
       if (one_chunk) CK(cudaEventRecord(s->ev_a0, s->stream));
       if (s->d_cand_f32) {
-        CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream, er));
+        if (kept) {
+          CK(run_cand_from_eps_f32(a.par, s->d, c0, c1, er, s->d_cand_f32, s->stream));
+        } else {
+          CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream, er));
+        }
         if (one_chunk) CK(cudaEventRecord(s->ev_a1, s->stream));
         ac.par.src = SRC_EXPLICIT_F32;
         ac.par.params_f32 = s->d_cand_f32;
@@ -882,7 +937,11 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
           ac.tc_block_bytes = tc_block_bytes(s->plan.tcp);
         }
       } else {
-        CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream, er));
+        if (kept) {
+          CK(run_cand_from_eps(a.par, s->d, c0, c1, er, s->d_cand, s->stream));
+        } else {
+          CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream, er));
+        }
         if (one_chunk) CK(cudaEventRecord(s->ev_a1, s->stream));
         ac.par.src = SRC_EXPLICIT;
         ac.par.params = s->d_cand;
@@ -900,6 +959,18 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
       count_launch();
     }
     s->eps_rows_valid = er != nullptr && s->a1 > s->a0;
+    if (er && whole && s->a1 > s->a0) {
+      if (double* nx = eps_next_buffer(s)) {  // the next generation's noise, beside this rollout
+        const long long rows = s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop;
+        const DKey next = fold_in(fold_in(fold_in(s->rng, 0), (uint64_t)(s->iteration + 1)), 0);
+        CK(cudaStreamWaitEvent(s->side, s->ev_r0, 0));
+        CK(run_noise_rows(next, rows * s->d, nx, s->n_sms, s->side));
+        CK(cudaEventRecord(s->ev_noise, s->side));
+        count_launch();
+        s->eps_next_valid = true;
+        s->eps_next_key = next;
+      }
+    }
   }
   CK(cudaEventRecord(s->ev_r1, s->stream));
   CK(run_fitness(a.ep_returns, s->count, a.n_agents, s->a0, s->d_fitness, a.lane_steps, s->e, s->d_steps,
@@ -1767,6 +1838,33 @@ extern "C" int evorl_measure_dmma_peak(double* tflops) {
   DEV_OR_RETURN();
   *tflops = measure_dmma_peak_tflops();
   CK(cudaGetLastError());
+  return EVORL_OK;
+}
+
+// The ask's noise generator at full machine occupancy: n normals of a fixed
+// key by k_noise_rows (16 blocks per SM), device ms of the second of two runs.
+extern "C" int evorl_measure_noise_rate(int64_t n, float* ms) {
+  DEV_OR_RETURN();
+  if (n <= 0) return set_err(EVORL_E_INVALID_ARGUMENT, "measure_noise_rate: n must be positive");
+  int dev = 0, sms = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  Scratch buf;
+  double* eps;
+  if (int rc = up(buf, (const double*)nullptr, (size_t)n, &eps)) return rc;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const DKey key{0x9E3779B97F4A7C15ull, 0xBB67AE8584CAA73Bull};
+  cudaError_t err = run_noise_rows(key, n, eps, 16 * sms, 0);
+  if (err == cudaSuccess) err = cudaEventRecord(e0, 0);
+  if (err == cudaSuccess) err = run_noise_rows(key, n, eps, 16 * sms, 0);
+  if (err == cudaSuccess) err = cudaEventRecord(e1, 0);
+  if (err == cudaSuccess) err = cudaEventSynchronize(e1);
+  if (err == cudaSuccess) err = cudaEventElapsedTime(ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CK(err);
   return EVORL_OK;
 }
 

@@ -196,6 +196,84 @@ cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, d
   return materialize(par, d, a0, a1, out, stream, eps_out);
 }
 
+// ------------------------------------------------ OpenES noise kept ahead
+// Normals [0, n) of the ask stream `key` into eps (eps[t] = normal #t), by a
+// persistent grid of one small block per SM: launched beside a resident
+// rollout (one team CTA per SM leaves room for exactly one such block), it
+// fills the next generation's noise rows while the current one rolls out.
+constexpr int NOISE_T = 128;
+__global__ void __launch_bounds__(NOISE_T) k_noise_rows(DKey key, long long n, double* __restrict__ eps) {
+  const long long pairs = (n + 1) >> 1;
+  const long long stride = (long long)gridDim.x * NOISE_T;
+  for (long long b = blockIdx.x * (long long)NOISE_T + threadIdx.x; b < pairs; b += stride) {
+    double c, sn;
+    normal_pair(key, (uint64_t)b, c, sn);
+    if (2 * b + 1 < n) {
+      reinterpret_cast<double2*>(eps)[b] = make_double2(c, sn);
+    } else {
+      eps[2 * b] = c;
+    }
+  }
+}
+cudaError_t run_noise_rows(DKey key, long long n, double* eps, int blocks, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  k_noise_rows<<<(unsigned)std::max(1, blocks), NOISE_T, 0, stream>>>(key, n, eps);
+  return cudaGetLastError();
+}
+
+// The OpenES ask from kept noise rows: entry t = row * d + p of the rows
+// [r0, r1) the agents [a0, a1) use gives candidate p of agent row (and of
+// row + base, negated, when mirrored) -- the values k_materialize_openes
+// computes, without regenerating the normals.
+template <typename T>
+__global__ void k_cand_from_eps(const ParamDesc P, long long d, int a0, int a1, long long t0, long long t1,
+                                const double* __restrict__ eps, T* __restrict__ out) {
+  const long long t = t0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= t1) return;
+  long long row, p;
+  if (t1 <= 0xFFFFFFFFll && d <= 0xFFFFFFFFll) {
+    const uint32_t q = (uint32_t)t / (uint32_t)d;
+    row = q;
+    p = t - (long long)q * d;
+  } else {
+    row = t / d;
+    p = t - row * d;
+  }
+  const double e = eps[t];
+  const double m = P.mean[p];
+  const int ag[2] = {(int)row, P.mirrored ? (int)row + P.base : -1};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int a = ag[k];
+    if (a < a0 || a >= a1) continue;
+    const double v = dadd(dmul(P.sigma, k ? -e : e), m);
+    if constexpr (sizeof(T) == 4) {
+      out[(long long)(a - a0) * d + p] = __double2float_rn(v);
+    } else {
+      out[(long long)(a - a0) * d + p] = v;
+    }
+  }
+}
+template <typename T>
+static cudaError_t cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps, T* out,
+                                 cudaStream_t stream) {
+  if (par.src != SRC_OPENES) return cudaErrorInvalidValue;
+  if (a1 <= a0) return cudaSuccess;
+  long long r0, r1;
+  openes_rows(par, a0, a1, r0, r1);
+  const long long t0 = r0 * d, t1 = r1 * d;
+  k_cand_from_eps<T><<<(unsigned)((t1 - t0 + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1, eps, out);
+  return cudaGetLastError();
+}
+cudaError_t run_cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps, double* out,
+                              cudaStream_t stream) {
+  return cand_from_eps(par, d, a0, a1, eps, out, stream);
+}
+cudaError_t run_cand_from_eps_f32(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
+                                  float* out, cudaStream_t stream) {
+  return cand_from_eps(par, d, a0, a1, eps, out, stream);
+}
+
 template <typename T, int N>
 struct VecLoad {
   EVB_DEV static void load(const T* __restrict__ src, T* dst) {

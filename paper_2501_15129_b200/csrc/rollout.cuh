@@ -191,6 +191,16 @@ cudaError_t launch_rollout_warp(const RolloutArgs& a, const WarpPlanOut& plan, i
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
                             cudaStream_t stream, double* eps_out = nullptr);
 
+// OpenES noise kept ahead of the ask: normals [0, n) of the ask stream `key`
+// into eps (persistent grid of `blocks` 128-thread blocks, sized to share the
+// SMs with a resident rollout), and the ask's candidates from such rows
+// (bit-identical to run_materialize / run_materialize_f32 for SRC_OPENES).
+cudaError_t run_noise_rows(DKey key, long long n, double* eps, int blocks, cudaStream_t stream);
+cudaError_t run_cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps, double* out,
+                              cudaStream_t stream);
+cudaError_t run_cand_from_eps_f32(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
+                                  float* out, cudaStream_t stream);
+
 // Materialise candidates [a0, a1) as fp32 (the value the fp32 policy paths
 // round each fp64 candidate parameter to).  OpenES: one Box-Muller pair per
 // thread, shared by the mirrored agents.

@@ -27,7 +27,7 @@ from ._lib import check
 __all__ = ["EsConfig", "EsWorkflow", "StepMetrics", "batched_rollout", "gaussian_matrix",
            "centered_ranks", "rank_desc", "openes_ask", "openes_tell", "ars_ask", "ars_tell",
            "env_step_batch", "threefry2x64", "stream_words", "param_count", "mlp_desc",
-           "measure_fp64_peak", "sym_eig"]
+           "measure_fp64_peak", "measure_noise_rate", "sym_eig"]
 
 
 def _p(a: np.ndarray):
@@ -582,6 +582,13 @@ def sym_eig(A):
     sw = C.c_int32()
     check(_lib.load().evorl_sym_eig(_p(A), n, _p(ev), _p(V), C.byref(sw)))
     return ev, V, sw.value
+
+
+def measure_noise_rate(n: int = 1 << 27) -> float:
+    """Normals/s of the ask's noise generator at full occupancy (n normals)."""
+    ms = C.c_float()
+    check(_lib.load().evorl_measure_noise_rate(int(n), C.byref(ms)))
+    return n / (ms.value * 1e-3)
 
 
 def measure_fp64_peak() -> float:

@@ -482,10 +482,12 @@ def test_chunked_materialised_ask_is_identical(evb):
 
 def test_tell_from_kept_noise_rows_is_identical(evb):
     """The OpenES tell reads the noise rows the ask kept (one rank
-    materialising every row) instead of regenerating them: the updated mean is
-    bit-identical to the regenerating tell (EVORL_EPS_ROWS_CAP_BYTES=0 in a
-    child process) on the warp, fp64-team, tc-team and oz-team paths,
-    mirrored or not, and with a chunked materialised ask."""
+    materialising every row) instead of regenerating them, and the next
+    generation's rows are generated beside the current rollout: the updated
+    mean is bit-identical to the regenerating tell (EVORL_EPS_ROWS_CAP_BYTES=0
+    in a child process) and to the ask generating its own noise
+    (EVORL_NO_NOISE_AHEAD=1) on the warp, fp64-team, tc-team and oz-team
+    paths, mirrored or not, and with a chunked materialised ask."""
     import subprocess
     import sys
     code = ("import numpy as np, paper_2501_15129_b200 as evb\n"
@@ -497,7 +499,8 @@ def test_tell_from_kept_noise_rows_is_identical(evb):
             "    for _ in range(3): g.step()\n"
             "    print('MEAN', g.mean().tobytes().hex())\n")
     outs = []
-    for env_kv in ({}, {"EVORL_EPS_ROWS_CAP_BYTES": "0"}, {"EVORL_CAND_CAP_BYTES": str(5 * 67073 * 8)}):
+    for env_kv in ({}, {"EVORL_EPS_ROWS_CAP_BYTES": "0"}, {"EVORL_CAND_CAP_BYTES": str(5 * 67073 * 8)},
+                   {"EVORL_NO_NOISE_AHEAD": "1"}):
         env = dict(os.environ)
         env.update(env_kv)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
@@ -506,6 +509,7 @@ def test_tell_from_kept_noise_rows_is_identical(evb):
     assert len(outs[0]) == 6
     assert outs[0] == outs[1]
     assert outs[0] == outs[2]  # (the oz rows in 5-agent chunks)
+    assert outs[0] == outs[3]  # noise generated at the ask, not beside the previous rollout
 
 
 @pytest.mark.parametrize("mirrored", [True, False])
