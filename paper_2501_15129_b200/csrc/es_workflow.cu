@@ -752,6 +752,18 @@ static double* eps_next_buffer(evorl_es* s) {
   return s->d_eps_next;
 }
 
+static long long rows_of(const evorl_es* s) { return s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop; }
+static int sms_of(evorl_es* s) {
+  if (s->n_sms <= 0 && cudaDeviceGetAttribute(&s->n_sms, cudaDevAttrMultiProcessorCount, s->cfg.device) != cudaSuccess)
+    s->n_sms = 148;
+  return s->n_sms;
+}
+// EVORL_NO_FUSED_ASK=1: the oz ask as materialise + pre-split (used by the tests)
+static bool no_fused_ask() {
+  static const bool off = getenv("EVORL_NO_FUSED_ASK") && atoi(getenv("EVORL_NO_FUSED_ASK")) != 0;
+  return off;
+}
+
 static RolloutArgs rollout_args(const evorl_es* s) {
   RolloutArgs a{};
   a.env = s->env;
@@ -937,7 +949,14 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
           ac.tc_block_bytes = tc_block_bytes(s->plan.tcp);
         }
       } else {
-        if (kept) {
+        const bool fused = s->d_tc_blocks && er && whole && !no_fused_ask();
+        if (fused) {
+          // oz: the ask fused with the pre-split from the noise rows (generated
+          // here on the first generation, else kept from beside the last rollout)
+          if (!kept) CK(run_noise_rows(s->ask_key, rows_of(s) * s->d, er, 16 * sms_of(s), s->stream));
+          CK(run_oz_ask_split(a.par, s->net, s->plan.tcp, c0, c1, er, s->d_cand, s->d_tc_blocks, s->stream));
+          count_launch();
+        } else if (kept) {
           CK(run_cand_from_eps(a.par, s->d, c0, c1, er, s->d_cand, s->stream));
         } else {
           CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream, er));
@@ -946,8 +965,10 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
         ac.par.src = SRC_EXPLICIT;
         ac.par.params = s->d_cand;
         if (s->d_tc_blocks) {  // the oz team's layer-1 weights, pre-split into fixed-point byte slices
-          CK(run_oz_split(s->d_cand, s->net, s->plan.tcp, c1 - c0, s->d_tc_blocks, s->stream));
-          count_launch();
+          if (!fused) {
+            CK(run_oz_split(s->d_cand, s->net, s->plan.tcp, c1 - c0, s->d_tc_blocks, s->stream));
+            count_launch();
+          }
           ac.tc_blocks = s->d_tc_blocks;
           ac.tc_block_bytes = oz_block_bytes(s->plan.tcp);
         }

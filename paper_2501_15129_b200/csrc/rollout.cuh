@@ -227,5 +227,11 @@ long long oz_block_bytes(const TcPlanOut& plan);
 // the fp64 candidates [n_agents x d] -> pre-split blocks [n_agents][C]
 cudaError_t run_oz_split(const double* cand, const NetDesc& net, const TcPlanOut& plan, int n_agents,
                          unsigned char* blocks, cudaStream_t stream);
+// The OpenES ask of agents [a0, a1) fused with the pre-split, from kept noise
+// rows eps (row-major, d per row): the layer-1 byte-slice blocks (identical to
+// run_materialize + run_oz_split), the other parameters into cand, and the
+// fp64 layer-1 row of cand only where it holds a non-finite weight.
+cudaError_t run_oz_ask_split(const ParamDesc& par, const NetDesc& net, const TcPlanOut& po, int a0, int a1,
+                             const double* eps, double* cand, unsigned char* blocks, cudaStream_t stream);
 
 }  // namespace evorl_b200

@@ -38,6 +38,7 @@
 //   * Rows holding a non-finite weight (a diverged mean) are computed by an
 //     fp64 dot product instead (IEEE propagation and NetFault as the fp64 team).
 #include <algorithm>
+#include <climits>
 #include <cstring>
 
 #include "rollout.cuh"
@@ -186,6 +187,31 @@ EVB_DEV void oz_slice32(const double* w, double wscale, uint32_t (&out)[S][8]) {
     const bool H = Pb >= 32;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
+      const uint32_t v = gather_byte(H ? hi[4 * u] : lo[4 * u], H ? hi[4 * u + 1] : lo[4 * u + 1],
+                                     H ? hi[4 * u + 2] : lo[4 * u + 2], H ? hi[4 * u + 3] : lo[4 * u + 3],
+                                     (Pb & 31) >> 3);
+      out[i][u] = i == 0 ? v ^ 0x80808080u : v;
+    }
+  }
+}
+// The same for 16 consecutive weights: out[i] holds bytes 0..15 of slice i's
+// 32-byte record half (k order as oz_slice32).
+template <int S>
+EVB_DEV void oz_slice16(const double* w, double wscale, uint32_t (&out)[S][4]) {
+  const double off = 0x1p52 + (double)(1ull << (8 * S - 1));
+  uint32_t lo[16], hi[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const double t = __fma_rz(isfinite(w[q]) ? w[q] : 0.0, wscale, off);
+    lo[q] = (uint32_t)__double2loint(t);
+    hi[q] = (uint32_t)__double2hiint(t);
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    const int Pb = 8 * (S - 1 - i);
+    const bool H = Pb >= 32;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
       const uint32_t v = gather_byte(H ? hi[4 * u] : lo[4 * u], H ? hi[4 * u + 1] : lo[4 * u + 1],
                                      H ? hi[4 * u + 2] : lo[4 * u + 2], H ? hi[4 * u + 3] : lo[4 * u + 3],
                                      (Pb & 31) >> 3);
@@ -857,6 +883,141 @@ __global__ void k_oz_split(const double* __restrict__ cand, long long d, long lo
     }
   }
   reinterpret_cast<int*>(blk + (size_t)S * W1p * OZ_M)[row] = (Fr & 0xFFFF) | ((ok && !fin) ? (1 << 16) : 0);
+}
+
+// The OpenES ask fused with the pre-split, from kept noise rows: a block owns
+// noise row nr, one CTA's 16-row tile of layer 1, and both agents using the row
+// (nr, and nr + base negated when mirrored).  Thread group h holds the k-range
+// [16h, 16h + 16) of every row of the tile: the noise and the mean are read
+// once, each agent's weights w = sigma (+-eps) + mean are formed in registers
+// (the ask's arithmetic), and the row maximum, exponent and byte slices follow
+// as in k_oz_split -- no fp64 layer-1 candidate matrix is written or re-read.
+// Rows holding a non-finite weight (a diverged mean) also get their fp64
+// values in the candidate matrix: only those are read back by the team.
+constexpr int OZ_AS_ROWS = 16;  // rows per block: 16 x 16 half-chunks = 256 threads, two blocks per SM
+template <int S>
+__global__ void __launch_bounds__(256, 2) k_oz_ask_split(const ParamDesc P, long long d, long long w_off1, int W1,
+                                                      int W2, int W1p, int C, int a0, int a1, long long r0,
+                                                      const double* __restrict__ eps, double* __restrict__ cand,
+                                                      unsigned char* __restrict__ blocks, long long block_bytes) {
+  __shared__ double smax[16][OZ_AS_ROWS];
+  __shared__ int sfin[16][OZ_AS_ROWS];
+  constexpr int TPB = OZ_M / OZ_AS_ROWS;
+  const int lane = threadIdx.x % OZ_AS_ROWS, h = threadIdx.x / OZ_AS_ROWS;
+  const int tile = (int)(blockIdx.x % TPB);
+  const long long rc = blockIdx.x / TPB;
+  const int crank = (int)(rc % C);
+  const long long nr = r0 + rc / C;  // noise row
+  const int row = tile * OZ_AS_ROWS + lane, r = crank * OZ_M + row;
+  const bool ok = r < W2;
+  const int nh = W1p / 16;  // k half-chunks in use
+  double e[16], m[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int k = h * 16 + q;
+    const bool v = h < nh && ok && k < W1;
+    const long long p = w_off1 + (long long)k * W2 + r;
+    e[q] = v ? eps[nr * d + p] : 0.0;
+    m[q] = v ? P.mean[p] : 0.0;
+  }
+  for (int side = 0; side < 2; ++side) {
+    const long long a = side == 0 ? nr : (P.mirrored ? nr + P.base : -1);
+    if (a < a0 || a >= a1) continue;  // uniform over the block
+    double w[16];
+    double rm = 0.0;
+    bool fin = true;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int k = h * 16 + q;
+      const bool v = h < nh && ok && k < W1;
+      w[q] = v ? dadd(dmul(P.sigma, side ? -e[q] : e[q]), m[q]) : 0.0;  // (sigma * eps) + mean
+      rm = fmax(rm, fin_abs(w[q]));
+      fin = fin && isfinite(w[q]);
+    }
+    __syncthreads();  // the previous side's reduction was read
+    smax[h][lane] = rm;
+    sfin[h][lane] = fin ? 1 : 0;
+    __syncthreads();
+    for (int j = 0; j < nh; ++j) {
+      rm = fmax(rm, smax[j][lane]);
+      fin = fin && sfin[j][lane] != 0;
+    }
+    const int Fr = 8 * S - 1 - bound_exp(rm);
+    unsigned char* blk = blocks + ((a - a0) * C + crank) * block_bytes;
+    if (h < nh) {
+      uint32_t sl[S][4];
+      oz_slice16<S>(w, ldexp(1.0, Fr), sl);
+#pragma unroll
+      for (int i = 0; i < S; ++i)
+        *reinterpret_cast<uint4*>(blk + (((size_t)i * (W1p / 32) + (h >> 1)) * OZ_M + row) * 32 + (h & 1) * 16) =
+            make_uint4(sl[i][0], sl[i][1], sl[i][2], sl[i][3]);
+      if (!fin && ok) {  // the team computes this row in fp64 from the candidate matrix
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int k = h * 16 + q;
+          if (k < W1) cand[(a - a0) * d + w_off1 + (long long)k * W2 + r] = w[q];
+        }
+      }
+    }
+    if (h == 0)
+      reinterpret_cast<int*>(blk + (size_t)S * W1p * OZ_M)[row] = (Fr & 0xFFFF) | ((ok && !fin) ? (1 << 16) : 0);
+  }
+}
+
+// The other parameters (outside layer 1) of agents [a0, a1) from the kept
+// noise rows, as k_cand_from_eps.
+__global__ void k_oz_ask_rest(const ParamDesc P, long long d, long long w_off1, long long n_w1, int a0, int a1,
+                              long long r0, long long rows, const double* __restrict__ eps, double* __restrict__ cand) {
+  const long long rest = d - n_w1;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= rows * rest) return;
+  const long long nr = r0 + i / rest, j = i % rest;
+  const long long p = j < w_off1 ? j : j + n_w1;
+  const double e = eps[nr * d + p], mp = P.mean[p];
+  for (int side = 0; side < 2; ++side) {
+    const long long a = side == 0 ? nr : (P.mirrored ? nr + P.base : -1);
+    if (a < a0 || a >= a1) continue;
+    cand[(a - a0) * d + p] = dadd(dmul(P.sigma, side ? -e : e), mp);
+  }
+}
+
+cudaError_t run_oz_ask_split(const ParamDesc& par, const NetDesc& net, const TcPlanOut& po, int a0, int a1,
+                             const double* eps, double* cand, unsigned char* blocks, cudaStream_t stream) {
+  OzPlan p;
+  std::memcpy(&p, &po, sizeof p);
+  if (par.src != SRC_OPENES || p.W1p > 256 || p.W1p % 16) return cudaErrorInvalidValue;
+  if (a1 <= a0) return cudaSuccess;
+  // noise rows the agents use (agent a < base: row a; a >= base: row a - base)
+  long long r0 = a0, r1 = a1;
+  if (par.mirrored) {
+    const long long base = par.base;
+    r0 = LLONG_MAX;
+    r1 = LLONG_MIN;
+    if (a0 < base) {
+      r0 = std::min<long long>(r0, a0);
+      r1 = std::max<long long>(r1, std::min<long long>(a1, base));
+    }
+    if (a1 > base) {
+      r0 = std::min<long long>(r0, std::max<long long>(a0, base) - base);
+      r1 = std::max<long long>(r1, a1 - base);
+    }
+  }
+  const long long rows = r1 - r0;
+  const long long n_w1 = (long long)p.W1 * p.W2;
+  const long long bb = oz_block_bytes(po);
+  k_oz_ask_rest<<<(unsigned)((rows * (net.d - n_w1) + 255) / 256), 256, 0, stream>>>(
+      par, net.d, net.w_off[1], n_w1, a0, a1, r0, rows, eps, cand);
+  const unsigned grid = (unsigned)(rows * p.C * (OZ_M / OZ_AS_ROWS));
+#ifdef EVB_OZ_S5
+  if (p.S == 5) {
+    k_oz_ask_split<5><<<grid, 16 * OZ_AS_ROWS, 0, stream>>>(par, net.d, net.w_off[1], p.W1, p.W2, p.W1p, p.C, a0, a1, r0, eps,
+                                                cand, blocks, bb);
+    return cudaGetLastError();
+  }
+#endif
+  k_oz_ask_split<6><<<grid, 16 * OZ_AS_ROWS, 0, stream>>>(par, net.d, net.w_off[1], p.W1, p.W2, p.W1p, p.C, a0, a1, r0, eps,
+                                              cand, blocks, bb);
+  return cudaGetLastError();
 }
 
 cudaError_t run_oz_split(const double* cand, const NetDesc& net, const TcPlanOut& po, int n_agents,

@@ -486,8 +486,9 @@ def test_tell_from_kept_noise_rows_is_identical(evb):
     generation's rows are generated beside the current rollout: the updated
     mean is bit-identical to the regenerating tell (EVORL_EPS_ROWS_CAP_BYTES=0
     in a child process) and to the ask generating its own noise
-    (EVORL_NO_NOISE_AHEAD=1) on the warp, fp64-team, tc-team and oz-team
-    paths, mirrored or not, and with a chunked materialised ask."""
+    (EVORL_NO_NOISE_AHEAD=1), and the oz team's fused ask + pre-split to the
+    separate passes (EVORL_NO_FUSED_ASK=1), on the warp, fp64-team, tc-team
+    and oz-team paths, mirrored or not, and with a chunked materialised ask."""
     import subprocess
     import sys
     code = ("import numpy as np, paper_2501_15129_b200 as evb\n"
@@ -500,7 +501,7 @@ def test_tell_from_kept_noise_rows_is_identical(evb):
             "    print('MEAN', g.mean().tobytes().hex())\n")
     outs = []
     for env_kv in ({}, {"EVORL_EPS_ROWS_CAP_BYTES": "0"}, {"EVORL_CAND_CAP_BYTES": str(5 * 67073 * 8)},
-                   {"EVORL_NO_NOISE_AHEAD": "1"}):
+                   {"EVORL_NO_NOISE_AHEAD": "1"}, {"EVORL_NO_FUSED_ASK": "1"}):
         env = dict(os.environ)
         env.update(env_kv)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
@@ -510,6 +511,7 @@ def test_tell_from_kept_noise_rows_is_identical(evb):
     assert outs[0] == outs[1]
     assert outs[0] == outs[2]  # (the oz rows in 5-agent chunks)
     assert outs[0] == outs[3]  # noise generated at the ask, not beside the previous rollout
+    assert outs[0] == outs[4]  # oz: materialise + pre-split instead of the fused ask
 
 
 @pytest.mark.parametrize("mirrored", [True, False])
