@@ -911,14 +911,12 @@ __global__ void __launch_bounds__(256, 2) k_oz_ask_split(const ParamDesc P, long
   const int row = tile * OZ_AS_ROWS + lane, r = crank * OZ_M + row;
   const bool ok = r < W2;
   const int nh = W1p / 16;  // k half-chunks in use
-  double e[16], m[16];
+  double e[16];  // the mean is re-read per side (L1): fewer registers, more resident blocks
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int k = h * 16 + q;
     const bool v = h < nh && ok && k < W1;
-    const long long p = w_off1 + (long long)k * W2 + r;
-    e[q] = v ? eps[nr * d + p] : 0.0;
-    m[q] = v ? P.mean[p] : 0.0;
+    e[q] = v ? eps[nr * d + w_off1 + (long long)k * W2 + r] : 0.0;
   }
   for (int side = 0; side < 2; ++side) {
     const long long a = side == 0 ? nr : (P.mirrored ? nr + P.base : -1);
@@ -930,7 +928,8 @@ __global__ void __launch_bounds__(256, 2) k_oz_ask_split(const ParamDesc P, long
     for (int q = 0; q < 16; ++q) {
       const int k = h * 16 + q;
       const bool v = h < nh && ok && k < W1;
-      w[q] = v ? dadd(dmul(P.sigma, side ? -e[q] : e[q]), m[q]) : 0.0;  // (sigma * eps) + mean
+      w[q] = v ? dadd(dmul(P.sigma, side ? -e[q] : e[q]), P.mean[w_off1 + (long long)k * W2 + r])
+               : 0.0;  // (sigma * eps) + mean
       rm = fmax(rm, fin_abs(w[q]));
       fin = fin && isfinite(w[q]);
     }
