@@ -472,7 +472,9 @@ def main():
                "in_generation": "k_noise_rows beside the previous generation's rollout (one block per SM on a "
                                 "low-priority stream), off the critical path",
                "ask_on_path_ms": ask_ms,
-               "ask_on_path": "k_cand_from_eps: candidates = mean + sigma * kept noise rows (HBM-bound)"}
+               "ask_on_path": ("k_oz_ask_split: the ask fused with the layer-1 pre-split from the kept noise rows"
+                               if eff_prec == "oz" else
+                               "k_cand_from_eps: candidates = mean + sigma * kept noise rows (HBM-bound)")}
 
     # ---- the other policy precisions on the same workload, beside the headline:
     # f64 (DMMA team, the bit-level parity path) and tc (fp32-accurate tcgen05
