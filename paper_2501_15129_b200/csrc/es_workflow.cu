@@ -203,6 +203,7 @@ struct evorl_es {
   double* d_eps_next = nullptr;
   bool eps_next_valid = false, eps_next_failed = false;
   DKey eps_next_key{};
+  long long eps_next_r0 = 0, eps_next_r1 = 0;  // rows the kept-ahead buffer holds
   cudaStream_t side = nullptr;
   cudaEvent_t ev_noise = nullptr;
   int n_sms = 0;
@@ -709,13 +710,13 @@ static int check_ask(const evorl_es* s) {  // the ask-side argument checks
   return EVORL_OK;
 }
 
-// The buffer the ask keeps this generation's OpenES noise rows in, or null
-// (regenerated by the tell): only when this rank materialises every sampled
-// row (unsharded), regenerated-noise mode, under a 4 GiB cap
-// (EVORL_EPS_ROWS_CAP_BYTES overrides it; 0 disables -- used by the tests).
+// The buffer the ask keeps this generation's OpenES noise rows in (the rows
+// this rank's agents use, from its first row on), or null: regenerated-noise
+// mode, under a 4 GiB cap (EVORL_EPS_ROWS_CAP_BYTES overrides it; 0 disables
+// -- used by the tests).  The tell reads it only when the rank holds every
+// row (unsharded); sharded, the tell regenerates its coordinate slice.
 static double* eps_rows_buffer(evorl_es* s) {
   if (s->cfg.algo != EVORL_ALGO_OPENES || s->d_table || s->eps_rows_failed) return nullptr;
-  if (s->a0 != 0 || s->a1 != s->cfg.pop) return nullptr;
   static const double kCap =
       getenv("EVORL_EPS_ROWS_CAP_BYTES") ? atof(getenv("EVORL_EPS_ROWS_CAP_BYTES")) : 4.0 * (1ull << 30);
   const long long rows = s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop;
@@ -899,11 +900,13 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
     // small policy: materialise the shard's candidates (fully parallel ask),
     // then one warp per lane with the weights resident in shared memory
     double* er = a.par.src == SRC_OPENES ? eps_rows_buffer(s) : nullptr;
+    long long r0 = 0, r1 = 0;
+    if (er) openes_row_range(a.par, s->a0, s->a1, &r0, &r1);
     CK(cudaEventRecord(s->ev_a0, s->stream));
-    CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream, er));
+    CK(run_materialize(a.par, s->d, s->a0, s->a1, s->d_cand, s->stream, er, r0));
     CK(cudaEventRecord(s->ev_a1, s->stream));
     s->ask_timed = true;
-    s->eps_rows_valid = er != nullptr;
+    s->eps_rows_valid = er != nullptr && r0 == 0 && r1 == rows_of(s);
     count_launch();
     a.par.src = SRC_EXPLICIT;
     a.par.params = s->d_cand;
@@ -913,10 +916,12 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
     // team path: materialise the shard's candidates (chunks of cand_cap
     // agents), then roll each chunk out
     double* er = a.par.src == SRC_OPENES ? eps_rows_buffer(s) : nullptr;
+    long long r0 = 0, r1 = 0;  // noise rows of this shard: er holds rows [r0, r1)
+    if (er) openes_row_range(a.par, s->a0, s->a1, &r0, &r1);
     const bool whole = s->cand_cap >= s->a1 - s->a0;  // one materialised chunk
     bool kept = false;  // this ask's noise rows were generated beside the last rollout
     if (er && whole && s->eps_next_valid && s->eps_next_key.hi == s->ask_key.hi &&
-        s->eps_next_key.lo == s->ask_key.lo) {
+        s->eps_next_key.lo == s->ask_key.lo && s->eps_next_r0 == r0 && s->eps_next_r1 == r1) {
       CK(cudaStreamWaitEvent(s->stream, s->ev_noise, 0));
       std::swap(s->d_eps_rows, s->d_eps_next);
       er = s->d_eps_rows;
@@ -935,9 +940,9 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
       if (one_chunk) CK(cudaEventRecord(s->ev_a0, s->stream));
       if (s->d_cand_f32) {
         if (kept) {
-          CK(run_cand_from_eps_f32(a.par, s->d, c0, c1, er, s->d_cand_f32, s->stream));
+          CK(run_cand_from_eps_f32(a.par, s->d, c0, c1, er, r0, s->d_cand_f32, s->stream));
         } else {
-          CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream, er));
+          CK(run_materialize_f32(a.par, s->d, c0, c1, s->d_cand_f32, s->stream, er, r0));
         }
         if (one_chunk) CK(cudaEventRecord(s->ev_a1, s->stream));
         ac.par.src = SRC_EXPLICIT_F32;
@@ -953,13 +958,13 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
         if (fused) {
           // oz: the ask fused with the pre-split from the noise rows (generated
           // here on the first generation, else kept from beside the last rollout)
-          if (!kept) CK(run_noise_rows(s->ask_key, rows_of(s) * s->d, er, 16 * sms_of(s), s->stream));
-          CK(run_oz_ask_split(a.par, s->net, s->plan.tcp, c0, c1, er, s->d_cand, s->d_tc_blocks, s->stream));
+          if (!kept) CK(run_noise_rows(s->ask_key, r0 * s->d, (r1 - r0) * s->d, er, 16 * sms_of(s), s->stream));
+          CK(run_oz_ask_split(a.par, s->net, s->plan.tcp, c0, c1, er, r0, s->d_cand, s->d_tc_blocks, s->stream));
           count_launch();
         } else if (kept) {
-          CK(run_cand_from_eps(a.par, s->d, c0, c1, er, s->d_cand, s->stream));
+          CK(run_cand_from_eps(a.par, s->d, c0, c1, er, r0, s->d_cand, s->stream));
         } else {
-          CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream, er));
+          CK(run_materialize(a.par, s->d, c0, c1, s->d_cand, s->stream, er, r0));
         }
         if (one_chunk) CK(cudaEventRecord(s->ev_a1, s->stream));
         ac.par.src = SRC_EXPLICIT;
@@ -979,17 +984,19 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
       CK(launch_rollout(ac, s->cfg.precision, s->stream));
       count_launch();
     }
-    s->eps_rows_valid = er != nullptr && s->a1 > s->a0;
+    // the tell reads the kept rows only when they are every row (unsharded)
+    s->eps_rows_valid = er != nullptr && s->a1 > s->a0 && r0 == 0 && r1 == rows_of(s);
     if (er && whole && s->a1 > s->a0) {
       if (double* nx = eps_next_buffer(s)) {  // the next generation's noise, beside this rollout
-        const long long rows = s->cfg.openes_mirrored ? s->cfg.pop / 2 : s->cfg.pop;
         const DKey next = fold_in(fold_in(fold_in(s->rng, 0), (uint64_t)(s->iteration + 1)), 0);
         CK(cudaStreamWaitEvent(s->side, s->ev_r0, 0));
-        CK(run_noise_rows(next, rows * s->d, nx, s->n_sms, s->side));
+        CK(run_noise_rows(next, r0 * s->d, (r1 - r0) * s->d, nx, s->n_sms, s->side));
         CK(cudaEventRecord(s->ev_noise, s->side));
         count_launch();
         s->eps_next_valid = true;
         s->eps_next_key = next;
+        s->eps_next_r0 = r0;
+        s->eps_next_r1 = r1;
       }
     }
   }
@@ -1877,9 +1884,9 @@ extern "C" int evorl_measure_noise_rate(int64_t n, float* ms) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   const DKey key{0x9E3779B97F4A7C15ull, 0xBB67AE8584CAA73Bull};
-  cudaError_t err = run_noise_rows(key, n, eps, 16 * sms, 0);
+  cudaError_t err = run_noise_rows(key, 0, n, eps, 16 * sms, 0);
   if (err == cudaSuccess) err = cudaEventRecord(e0, 0);
-  if (err == cudaSuccess) err = run_noise_rows(key, n, eps, 16 * sms, 0);
+  if (err == cudaSuccess) err = run_noise_rows(key, 0, n, eps, 16 * sms, 0);
   if (err == cudaSuccess) err = cudaEventRecord(e1, 0);
   if (err == cudaSuccess) err = cudaEventSynchronize(e1);
   if (err == cudaSuccess) err = cudaEventElapsedTime(ms, e0, e1);

@@ -95,7 +95,7 @@ __global__ void k_materialize_f32(const ParamDesc P, long long d, int a0, int a1
 // regenerating the Box-Muller pairs).
 template <typename T>
 __global__ void k_materialize_openes(const ParamDesc P, long long d, int a0, int a1, long long t0, long long t1,
-                                     T* out, double* eps_out) {
+                                     T* out, double* eps_out, long long e0) {
   const long long b = (t0 >> 1) + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (2 * b >= t1) return;
   double c, sn;
@@ -111,13 +111,9 @@ __global__ void k_materialize_openes(const ParamDesc P, long long d, int a0, int
     row2b = (2 * b) / d;
     p2b = 2 * b - row2b * d;
   }
-  if (eps_out) {
-    if (2 * b >= t0 && 2 * b + 1 < t1)
-      reinterpret_cast<double2*>(eps_out)[b] = make_double2(c, sn);
-    else if (2 * b >= t0)
-      eps_out[2 * b] = c;
-    else
-      eps_out[2 * b + 1] = sn;
+  if (eps_out) {  // entry t at eps_out[t - e0] (the buffer's first row need not be row 0)
+    if (2 * b >= t0) eps_out[2 * b - e0] = c;
+    if (2 * b + 1 < t1) eps_out[2 * b + 1 - e0] = sn;
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -165,7 +161,7 @@ static void openes_rows(const ParamDesc& par, int a0, int a1, long long& r0, lon
 
 template <typename T>
 static cudaError_t materialize(const ParamDesc& par, long long d, int a0, int a1, T* out, cudaStream_t stream,
-                               double* eps_out = nullptr) {
+                               double* eps_out = nullptr, long long eps_row0 = 0) {
   const long long n = (long long)(a1 - a0) * d;
   if (n <= 0) return cudaSuccess;
   if (par.src == SRC_OPENES) {
@@ -173,8 +169,9 @@ static cudaError_t materialize(const ParamDesc& par, long long d, int a0, int a1
     openes_rows(par, a0, a1, r0, r1);
     const long long t0 = r0 * d, t1 = r1 * d;
     const long long blocks = ((t1 + 1) >> 1) - (t0 >> 1);
+    if (eps_out && r0 < eps_row0) return cudaErrorInvalidValue;
     k_materialize_openes<T><<<(unsigned)((blocks + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1, out,
-                                                                                     eps_out);
+                                                                                     eps_out, eps_row0 * d);
     return cudaGetLastError();
   }
   if constexpr (sizeof(T) == 4) {
@@ -186,14 +183,14 @@ static cudaError_t materialize(const ParamDesc& par, long long d, int a0, int a1
 }
 
 cudaError_t run_materialize_f32(const ParamDesc& par, long long d, int a0, int a1, float* out,
-                                cudaStream_t stream, double* eps_out) {
+                                cudaStream_t stream, double* eps_out, long long eps_row0) {
   if (eps_out && par.src != SRC_OPENES) return cudaErrorInvalidValue;
-  return materialize(par, d, a0, a1, out, stream, eps_out);
+  return materialize(par, d, a0, a1, out, stream, eps_out, eps_row0);
 }
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
-                            cudaStream_t stream, double* eps_out) {
+                            cudaStream_t stream, double* eps_out, long long eps_row0) {
   if (eps_out && par.src != SRC_OPENES) return cudaErrorInvalidValue;
-  return materialize(par, d, a0, a1, out, stream, eps_out);
+  return materialize(par, d, a0, a1, out, stream, eps_out, eps_row0);
 }
 
 // ------------------------------------------------ OpenES noise kept ahead
@@ -202,22 +199,21 @@ cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, d
 // rollout (one team CTA per SM leaves room for exactly one such block), it
 // fills the next generation's noise rows while the current one rolls out.
 constexpr int NOISE_T = 128;
-__global__ void __launch_bounds__(NOISE_T) k_noise_rows(DKey key, long long n, double* __restrict__ eps) {
-  const long long pairs = (n + 1) >> 1;
+__global__ void __launch_bounds__(NOISE_T) k_noise_rows(DKey key, long long t0, long long t1,
+                                                        double* __restrict__ eps) {
+  const long long b0 = t0 >> 1, pairs = ((t1 + 1) >> 1) - b0;
   const long long stride = (long long)gridDim.x * NOISE_T;
-  for (long long b = blockIdx.x * (long long)NOISE_T + threadIdx.x; b < pairs; b += stride) {
+  for (long long i = blockIdx.x * (long long)NOISE_T + threadIdx.x; i < pairs; i += stride) {
+    const long long b = b0 + i;
     double c, sn;
     normal_pair(key, (uint64_t)b, c, sn);
-    if (2 * b + 1 < n) {
-      reinterpret_cast<double2*>(eps)[b] = make_double2(c, sn);
-    } else {
-      eps[2 * b] = c;
-    }
+    if (2 * b >= t0) eps[2 * b - t0] = c;
+    if (2 * b + 1 < t1) eps[2 * b + 1 - t0] = sn;
   }
 }
-cudaError_t run_noise_rows(DKey key, long long n, double* eps, int blocks, cudaStream_t stream) {
+cudaError_t run_noise_rows(DKey key, long long t0, long long n, double* eps, int blocks, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  k_noise_rows<<<(unsigned)std::max(1, blocks), NOISE_T, 0, stream>>>(key, n, eps);
+  k_noise_rows<<<(unsigned)std::max(1, blocks), NOISE_T, 0, stream>>>(key, t0, t0 + n, eps);
   return cudaGetLastError();
 }
 
@@ -227,7 +223,7 @@ cudaError_t run_noise_rows(DKey key, long long n, double* eps, int blocks, cudaS
 // computes, without regenerating the normals.
 template <typename T>
 __global__ void k_cand_from_eps(const ParamDesc P, long long d, int a0, int a1, long long t0, long long t1,
-                                const double* __restrict__ eps, T* __restrict__ out) {
+                                const double* __restrict__ eps, long long e0, T* __restrict__ out) {
   const long long t = t0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= t1) return;
   long long row, p;
@@ -239,7 +235,7 @@ __global__ void k_cand_from_eps(const ParamDesc P, long long d, int a0, int a1, 
     row = t / d;
     p = t - row * d;
   }
-  const double e = eps[t];
+  const double e = eps[t - e0];
   const double m = P.mean[p];
   const int ag[2] = {(int)row, P.mirrored ? (int)row + P.base : -1};
 #pragma unroll
@@ -255,23 +251,28 @@ __global__ void k_cand_from_eps(const ParamDesc P, long long d, int a0, int a1, 
   }
 }
 template <typename T>
-static cudaError_t cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps, T* out,
-                                 cudaStream_t stream) {
+static cudaError_t cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
+                                 long long eps_row0, T* out, cudaStream_t stream) {
   if (par.src != SRC_OPENES) return cudaErrorInvalidValue;
   if (a1 <= a0) return cudaSuccess;
   long long r0, r1;
   openes_rows(par, a0, a1, r0, r1);
+  if (r0 < eps_row0) return cudaErrorInvalidValue;
   const long long t0 = r0 * d, t1 = r1 * d;
-  k_cand_from_eps<T><<<(unsigned)((t1 - t0 + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1, eps, out);
+  k_cand_from_eps<T><<<(unsigned)((t1 - t0 + 255) / 256), 256, 0, stream>>>(par, d, a0, a1, t0, t1, eps,
+                                                                             eps_row0 * d, out);
   return cudaGetLastError();
 }
-cudaError_t run_cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps, double* out,
-                              cudaStream_t stream) {
-  return cand_from_eps(par, d, a0, a1, eps, out, stream);
+cudaError_t run_cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
+                              long long eps_row0, double* out, cudaStream_t stream) {
+  return cand_from_eps(par, d, a0, a1, eps, eps_row0, out, stream);
 }
 cudaError_t run_cand_from_eps_f32(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
-                                  float* out, cudaStream_t stream) {
-  return cand_from_eps(par, d, a0, a1, eps, out, stream);
+                                  long long eps_row0, float* out, cudaStream_t stream) {
+  return cand_from_eps(par, d, a0, a1, eps, eps_row0, out, stream);
+}
+void openes_row_range(const ParamDesc& par, int a0, int a1, long long* r0, long long* r1) {
+  openes_rows(par, a0, a1, *r0, *r1);
 }
 
 template <typename T, int N>

@@ -187,25 +187,29 @@ cudaError_t launch_rollout_warp(const RolloutArgs& a, const WarpPlanOut& plan, i
                                 cudaStream_t stream);
 // Materialise candidates [a0, a1) (row-major, d each) from a ParamDesc.
 // SRC_OPENES only: eps_out (optional) receives the sampled noise entries of
-// the rows these agents use, at their stream index row * d + p.
+// the rows these agents use, entry (row, p) at eps_out[(row - eps_row0) d + p].
 cudaError_t run_materialize(const ParamDesc& par, long long d, int a0, int a1, double* out,
-                            cudaStream_t stream, double* eps_out = nullptr);
+                            cudaStream_t stream, double* eps_out = nullptr, long long eps_row0 = 0);
+// The OpenES noise rows [r0, r1) agents [a0, a1) use (row a, or a - base
+// for the mirrored half).
+void openes_row_range(const ParamDesc& par, int a0, int a1, long long* r0, long long* r1);
 
-// OpenES noise kept ahead of the ask: normals [0, n) of the ask stream `key`
-// into eps (persistent grid of `blocks` 128-thread blocks, sized to share the
-// SMs with a resident rollout), and the ask's candidates from such rows
-// (bit-identical to run_materialize / run_materialize_f32 for SRC_OPENES).
-cudaError_t run_noise_rows(DKey key, long long n, double* eps, int blocks, cudaStream_t stream);
-cudaError_t run_cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps, double* out,
-                              cudaStream_t stream);
+// OpenES noise kept ahead of the ask: normals [t0, t0 + n) of the ask stream
+// `key` into eps[t - t0] (persistent grid of `blocks` 128-thread blocks, sized
+// to share the SMs with a resident rollout), and the ask's candidates from
+// such rows, eps holding rows from eps_row0 on (bit-identical to
+// run_materialize / run_materialize_f32 for SRC_OPENES).
+cudaError_t run_noise_rows(DKey key, long long t0, long long n, double* eps, int blocks, cudaStream_t stream);
+cudaError_t run_cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
+                              long long eps_row0, double* out, cudaStream_t stream);
 cudaError_t run_cand_from_eps_f32(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
-                                  float* out, cudaStream_t stream);
+                                  long long eps_row0, float* out, cudaStream_t stream);
 
 // Materialise candidates [a0, a1) as fp32 (the value the fp32 policy paths
 // round each fp64 candidate parameter to).  OpenES: one Box-Muller pair per
 // thread, shared by the mirrored agents.
 cudaError_t run_materialize_f32(const ParamDesc& par, long long d, int a0, int a1, float* out,
-                                cudaStream_t stream, double* eps_out = nullptr);
+                                cudaStream_t stream, double* eps_out = nullptr, long long eps_row0 = 0);
 
 // Tensor-core rollout (rollout_tc.cu, precision EVORL_PREC_TC): obs -> W1 -> W2 -> O
 // policies with W2 a multiple of 128; the W2 x W1 layer runs on tcgen05.
@@ -228,10 +232,11 @@ long long oz_block_bytes(const TcPlanOut& plan);
 cudaError_t run_oz_split(const double* cand, const NetDesc& net, const TcPlanOut& plan, int n_agents,
                          unsigned char* blocks, cudaStream_t stream);
 // The OpenES ask of agents [a0, a1) fused with the pre-split, from kept noise
-// rows eps (row-major, d per row): the layer-1 byte-slice blocks (identical to
+// rows eps (row-major, d per row, from row eps_row0 on): the layer-1 byte-slice blocks (identical to
 // run_materialize + run_oz_split), the other parameters into cand, and the
 // fp64 layer-1 row of cand only where it holds a non-finite weight.
 cudaError_t run_oz_ask_split(const ParamDesc& par, const NetDesc& net, const TcPlanOut& po, int a0, int a1,
-                             const double* eps, double* cand, unsigned char* blocks, cudaStream_t stream);
+                             const double* eps, long long eps_row0, double* cand, unsigned char* blocks,
+                             cudaStream_t stream);
 
 }  // namespace evorl_b200

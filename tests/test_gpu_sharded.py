@@ -33,6 +33,10 @@ CFGS = {
     # many row chunks in the tell (384 base rows, d = 133121): sized from the
     # shard span the chunking would be 10 row chunks on one GPU and 12 per rank
     # at world 2 (a different summation order of the search gradient)
+    # the oz team: per-rank noise rows kept ahead (generated beside the rollout)
+    # and the ask fused with the layer-1 pre-split, on each rank's own rows
+    "openes_oz": dict(algo="openes", env="pendulum", fixed_horizon=True, pop=40, hidden=(128, 128),
+                      max_episode_steps=30, fitness_episodes=16, precision="oz"),
     "openes_chunks": dict(algo="openes", env="pendulum", fixed_horizon=True, pop=768, hidden=(256, 512),
                           max_episode_steps=20, vbn_samples=200),
 }
