@@ -514,6 +514,35 @@ def test_tell_from_kept_noise_rows_is_identical(evb):
     assert outs[0] == outs[4]  # oz: materialise + pre-split instead of the fused ask
 
 
+def test_noise_kept_ahead_survives_state_changes(evb):
+    """The next generation's noise rows are generated beside the rollout for
+    the NEXT ask key; a rewound iteration counter (set_counters), a new mean
+    (set_mean) or a new shard between generations must fall back or reuse them
+    correctly: fitness bit-identical to a child process that never keeps noise
+    ahead (EVORL_NO_NOISE_AHEAD=1)."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, paper_2501_15129_b200 as evb\n"
+            "kw = dict(algo='openes', env='pendulum', fixed_horizon=True, pop=24, hidden=(256, 256),\n"
+            "          max_episode_steps=25, fitness_episodes=8, precision='oz')\n"
+            "g = evb.EsWorkflow(evb.EsConfig(**kw)).init((9, 10))\n"
+            "out = []\n"
+            "g.step(); g.step(); out.append(g.fitness())\n"
+            "it, st, ep = g.counters(); g.set_counters(it - 1, st, ep)\n"
+            "g.step(); out.append(g.fitness())\n"
+            "g.set_mean(g.mean() * 0.5); g.step(); out.append(g.fitness())\n"
+            "g.set_shard(1, 2); g.phase_rollout(); a0, a1, _, _ = g.shard_ranges(); out.append(g.fitness()[a0:a1])\n"
+            "print('FIT', np.concatenate(out).tobytes().hex())\n")
+    outs = []
+    for env_kv in ({}, {"EVORL_NO_NOISE_AHEAD": "1"}):
+        env = dict(os.environ)
+        env.update(env_kv)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        outs.append([x.split()[1] for x in r.stdout.decode().splitlines() if x.startswith("FIT ")][-1])
+    assert outs[0] == outs[1]
+
+
 @pytest.mark.parametrize("mirrored", [True, False])
 def test_openes_noise_table_generations_match_oracle(oracle, evb, mirrored):
     """OpenES noise-table mode (proj/src/ec.cpp:50-86): the table (normals of
