@@ -39,6 +39,7 @@
 //     fp64 dot product instead (IEEE propagation and NetFault as the fp64 team).
 #include <algorithm>
 #include <climits>
+#include <cstdint>
 #include <cstring>
 
 #include "rollout.cuh"
@@ -898,8 +899,7 @@ constexpr int OZ_AS_ROWS = 16;  // rows per block: 16 x 16 half-chunks = 256 thr
 template <int S>
 __global__ void __launch_bounds__(256, 2) k_oz_ask_split(const ParamDesc P, long long d, long long w_off1, int W1,
                                                       int W2, int W1p, int C, int a0, int a1, long long r0,
-                                                      const double* __restrict__ eps, long long e0,
-                                                      double* __restrict__ cand,
+                                                      const double* __restrict__ eps, double* __restrict__ cand,
                                                       unsigned char* __restrict__ blocks, long long block_bytes) {
   __shared__ double smax[16][OZ_AS_ROWS];
   __shared__ int sfin[16][OZ_AS_ROWS];
@@ -917,7 +917,7 @@ __global__ void __launch_bounds__(256, 2) k_oz_ask_split(const ParamDesc P, long
   for (int q = 0; q < 16; ++q) {
     const int k = h * 16 + q;
     const bool v = h < nh && ok && k < W1;
-    e[q] = v ? eps[nr * d + w_off1 + (long long)k * W2 + r - e0] : 0.0;
+    e[q] = v ? eps[nr * d + w_off1 + (long long)k * W2 + r] : 0.0;
   }
   for (int side = 0; side < 2; ++side) {
     const long long a = side == 0 ? nr : (P.mirrored ? nr + P.base : -1);
@@ -967,14 +967,13 @@ __global__ void __launch_bounds__(256, 2) k_oz_ask_split(const ParamDesc P, long
 // The other parameters (outside layer 1) of agents [a0, a1) from the kept
 // noise rows, as k_cand_from_eps.
 __global__ void k_oz_ask_rest(const ParamDesc P, long long d, long long w_off1, long long n_w1, int a0, int a1,
-                              long long r0, long long rows, const double* __restrict__ eps, long long e0,
-                              double* __restrict__ cand) {
+                              long long r0, long long rows, const double* __restrict__ eps, double* __restrict__ cand) {
   const long long rest = d - n_w1;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= rows * rest) return;
   const long long nr = r0 + i / rest, j = i % rest;
   const long long p = j < w_off1 ? j : j + n_w1;
-  const double e = eps[nr * d + p - e0], mp = P.mean[p];
+  const double e = eps[nr * d + p], mp = P.mean[p];
   for (int side = 0; side < 2; ++side) {
     const long long a = side == 0 ? nr : (P.mirrored ? nr + P.base : -1);
     if (a < a0 || a >= a1) continue;
@@ -1005,21 +1004,25 @@ cudaError_t run_oz_ask_split(const ParamDesc& par, const NetDesc& net, const TcP
     }
   }
   if (r0 < eps_row0) return cudaErrorInvalidValue;
-  const long long rows = r1 - r0, e0 = eps_row0 * net.d;
+  const long long rows = r1 - r0;
+  // the kernels index eps by the global row: address of (virtual) row 0
+  // (integer arithmetic: only rows >= eps_row0 are ever read)
+  eps = reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(eps) -
+                                        (uintptr_t)(eps_row0 * net.d) * sizeof(double));
   const long long n_w1 = (long long)p.W1 * p.W2;
   const long long bb = oz_block_bytes(po);
   k_oz_ask_rest<<<(unsigned)((rows * (net.d - n_w1) + 255) / 256), 256, 0, stream>>>(
-      par, net.d, net.w_off[1], n_w1, a0, a1, r0, rows, eps, e0, cand);
+      par, net.d, net.w_off[1], n_w1, a0, a1, r0, rows, eps, cand);
   const unsigned grid = (unsigned)(rows * p.C * (OZ_M / OZ_AS_ROWS));
 #ifdef EVB_OZ_S5
   if (p.S == 5) {
     k_oz_ask_split<5><<<grid, 16 * OZ_AS_ROWS, 0, stream>>>(par, net.d, net.w_off[1], p.W1, p.W2, p.W1p, p.C, a0,
-                                                            a1, r0, eps, e0, cand, blocks, bb);
+                                                            a1, r0, eps, cand, blocks, bb);
     return cudaGetLastError();
   }
 #endif
   k_oz_ask_split<6><<<grid, 16 * OZ_AS_ROWS, 0, stream>>>(par, net.d, net.w_off[1], p.W1, p.W2, p.W1p, p.C, a0,
-                                                          a1, r0, eps, e0, cand, blocks, bb);
+                                                          a1, r0, eps, cand, blocks, bb);
   return cudaGetLastError();
 }
 
