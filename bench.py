@@ -376,18 +376,15 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            es.set_mean(mean_h)
-            es.set_adam(m_h, v_h, t_h)
-            es.step()
-            mean_h = es.mean()
-            m_h, v_h, t_h = es.adam()
+            mean_h, m_h, v_h, t_h, _ = es.step_host(mean_h, m_h, v_h, t_h)
             e1.record()
             barrier()
             ets.append(e0.elapsed_time(e1))
         e2e = {"value": env_steps_per_gen * len(ets) / (sum(ets) / 1e3), "unit": "env-steps/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "generations_per_sec": len(ets) / (sum(ets) / 1e3),
-               "path": "C ABI evorl_es_set_mean/set_adam -> evorl_es_step -> get_mean/get_adam"}
+               "path": "C ABI evorl_es_step_host: host EsState (mean, Adam m/v/t) in, generation, updated "
+                       "state + StepMetrics out"}
 
     # ---- roofline of the dominant kernel (the fused rollout)
     roll_ms = statistics.mean(roll) if roll else None

@@ -232,6 +232,13 @@ int64_t evorl_es_dim(const evorl_es* es);
 int evorl_es_init(evorl_es* es, uint64_t key_hi, uint64_t key_lo);
 /* Workflow::step: one full generation on the device. */
 int evorl_es_step(evorl_es* es, evorl_step_metrics* out);
+/* Workflow::step with a host-resident EsState (the reference's layout): uploads
+ * mean (and the Adam moments m, v and step count t -- pass NULL for m_in/v_in
+ * to keep the device's), runs the generation, downloads the updated state
+ * (NULL outputs are skipped); one synchronisation, staged through pinned
+ * memory.  Unsharded handles only. */
+int evorl_es_step_host(evorl_es* es, const double* mean_in, const double* m_in, const double* v_in, int64_t t_in,
+                       double* mean_out, double* m_out, double* v_out, int64_t* t_out, evorl_step_metrics* out);
 /* Workflow::evaluate (centre evaluation, proj/src/workflow.cpp:103-129) */
 int evorl_es_evaluate(evorl_es* es, int32_t episodes, uint64_t key_hi, uint64_t key_lo,
                       double* mean_return, double* return_std);

@@ -207,6 +207,8 @@ struct evorl_es {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_noise = nullptr;
   int n_sms = 0;
+  // evorl_es_step_host: pinned staging of the host-resident state (3 d + 1)
+  double* h_stage = nullptr;
   cudaStream_t stream = nullptr;
   // WorkflowState (proj/include/evorl/workflow.hpp:31-36)
   DKey rng{};
@@ -307,6 +309,7 @@ static void free_all(evorl_es* s) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
+  if (s->h_stage) cudaFreeHost(s->h_stage);
   for (cudaEvent_t ev : {s->ev_r0, s->ev_r1, s->ev_s0, s->ev_s1, s->ev_a0, s->ev_a1, s->ev_noise})
     if (ev) cudaEventDestroy(ev);
   void* cm[] = {s->cma.d_w, s->cma.dev.C, s->cma.dev.B, s->cma.dev.D, s->cma.dev.ps, s->cma.dev.pc,
@@ -1206,6 +1209,49 @@ extern "C" int evorl_es_step(evorl_es* s, evorl_step_metrics* out) {
   int rc = evorl_es_phase_rollout(s);
   if (rc) return rc;
   return evorl_es_phase_tell(s, out);
+}
+
+// Workflow::step with the EsState on the host (the reference's own layout:
+// mean and the Adam moments live with the caller): the state is staged through
+// pinned memory and copied with stream-ordered async copies around the two
+// phases, one synchronisation at the end instead of one per transfer call.
+extern "C" int evorl_es_step_host(evorl_es* s, const double* mean_in, const double* m_in, const double* v_in,
+                                  int64_t t_in, double* mean_out, double* m_out, double* v_out, int64_t* t_out,
+                                  evorl_step_metrics* out) {
+  if (s->world != 1) return set_err(EVORL_E_INVALID_ARGUMENT, "sharded handle: use the phase API");
+  if (!mean_in || !mean_out) return set_err(EVORL_E_INVALID_ARGUMENT, "step_host: mean buffers are required");
+  if ((m_in == nullptr) != (v_in == nullptr))
+    return set_err(EVORL_E_INVALID_ARGUMENT, "step_host: the Adam moments come as a pair");
+  CK(cudaSetDevice(s->cfg.device));
+  const size_t d = (size_t)s->d;
+  if (!s->h_stage) CK(cudaMallocHost((void**)&s->h_stage, sizeof(double) * (3 * d + 1)));
+  double* st = s->h_stage;
+  long long* st_t = reinterpret_cast<long long*>(st + 3 * d);
+  std::memcpy(st, mean_in, sizeof(double) * d);
+  CK(cudaMemcpyAsync(s->d_mean, st, sizeof(double) * d, cudaMemcpyHostToDevice, s->stream));
+  if (m_in) {
+    std::memcpy(st + d, m_in, sizeof(double) * d);
+    std::memcpy(st + 2 * d, v_in, sizeof(double) * d);
+    *st_t = t_in;
+    CK(cudaMemcpyAsync(s->d_m, st + d, sizeof(double) * d, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->d_v, st + 2 * d, sizeof(double) * d, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->d_t, st_t, sizeof(long long), cudaMemcpyHostToDevice, s->stream));
+    s->adam_t_host = t_in;
+  }
+  if (int rc = evorl_es_phase_rollout(s)) return rc;  // (both phases order after the copies on the stream)
+  if (int rc = evorl_es_phase_tell(s, out)) return rc;
+  CK(cudaMemcpyAsync(st, s->d_mean, sizeof(double) * d, cudaMemcpyDeviceToHost, s->stream));
+  if (m_out || v_out || t_out) {
+    CK(cudaMemcpyAsync(st + d, s->d_m, sizeof(double) * d, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(st + 2 * d, s->d_v, sizeof(double) * d, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(st_t, s->d_t, sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  std::memcpy(mean_out, st, sizeof(double) * d);
+  if (m_out) std::memcpy(m_out, st + d, sizeof(double) * d);
+  if (v_out) std::memcpy(v_out, st + 2 * d, sizeof(double) * d);
+  if (t_out) *t_out = *st_t;
+  return EVORL_OK;
 }
 
 extern "C" int evorl_es_set_shard(evorl_es* s, int32_t rank, int32_t world) {

@@ -158,6 +158,23 @@ class EsWorkflow:
         check(self.L.evorl_es_step(self.h, C.byref(m)))
         return self._metrics(m)
 
+    def step_host(self, mean, m=None, v=None, t: int = 0):
+        """Workflow::step with the state on the host (evorl_es_step_host):
+        returns (mean, m, v, t, metrics) after the generation; m, v None keeps
+        the device's Adam moments."""
+        mean = np.ascontiguousarray(mean, np.float64)
+        if mean.shape != (self.dim,):
+            raise ValueError("step_host: mean size mismatch")
+        mi = vi = None
+        if m is not None:
+            mi, vi = np.ascontiguousarray(m, np.float64), np.ascontiguousarray(v, np.float64)
+        mo, mm, vv, tt = np.empty(self.dim), np.empty(self.dim), np.empty(self.dim), C.c_int64()
+        met = _lib.StepMetricsC()
+        check(self.L.evorl_es_step_host(self.h, _p(mean), _p(mi) if mi is not None else None,
+                                        _p(vi) if vi is not None else None, int(t), _p(mo), _p(mm), _p(vv),
+                                        C.byref(tt), C.byref(met)))
+        return mo, mm, vv, tt.value, self._metrics(met)
+
     def evaluate(self, episodes: int, key) -> tuple[float, float]:
         hi, lo = _key(key)
         mr, sd = C.c_double(), C.c_double()

@@ -514,6 +514,29 @@ def test_tell_from_kept_noise_rows_is_identical(evb):
     assert outs[0] == outs[4]  # oz: materialise + pre-split instead of the fused ask
 
 
+def test_step_host_matches_the_device_state_calls(evb):
+    """evorl_es_step_host (host-resident EsState in, updated state out) is the
+    set_mean / set_adam / step / mean / adam sequence in one call."""
+    kw = dict(algo="openes", env="pendulum", fixed_horizon=True, pop=24, hidden=(64, 64),
+              max_episode_steps=40, fitness_episodes=4)
+    a = evb.EsWorkflow(evb.EsConfig(**kw)).init((3, 4))
+    b = evb.EsWorkflow(evb.EsConfig(**kw)).init((3, 4))
+    mean = a.mean()
+    m, v, t = a.adam()
+    for _ in range(3):
+        mean2, m2, v2, t2, met = a.step_host(mean, m, v, t)
+        b.set_mean(mean)
+        b.set_adam(m, v, t)
+        metb = b.step()
+        assert np.array_equal(mean2, b.mean())
+        mb, vb, tb = b.adam()
+        assert np.array_equal(m2, mb) and np.array_equal(v2, vb) and t2 == tb == t + 1
+        assert met["fitness/mean"] == metb["fitness/mean"]
+        mean, m, v, t = mean2 * 0.999, m2, v2, t2  # the caller may edit its state between steps
+    _, _, _, _, met = a.step_host(mean)  # moments kept on the device
+    assert np.isfinite(met["fitness/mean"])
+
+
 def test_noise_kept_ahead_survives_state_changes(evb):
     """The next generation's noise rows are generated beside the rollout for
     the NEXT ask key; a rewound iteration counter (set_counters), a new mean
