@@ -364,8 +364,12 @@ def main():
     e2e = None
     if world == 1 and not args.no_e2e:
         d = es.dim
-        mean_h = np.ascontiguousarray(es.mean())
-        m_h, v_h, t_h = es.adam()
+        # the host-resident EsState in page-locked buffers (updated in place)
+        mean_h, m_h, v_h = (evb.pinned_empty(es.dim) for _ in range(3))
+        mean_h[:] = es.mean()
+        m0, v0, t_h = es.adam()
+        m_h[:] = m0
+        v_h[:] = v0
         h2d = 3 * d * 8 + 8
         d2h = 3 * d * 8 + 8 + 5 * 8
         barrier()
@@ -376,15 +380,15 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            mean_h, m_h, v_h, t_h, _ = es.step_host(mean_h, m_h, v_h, t_h)
+            _, _, _, t_h, _ = es.step_host(mean_h, m_h, v_h, t_h, out=(mean_h, m_h, v_h))
             e1.record()
             barrier()
             ets.append(e0.elapsed_time(e1))
         e2e = {"value": env_steps_per_gen * len(ets) / (sum(ets) / 1e3), "unit": "env-steps/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "generations_per_sec": len(ets) / (sum(ets) / 1e3),
-               "path": "C ABI evorl_es_step_host: host EsState (mean, Adam m/v/t) in, generation, updated "
-                       "state + StepMetrics out"}
+               "path": "C ABI evorl_es_step_host: host EsState (mean, Adam m/v/t, page-locked buffers) in, "
+                       "generation, updated state + StepMetrics out"}
 
     # ---- roofline of the dominant kernel (the fused rollout)
     roll_ms = statistics.mean(roll) if roll else None

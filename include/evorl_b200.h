@@ -239,6 +239,10 @@ int evorl_es_step(evorl_es* es, evorl_step_metrics* out);
  * memory.  Unsharded handles only. */
 int evorl_es_step_host(evorl_es* es, const double* mean_in, const double* m_in, const double* v_in, int64_t t_in,
                        double* mean_out, double* m_out, double* v_out, int64_t* t_out, evorl_step_metrics* out);
+/* Page-locked host buffers: evorl_es_step_host copies them with the DMA engines
+ * directly (no staging copy); in and out may be the same buffer. */
+int evorl_host_alloc(int64_t bytes, void** out);
+void evorl_host_free(void* p);
 /* Workflow::evaluate (centre evaluation, proj/src/workflow.cpp:103-129) */
 int evorl_es_evaluate(evorl_es* es, int32_t episodes, uint64_t key_hi, uint64_t key_lo,
                       double* mean_return, double* return_std);

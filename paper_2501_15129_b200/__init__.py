@@ -8,13 +8,13 @@ from ._lib import (CheckpointError, ConfigError, DeviceError, EnvFault, EvorlErr
                    InvalidArgument, LengthError, MissingExtension, NetFault, Unsupported)
 from .es import (CmaEs, EsConfig, EsWorkflow, StepMetrics, ars_ask, ars_tell, batched_rollout,
                  centered_ranks, env_step_batch, gaussian_matrix, measure_fp64_peak, measure_noise_rate,
-                 mlp_desc, openes_ask, openes_tell, param_count, rank_desc, stream_words, sym_eig,
-                 threefry2x64)
+                 mlp_desc, openes_ask, openes_tell, param_count, pinned_empty, rank_desc, stream_words,
+                 sym_eig, threefry2x64)
 
 __all__ = [
     "ConfigError", "DeviceError", "EnvFault", "EvorlError", "InvalidArgument", "LengthError",
     "MissingExtension", "NetFault", "Unsupported", "CheckpointError", "CmaEs", "EsConfig", "EsWorkflow", "StepMetrics",
     "ars_ask", "ars_tell", "batched_rollout", "centered_ranks", "env_step_batch",
     "gaussian_matrix", "measure_fp64_peak", "measure_noise_rate", "mlp_desc", "openes_ask", "openes_tell",
-    "param_count", "rank_desc", "stream_words", "sym_eig", "threefry2x64",
+    "param_count", "pinned_empty", "rank_desc", "stream_words", "sym_eig", "threefry2x64",
 ]

@@ -133,7 +133,7 @@ EXPORTS = [
     "evorl_es_set_obs_norm", "evorl_es_set_counters", "evorl_es_set_shard",
     "evorl_es_shard_ranges", "evorl_es_phase_rollout", "evorl_es_phase_tell",
     "evorl_es_device_buffers", "evorl_es_stream", "evorl_es_last_timings", "evorl_es_last_ask_ms",
-    "evorl_es_step_host",
+    "evorl_es_step_host", "evorl_host_alloc", "evorl_host_free",
     "evorl_measure_fp64_peak", "evorl_measure_dmma_peak", "evorl_measure_noise_rate", "evorl_es_cma_get", "evorl_es_cma_set",
     "evorl_sym_eig", "evorl_es_save", "evorl_es_load", "evorl_batched_rollout_transitions",
     "evorl_cma_create", "evorl_cma_ask", "evorl_cma_tell", "evorl_es_device_var",
@@ -210,6 +210,9 @@ def load() -> C.CDLL:
     L.evorl_es_last_timings.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]
     L.evorl_es_last_ask_ms.argtypes = [vp, C.POINTER(C.c_float)]
     L.evorl_es_step_host.argtypes = [vp, vp, vp, vp, C.c_int64, vp, vp, vp, C.POINTER(C.c_int64), vp]
+    L.evorl_host_alloc.argtypes = [C.c_int64, C.POINTER(vp)]
+    L.evorl_host_free.argtypes = [vp]
+    L.evorl_host_free.restype = None
     L.evorl_measure_fp64_peak.argtypes = [C.POINTER(dbl)]
     L.evorl_measure_noise_rate.argtypes = [C.c_int64, C.POINTER(C.c_float)]
     L.evorl_measure_dmma_peak.argtypes = [C.POINTER(dbl)]

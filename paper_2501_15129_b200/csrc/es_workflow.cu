@@ -1225,33 +1225,60 @@ extern "C" int evorl_es_step_host(evorl_es* s, const double* mean_in, const doub
   CK(cudaSetDevice(s->cfg.device));
   const size_t d = (size_t)s->d;
   if (!s->h_stage) CK(cudaMallocHost((void**)&s->h_stage, sizeof(double) * (3 * d + 1)));
-  double* st = s->h_stage;
-  long long* st_t = reinterpret_cast<long long*>(st + 3 * d);
-  std::memcpy(st, mean_in, sizeof(double) * d);
-  CK(cudaMemcpyAsync(s->d_mean, st, sizeof(double) * d, cudaMemcpyHostToDevice, s->stream));
+  long long* st_t = reinterpret_cast<long long*>(s->h_stage + 3 * d);
+  // a caller buffer in page-locked memory (evorl_host_alloc) is copied directly
+  // by the DMA engines; a pageable one goes through the handle's pinned stage
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes a{};
+    const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  auto up = [&](double* dev, const double* host, size_t k) -> cudaError_t {
+    const double* src = host;
+    if (!pinned(host)) {
+      std::memcpy(s->h_stage + k * d, host, sizeof(double) * d);
+      src = s->h_stage + k * d;
+    }
+    return cudaMemcpyAsync(dev, src, sizeof(double) * d, cudaMemcpyHostToDevice, s->stream);
+  };
+  double* direct[3] = {nullptr, nullptr, nullptr};  // outputs written by DMA in place
+  auto down = [&](double* host, const double* dev, size_t k) -> cudaError_t {
+    double* dst = pinned(host) ? host : s->h_stage + k * d;
+    if (dst == host) direct[k] = host;
+    return cudaMemcpyAsync(dst, dev, sizeof(double) * d, cudaMemcpyDeviceToHost, s->stream);
+  };
+  CK(up(s->d_mean, mean_in, 0));
   if (m_in) {
-    std::memcpy(st + d, m_in, sizeof(double) * d);
-    std::memcpy(st + 2 * d, v_in, sizeof(double) * d);
+    CK(up(s->d_m, m_in, 1));
+    CK(up(s->d_v, v_in, 2));
     *st_t = t_in;
-    CK(cudaMemcpyAsync(s->d_m, st + d, sizeof(double) * d, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemcpyAsync(s->d_v, st + 2 * d, sizeof(double) * d, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(s->d_t, st_t, sizeof(long long), cudaMemcpyHostToDevice, s->stream));
     s->adam_t_host = t_in;
   }
   if (int rc = evorl_es_phase_rollout(s)) return rc;  // (both phases order after the copies on the stream)
   if (int rc = evorl_es_phase_tell(s, out)) return rc;
-  CK(cudaMemcpyAsync(st, s->d_mean, sizeof(double) * d, cudaMemcpyDeviceToHost, s->stream));
-  if (m_out || v_out || t_out) {
-    CK(cudaMemcpyAsync(st + d, s->d_m, sizeof(double) * d, cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaMemcpyAsync(st + 2 * d, s->d_v, sizeof(double) * d, cudaMemcpyDeviceToHost, s->stream));
-    CK(cudaMemcpyAsync(st_t, s->d_t, sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
-  }
+  CK(down(mean_out, s->d_mean, 0));
+  if (m_out) CK(down(m_out, s->d_m, 1));
+  if (v_out) CK(down(v_out, s->d_v, 2));
+  if (t_out) CK(cudaMemcpyAsync(st_t, s->d_t, sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
-  std::memcpy(mean_out, st, sizeof(double) * d);
-  if (m_out) std::memcpy(m_out, st + d, sizeof(double) * d);
-  if (v_out) std::memcpy(v_out, st + 2 * d, sizeof(double) * d);
+  if (!direct[0]) std::memcpy(mean_out, s->h_stage, sizeof(double) * d);
+  if (m_out && !direct[1]) std::memcpy(m_out, s->h_stage + d, sizeof(double) * d);
+  if (v_out && !direct[2]) std::memcpy(v_out, s->h_stage + 2 * d, sizeof(double) * d);
   if (t_out) *t_out = *st_t;
   return EVORL_OK;
+}
+
+// Page-locked host memory for the host-state calls (freed by evorl_host_free).
+extern "C" int evorl_host_alloc(int64_t bytes, void** out) {
+  *out = nullptr;
+  if (bytes <= 0) return set_err(EVORL_E_INVALID_ARGUMENT, "host_alloc: bytes must be positive");
+  CK(cudaMallocHost(out, (size_t)bytes));
+  return EVORL_OK;
+}
+extern "C" void evorl_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 extern "C" int evorl_es_set_shard(evorl_es* s, int32_t rank, int32_t world) {

@@ -27,7 +27,7 @@ from ._lib import check
 __all__ = ["EsConfig", "EsWorkflow", "StepMetrics", "batched_rollout", "gaussian_matrix",
            "centered_ranks", "rank_desc", "openes_ask", "openes_tell", "ars_ask", "ars_tell",
            "env_step_batch", "threefry2x64", "stream_words", "param_count", "mlp_desc",
-           "measure_fp64_peak", "measure_noise_rate", "sym_eig"]
+           "measure_fp64_peak", "measure_noise_rate", "pinned_empty", "sym_eig"]
 
 
 def _p(a: np.ndarray):
@@ -158,17 +158,26 @@ class EsWorkflow:
         check(self.L.evorl_es_step(self.h, C.byref(m)))
         return self._metrics(m)
 
-    def step_host(self, mean, m=None, v=None, t: int = 0):
+    def step_host(self, mean, m=None, v=None, t: int = 0, out=None):
         """Workflow::step with the state on the host (evorl_es_step_host):
         returns (mean, m, v, t, metrics) after the generation; m, v None keeps
-        the device's Adam moments."""
+        the device's Adam moments.  `out` = three float64 arrays of length dim
+        to write the state into (they may be the inputs; page-locked ones from
+        pinned_empty() are copied by DMA directly)."""
         mean = np.ascontiguousarray(mean, np.float64)
         if mean.shape != (self.dim,):
             raise ValueError("step_host: mean size mismatch")
         mi = vi = None
         if m is not None:
             mi, vi = np.ascontiguousarray(m, np.float64), np.ascontiguousarray(v, np.float64)
-        mo, mm, vv, tt = np.empty(self.dim), np.empty(self.dim), np.empty(self.dim), C.c_int64()
+        if out is None:
+            mo, mm, vv = np.empty(self.dim), np.empty(self.dim), np.empty(self.dim)
+        else:
+            mo, mm, vv = out
+            for a in out:
+                if a.dtype != np.float64 or a.shape != (self.dim,) or not a.flags.c_contiguous:
+                    raise ValueError("step_host: out arrays must be contiguous float64 of length dim")
+        tt = C.c_int64()
         met = _lib.StepMetricsC()
         check(self.L.evorl_es_step_host(self.h, _p(mean), _p(mi) if mi is not None else None,
                                         _p(vi) if vi is not None else None, int(t), _p(mo), _p(mm), _p(vv),
@@ -599,6 +608,18 @@ def sym_eig(A):
     sw = C.c_int32()
     check(_lib.load().evorl_sym_eig(_p(A), n, _p(ev), _p(V), C.byref(sw)))
     return ev, V, sw.value
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """A float64 array of n entries in page-locked host memory
+    (evorl_host_alloc; freed with the array)."""
+    import weakref
+    L = _lib.load()
+    p = C.c_void_p()
+    check(L.evorl_host_alloc(int(n) * 8, C.byref(p)))
+    buf = (C.c_double * int(n)).from_address(p.value)
+    weakref.finalize(buf, L.evorl_host_free, p.value)
+    return np.frombuffer(buf, dtype=np.float64)
 
 
 def measure_noise_rate(n: int = 1 << 27) -> float:

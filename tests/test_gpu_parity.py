@@ -535,6 +535,19 @@ def test_step_host_matches_the_device_state_calls(evb):
         mean, m, v, t = mean2 * 0.999, m2, v2, t2  # the caller may edit its state between steps
     _, _, _, _, met = a.step_host(mean)  # moments kept on the device
     assert np.isfinite(met["fitness/mean"])
+    # page-locked state buffers, updated in place, give the same generations
+    c = evb.EsWorkflow(evb.EsConfig(**kw)).init((3, 4))
+    d = evb.EsWorkflow(evb.EsConfig(**kw)).init((3, 4))
+    pm, pmm, pv = (evb.pinned_empty(c.dim) for _ in range(3))
+    pm[:] = c.mean()
+    m0, v0, t = c.adam()
+    pmm[:] = m0
+    pv[:] = v0
+    mean, m, v = pm.copy(), m0.copy(), v0.copy()
+    for _ in range(2):
+        _, _, _, t, _ = c.step_host(pm, pmm, pv, t, out=(pm, pmm, pv))
+        mean, m, v, _, _ = d.step_host(mean, m, v, t - 1)
+        assert np.array_equal(pm, mean) and np.array_equal(pmm, m) and np.array_equal(pv, v)
 
 
 def test_noise_kept_ahead_survives_state_changes(evb):
