@@ -161,7 +161,16 @@ def test_oz_config3_ranks_match_fp64_path(evb):
     # CMA-ES: candidates from the device ask GEMM, no pre-split blocks (in-kernel slicing)
     dict(algo="cmaes", env="pendulum", fixed_horizon=True, pop=16, hidden=[16, 128], max_episode_steps=100,
          fitness_episodes=8, vbn_samples=300, cmaes_elites=8, cmaes_sigma0=0.1, cmaes_max_dim=4096),
-], ids=["evaluate", "noise-table", "cmaes"])
+    # VES (SRC_OPENES ask, no kept noise) and CEM (diagonal-variance ask)
+    dict(algo="ves", env="pendulum", fixed_horizon=True, pop=16, hidden=[32, 128], max_episode_steps=100,
+         fitness_episodes=8, vbn_samples=300, ves_elites=4),
+    dict(algo="cem", env="pendulum", fixed_horizon=True, pop=16, hidden=[32, 128], max_episode_steps=100,
+         fitness_episodes=8, cem_elites=4),
+    # OpenES without mirroring (every agent its own noise row, kept ahead) and
+    # with running_stats normalisation (per-lane Welford in the oz env warps)
+    dict(algo="openes", env="pendulum", fixed_horizon=True, pop=12, hidden=[64, 128], max_episode_steps=100,
+         fitness_episodes=8, openes_mirrored=False, obs_norm="running_stats"),
+], ids=["evaluate", "noise-table", "cmaes", "ves", "cem", "openes-unmirrored-rs"])
 def test_oz_other_callers_match_fp64(evb, kw):
     """The oz team behind the workflow's other callers: per-generation fitness
     within RTOL_OZ of the fp64 team from the same state, ranks identical, and
