@@ -204,6 +204,12 @@ struct evorl_es {
   bool eps_next_valid = false, eps_next_failed = false;
   DKey eps_next_key{};
   long long eps_next_r0 = 0, eps_next_r1 = 0;  // rows the kept-ahead buffer holds
+  // coordinate-sharded tell: the noise columns [p0, p1) of every row, generated
+  // beside the previous rollout (cur: this generation's tell; next: being filled)
+  double *d_cols_cur = nullptr, *d_cols_next = nullptr;
+  bool cols_cur_valid = false, cols_next_valid = false, cols_failed = false;
+  DKey cols_cur_key{}, cols_next_key{};
+  long long cols_cur_p0 = 0, cols_cur_p1 = 0, cols_next_p0 = 0, cols_next_p1 = 0;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_noise = nullptr;
   int n_sms = 0;
@@ -305,7 +311,7 @@ static void free_all(evorl_es* s) {
                   s->d_order, s->d_elite_idx, s->d_shaped, s->d_scores, s->d_elite_diff, s->d_metrics,
                   s->d_sel, s->d_steps, s->d_fault, s->d_adam_bc, s->d_ves_w, s->d_cand,
                   s->d_cand_f32, s->d_tell_part, s->d_table, s->d_offsets, s->d_tc_blocks, s->d_eps_rows,
-                  s->d_eps_next};
+                  s->d_eps_next, s->d_cols_cur, s->d_cols_next};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->h) cudaFreeHost(s->h);
@@ -989,6 +995,29 @@ extern "C" int evorl_es_phase_rollout(evorl_es* s) {
     }
     // the tell reads the kept rows only when they are every row (unsharded)
     s->eps_rows_valid = er != nullptr && s->a1 > s->a0 && r0 == 0 && r1 == rows_of(s);
+    if (er && s->world > 1 && s->p1 > s->p0 && s->a1 > s->a0 && eps_next_buffer(s) && !s->cols_failed) {
+      // the next generation's tell noise (every row, this rank's coordinates)
+      const long long span = s->p1 - s->p0, cap = rows_of(s) * ((s->d + s->world - 1) / s->world);
+      if (!s->d_cols_next) {
+        bool ok = cudaMalloc((void**)&s->d_cols_next, sizeof(double) * (size_t)cap) == cudaSuccess;
+        ok = ok && cudaMalloc((void**)&s->d_cols_cur, sizeof(double) * (size_t)cap) == cudaSuccess;
+        if (!ok) {
+          cudaGetLastError();
+          s->cols_failed = true;
+        }
+      }
+      if (!s->cols_failed && rows_of(s) * span <= cap) {
+        const DKey next = fold_in(fold_in(fold_in(s->rng, 0), (uint64_t)(s->iteration + 1)), 0);
+        CK(cudaStreamWaitEvent(s->side, s->ev_r0, 0));
+        CK(run_noise_cols(next, s->d, s->p0, s->p1, rows_of(s), s->d_cols_next, s->n_sms, s->side));
+        CK(cudaEventRecord(s->ev_noise, s->side));
+        count_launch();
+        s->cols_next_valid = true;
+        s->cols_next_key = next;
+        s->cols_next_p0 = s->p0;
+        s->cols_next_p1 = s->p1;
+      }
+    }
     if (er && whole && s->a1 > s->a0) {
       if (double* nx = eps_next_buffer(s)) {  // the next generation's noise, beside this rollout
         const DKey next = fold_in(fold_in(fold_in(s->rng, 0), (uint64_t)(s->iteration + 1)), 0);
@@ -1062,7 +1091,16 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       t.table = s->d_table;
       t.offsets = s->d_offsets;
       t.eps_rows = s->eps_rows_valid ? s->d_eps_rows : nullptr;
+      t.eps_ld = s->d;
+      t.eps_p0 = 0;
       s->eps_rows_valid = false;
+      if (!t.eps_rows && !t.table && s->cols_cur_valid && s->cols_cur_key.hi == s->ask_key.hi &&
+          s->cols_cur_key.lo == s->ask_key.lo && s->cols_cur_p0 == s->p0 && s->cols_cur_p1 == s->p1) {
+        CK(cudaStreamWaitEvent(st, s->ev_noise, 0));  // the side stream filled them beside the last rollout
+        t.eps_rows = s->d_cols_cur;
+        t.eps_ld = s->p1 - s->p0;
+        t.eps_p0 = s->p0;
+      }
       {
         const long long need = (long long)openes_tell_chunks(t.base, s->d) * (s->p1 - s->p0);
         if (need > s->tell_part_cap) {
@@ -1075,6 +1113,13 @@ extern "C" int evorl_es_phase_tell(evorl_es* s, evorl_step_metrics* out) {
       }
       t.partial = s->d_tell_part;
       CK(run_openes_tell(t, st));
+      // the columns filled beside this generation's rollout serve the next tell
+      std::swap(s->d_cols_cur, s->d_cols_next);
+      s->cols_cur_valid = s->cols_next_valid;
+      s->cols_cur_key = s->cols_next_key;
+      s->cols_cur_p0 = s->cols_next_p0;
+      s->cols_cur_p1 = s->cols_next_p1;
+      s->cols_next_valid = false;
       CK(run_inc_counter(s->d_t, st));
       s->adam_t_host += 1;
       sigma = s->cfg.openes_sigma;

@@ -395,18 +395,19 @@ __global__ void __launch_bounds__(TELL_T) k_openes_tell_rows(const OpenEsTellArg
     }
     __syncthreads();
     if (p < a.p1) {
-      const double* col = a.eps_rows + (long long)i0 * a.d + p;
+      const long long ld = a.eps_ld;
+      const double* col = a.eps_rows + (long long)i0 * ld + (p - a.eps_p0);
       int q = 0;
       for (; q + 4 <= lim; q += 4) {  // four rows' loads in flight
-        const double e0 = __ldcs(col), e1 = __ldcs(col + a.d), e2 = __ldcs(col + 2 * a.d),
-                     e3 = __ldcs(col + 3 * a.d);
+        const double e0 = __ldcs(col), e1 = __ldcs(col + ld), e2 = __ldcs(col + 2 * ld),
+                     e3 = __ldcs(col + 3 * ld);
         acc = fma(e0, wsh[q], acc);
         acc = fma(e1, wsh[q + 1], acc);
         acc = fma(e2, wsh[q + 2], acc);
         acc = fma(e3, wsh[q + 3], acc);
-        col += 4 * a.d;
+        col += 4 * ld;
       }
-      for (; q < lim; ++q, col += a.d) acc = fma(__ldcs(col), wsh[q], acc);
+      for (; q < lim; ++q, col += ld) acc = fma(__ldcs(col), wsh[q], acc);
     }
   }
   if (p >= a.p1) return;

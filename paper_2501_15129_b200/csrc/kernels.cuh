@@ -53,7 +53,8 @@ struct OpenEsTellArgs {
   double* partial;          // scratch: openes_tell_chunks(...) x (p1 - p0) doubles
   const double* table;      // noise-table mode: eps_i[p] = table[offsets[i] + p] (else regenerated)
   const long long* offsets;
-  const double* eps_rows;   // optional: eps_i[p] = eps_rows[i * d + p], kept by this generation's ask
+  const double* eps_rows;   // optional: eps_i[p] = eps_rows[i * eps_ld + p - eps_p0], kept by the ask
+  long long eps_ld, eps_p0; // (unsharded: the ask's rows, ld = d, p0 = 0; sharded: this rank's columns)
 };
 // Row chunks of the tell's noise contraction for a coordinate span (so the
 // grid fills the GPU; the chunk partials are summed in a fixed order).

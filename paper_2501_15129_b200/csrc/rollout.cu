@@ -217,6 +217,33 @@ cudaError_t run_noise_rows(DKey key, long long t0, long long n, double* eps, int
   return cudaGetLastError();
 }
 
+// The noise a coordinate-sharded tell reads: entries (row, p) of rows
+// [0, rows) and columns [p0, p1) into out[row (p1 - p0) + p - p0].  Thread
+// (row, j) computes Box-Muller pair j of the row's column range (pairs are
+// aligned to the stream, so the range's end pairs are half used).
+__global__ void __launch_bounds__(NOISE_T) k_noise_cols(DKey key, long long d, long long p0, long long p1,
+                                                        long long rows, double* __restrict__ out) {
+  const long long span = p1 - p0, per_row = span / 2 + 2;
+  const long long stride = (long long)gridDim.x * NOISE_T;
+  for (long long i = blockIdx.x * (long long)NOISE_T + threadIdx.x; i < rows * per_row; i += stride) {
+    const long long row = i / per_row, j = i - row * per_row;
+    const long long t0 = row * d + p0, t1 = row * d + p1;
+    const long long b = (t0 >> 1) + j;
+    if (2 * b >= t1) continue;
+    double c, sn;
+    normal_pair(key, (uint64_t)b, c, sn);
+    double* o = out + row * span;
+    if (2 * b >= t0) o[2 * b - t0] = c;
+    if (2 * b + 1 < t1) o[2 * b + 1 - t0] = sn;
+  }
+}
+cudaError_t run_noise_cols(DKey key, long long d, long long p0, long long p1, long long rows, double* out,
+                           int blocks, cudaStream_t stream) {
+  if (rows <= 0 || p1 <= p0) return cudaSuccess;
+  k_noise_cols<<<(unsigned)std::max(1, blocks), NOISE_T, 0, stream>>>(key, d, p0, p1, rows, out);
+  return cudaGetLastError();
+}
+
 // The OpenES ask from kept noise rows: entry t = row * d + p of the rows
 // [r0, r1) the agents [a0, a1) use gives candidate p of agent row (and of
 // row + base, negated, when mirrored) -- the values k_materialize_openes

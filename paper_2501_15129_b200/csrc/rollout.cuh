@@ -200,6 +200,10 @@ void openes_row_range(const ParamDesc& par, int a0, int a1, long long* r0, long 
 // such rows, eps holding rows from eps_row0 on (bit-identical to
 // run_materialize / run_materialize_f32 for SRC_OPENES).
 cudaError_t run_noise_rows(DKey key, long long t0, long long n, double* eps, int blocks, cudaStream_t stream);
+// ... and the columns [p0, p1) of rows [0, rows) (a coordinate-sharded tell's
+// noise) into out[row (p1 - p0) + p - p0]
+cudaError_t run_noise_cols(DKey key, long long d, long long p0, long long p1, long long rows, double* out,
+                           int blocks, cudaStream_t stream);
 cudaError_t run_cand_from_eps(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
                               long long eps_row0, double* out, cudaStream_t stream);
 cudaError_t run_cand_from_eps_f32(const ParamDesc& par, long long d, int a0, int a1, const double* eps,
