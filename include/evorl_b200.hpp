@@ -116,6 +116,18 @@ class EsWorkflow {
     check(evorl_es_step(h_.get(), &m));
     return {m.fitness_mean, m.fitness_max, m.fitness_min, m.sigma, m.update_skipped != 0};
   }
+  // Workflow::step with the EsState held by the caller (mean and the Adam
+  // moments, updated in place): one C-ABI call, one synchronisation
+  StepMetrics step_host(std::vector<double>& mean, std::vector<double>& m, std::vector<double>& v,
+                        std::int64_t& t) {
+    const std::size_t d = (std::size_t)dim();
+    if (mean.size() != d || m.size() != d || v.size() != d)
+      throw std::invalid_argument("step_host: size mismatch");
+    evorl_step_metrics met{};
+    check(evorl_es_step_host(h_.get(), mean.data(), m.data(), v.data(), t, mean.data(), m.data(), v.data(), &t,
+                             &met));
+    return {met.fitness_mean, met.fitness_max, met.fitness_min, met.sigma, met.update_skipped != 0};
+  }
   EvalReport evaluate(int episodes, RngKey key) {
     EvalReport r;
     check(evorl_es_evaluate(h_.get(), episodes, key.hi, key.lo, &r.mean_return, &r.return_std));
