@@ -744,8 +744,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) rollout_ozp_kernel(const __gri
             h[q] = zz > 0.0 ? zz : 0.0;  // ReLU (NaN -> 0, as cwiseMax)
             if (h[q] == INFINITY) bad |= 1u << (half * 4 + q);
           }
-          bad = __reduce_or_sync(0xffffffffu, bad);
-          if (lane < OZP_G && ((bad >> lane) & 1u)) bad1[g * OZP_G + lane] = (uint32_t)it + 1u;
+          if (__any_sync(0xffffffffu, bad != 0u)) {  // (rare: an infinite layer-1 activation)
+            bad = __reduce_or_sync(0xffffffffu, bad);
+            if (lane < OZP_G && ((bad >> lane) & 1u)) bad1[g * OZP_G + lane] = (uint32_t)it + 1u;
+          }
           // output layer: v[q] = w2[row][o] h[q] summed over the warp's 32 rows by a
           // reduce-scatter (lane bits 4, 3 select the lane q it ends on)
           const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
