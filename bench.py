@@ -344,10 +344,12 @@ def main():
         if dist is not None:
             dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         args.ask_ms = statistics.mean(ask) if ask and min(ask) > 0 else None
+        args.step_fn = step
         return cfg, es, float(tot.item()), roll, launches
 
     clk = ClockSampler(local)
     cfg, es, max_ms, roll, launches = timed_generations(args.precision, clk)
+    step_fn = args.step_fn
     ask_ms = args.ask_ms
 
     pop, e, H = cfg.pop, cfg.fitness_episodes, cfg.max_episode_steps
@@ -389,6 +391,44 @@ def main():
                "generations_per_sec": len(ets) / (sum(ets) / 1e3),
                "path": "C ABI evorl_es_step_host: host EsState (mean, Adam m/v/t, page-locked buffers) in, "
                        "generation, updated state + StepMetrics out"}
+    elif world > 1 and not args.no_e2e:
+        # sharded: every rank uploads the (replicated) host EsState, runs the
+        # sharded generation (CudaShardedEs.step: both collectives) and reads the
+        # updated state back; max over ranks
+        d = es.dim
+        mean_h, m_h, v_h = (evb.pinned_empty(d) for _ in range(3))
+        mean_h[:] = es.mean()
+        m0, v0, t_h = es.adam()
+        m_h[:] = m0
+        v_h[:] = v0
+        h2d = 3 * d * 8 + 8
+        d2h = 3 * d * 8 + 8 + 5 * 8
+        barrier()
+        ets = []
+        for _ in range(max(1, args.steps)):
+            flush.zero_()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            es.set_mean(mean_h)
+            es.set_adam(m_h, v_h, t_h)
+            step_fn()
+            mean_h[:] = es.mean()
+            m1, v1, t_h = es.adam()
+            m_h[:] = m1
+            v_h[:] = v1
+            e1.record()
+            barrier()
+            ets.append(e0.elapsed_time(e1))
+        tot_e = torch.tensor([sum(ets)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tot_e, op=dist.ReduceOp.MAX)
+        e_ms = float(tot_e.item())
+        e2e = {"value": env_steps_per_gen * len(ets) / (e_ms / 1e3), "unit": "env-steps/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "generations_per_sec": len(ets) / (e_ms / 1e3),
+               "path": "per rank: C ABI evorl_es_set_mean/set_adam (page-locked host EsState) -> "
+                       "CudaShardedEs.step (NCCL all-gathers) -> get_mean/get_adam; max over ranks"}
 
     # ---- roofline of the dominant kernel (the fused rollout)
     roll_ms = statistics.mean(roll) if roll else None
